@@ -1,0 +1,346 @@
+"""CPU oracle for the modified L-BFGS-B of arXiv 2203.16340 (ctypes wrapper).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` leg may import this
+package.  The product package ``paper_2203_16340_b200`` never imports it and
+the two share no code: this module wraps ``oracle/oracle.c`` (plain C, fp64,
+sequential loops, ``-ffp-contract=off``) and nothing else.
+
+Every function cites the paper passage it follows (``PAPER.md:N``); the
+readings of the paper it takes are listed in DESIGN.md section 3 (R1..R28).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CONVERGED, MAX_ITERS, LINESEARCH_FAILURE, AL_MAX_OUTER, AL_INNER_FAILURE = 0, 1, 2, 3, 4
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (no GPU needed)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+               _SRC, "-o", _LIB + ".tmp", "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _setup(_lib)
+    return _lib
+
+
+_dp = C.POINTER(C.c_double)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class _Lsq(C.Structure):
+    _fields_ = [("m", C.c_int64), ("ncols", C.c_int64), ("lda", C.c_int64),
+                ("M", _dp), ("colscale", _dp), ("split", C.c_int32),
+                ("b", _dp), ("c", _dp), ("delta", C.c_double),
+                ("n_eq", C.c_int32), ("E", _dp), ("e", _dp), ("lam", _dp),
+                ("n_in", C.c_int32), ("G", _dp), ("hv", _dp), ("mu", _dp),
+                ("rho", C.c_double)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("eps", C.c_double), ("c1", C.c_double), ("shrink", C.c_double),
+                ("tol", C.c_double), ("max_backtracks", C.c_int32),
+                ("screen_full_norm", C.c_int32), ("max_iters", C.c_int64)]
+
+
+class _Res(C.Structure):
+    _fields_ = [("f", C.c_double), ("pg_inf", C.c_double), ("gfree_inf", C.c_double),
+                ("iters", C.c_int64), ("n_fg", C.c_int64), ("n_backtracks", C.c_int64),
+                ("n_free", C.c_int64), ("status", C.c_int32), ("last_branch", C.c_int32),
+                ("n_fallbacks", C.c_int64)]
+
+
+class _AlOpts(C.Structure):
+    _fields_ = [("feas_tol", C.c_double), ("rho0", C.c_double), ("rho_factor", C.c_double),
+                ("rho_cap", C.c_double), ("max_outer", C.c_int32)]
+
+
+class _AlRes(C.Structure):
+    _fields_ = [("violation_inf", C.c_double), ("rho", C.c_double), ("f", C.c_double),
+                ("outer_iters", C.c_int64), ("inner_iters_total", C.c_int64),
+                ("status", C.c_int32)]
+
+
+def _setup(L):
+    i64, i32, d = C.c_int64, C.c_int32, C.c_double
+    L.orc_clip.argtypes = [i64, _dp, _dp, _dp, _dp]
+    L.orc_working_set.argtypes = [i64, _dp, _dp, _dp, _dp, d, _u8p]
+    L.orc_masked_dot.argtypes = [i64, _dp, _dp, _u8p]
+    L.orc_masked_dot.restype = d
+    L.orc_matvec.argtypes = [i64, i64, _dp, i64, _dp, _dp]
+    L.orc_matvec_t.argtypes = [i64, i64, _dp, i64, _dp, _dp]
+    L.orc_two_loop.argtypes = [i64, _dp, _u8p, i32, _dp, _dp, d, i32, _dp]
+    L.orc_project_direction.argtypes = [i64, _dp, _dp, _dp, _dp, _dp, d, _dp]
+    L.orc_project_direction.restype = i32
+    L.orc_max_step.argtypes = [i64, _dp, _dp, _dp, _dp]
+    L.orc_max_step.restype = d
+    L.orc_minimize_lsq.argtypes = [C.POINTER(_Lsq), _dp, _dp, i32, C.POINTER(_Opts), _dp,
+                                   C.POINTER(_Res)]
+    L.orc_al_solve.argtypes = [C.POINTER(_Lsq), _dp, _dp, _dp, _dp, i32, C.POINTER(_Opts),
+                               C.POINTER(_AlOpts), _dp, C.POINTER(_AlRes)]
+    L.orc_check_convergence.argtypes = [i64, _dp, _u8p, d]
+    L.orc_check_convergence.restype = i32
+    L.orc_lsq_value.argtypes = [C.POINTER(_Lsq), _dp]
+    L.orc_lsq_value.restype = d
+    L.orc_lsq_grad.argtypes = [C.POINTER(_Lsq), _dp, _dp]
+    L.orc_armijo_scalar_quadratic.argtypes = [d, d, d, d, d, i32]
+    L.orc_armijo_scalar_quadratic.restype = d
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_dp)
+
+
+def _u8(a):
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+# --------------------------------------------------------------------------
+# Elementwise pieces
+# --------------------------------------------------------------------------
+def clip(x, l=None, u=None):
+    """min(max(x, l), u) -- Alg. 2 line 1."""
+    x = _f64(x); l = None if l is None else _f64(l); u = None if u is None else _f64(u)
+    out = np.empty_like(x)
+    _L().orc_clip(x.size, _ptr(x), _ptr(l), _ptr(u), _ptr(out))
+    return out
+
+
+def working_set(x, g, l, u, eps):
+    """Eq. (1).  Returns a bool mask of FREE variables."""
+    x, g = _f64(x), _f64(g)
+    l = None if l is None else _f64(l); u = None if u is None else _f64(u)
+    fr = np.empty(x.size, dtype=np.uint8)
+    _L().orc_working_set(x.size, _ptr(x), _ptr(g), _ptr(l), _ptr(u), eps,
+                         fr.ctypes.data_as(_u8p))
+    return fr.astype(bool)
+
+
+def masked_dot(u, v, free=None):
+    """<u[S], v[S]> (Alg. 3 line 3)."""
+    u, v = _f64(u), _f64(v)
+    fr = None if free is None else _u8(free)
+    return _L().orc_masked_dot(u.size, _ptr(u), _ptr(v),
+                               None if fr is None else fr.ctypes.data_as(_u8p))
+
+
+def matvec(A, x):
+    """A x with A column-major (Fortran-ordered numpy array)."""
+    A = np.asfortranarray(A, dtype=np.float64); x = _f64(x)
+    m, n = A.shape
+    out = np.empty(m)
+    _L().orc_matvec(m, n, _ptr(A), m, _ptr(x), _ptr(out))
+    return out
+
+
+def matvec_t(A, r):
+    """A^T r with A column-major."""
+    A = np.asfortranarray(A, dtype=np.float64); r = _f64(r)
+    m, n = A.shape
+    out = np.empty(n)
+    _L().orc_matvec_t(m, n, _ptr(A), m, _ptr(r), _ptr(out))
+    return out
+
+
+def two_loop(g, free, S=(), Y=(), eps=1e-9, screen_full_norm=False):
+    """Alg. 3 literal; pairs oldest first.  Returns d = -q (R5)."""
+    g = _f64(g); n = g.size
+    fr = _u8(free)
+    nh = len(S)
+    Sm = _f64(np.reshape(S, (nh, n))) if nh else np.zeros((1, n))
+    Ym = _f64(np.reshape(Y, (nh, n))) if nh else np.zeros((1, n))
+    d = np.empty(n)
+    _L().orc_two_loop(n, _ptr(g), fr.ctypes.data_as(_u8p), nh, _ptr(Sm), _ptr(Ym), eps,
+                      int(bool(screen_full_norm)), _ptr(d))
+    return d
+
+
+def project_direction(x, g, d, l, u, eps):
+    """Alg. 2.  Returns (p, projected: bool)."""
+    x, g, d = _f64(x), _f64(g), _f64(d)
+    l = None if l is None else _f64(l); u = None if u is None else _f64(u)
+    p = np.empty_like(x)
+    br = _L().orc_project_direction(x.size, _ptr(x), _ptr(g), _ptr(d), _ptr(l), _ptr(u),
+                                    eps, _ptr(p))
+    return p, bool(br)
+
+
+def max_step(x, p, l, u):
+    """Minimum blocking ratio (R10)."""
+    x, p = _f64(x), _f64(p)
+    l = None if l is None else _f64(l); u = None if u is None else _f64(u)
+    return _L().orc_max_step(x.size, _ptr(x), _ptr(p), _ptr(l), _ptr(u))
+
+
+def check_convergence(g, free, tol):
+    g = _f64(g); fr = _u8(free)
+    return bool(_L().orc_check_convergence(g.size, _ptr(g), fr.ctypes.data_as(_u8p), tol))
+
+
+def armijo_scalar_quadratic(x, p, amax=1.0, c1=1e-4, shrink=0.5, max_bt=50):
+    return _L().orc_armijo_scalar_quadratic(x, p, amax, c1, shrink, max_bt)
+
+
+# --------------------------------------------------------------------------
+# LSQ objective family + Alg. 1 / Alg. 4
+# --------------------------------------------------------------------------
+@dataclass
+class Options:
+    eps: float = 1e-9          # R1
+    c1: float = 1e-4           # R11
+    shrink: float = 0.5        # R11
+    tol: float = 1e-6          # R15
+    max_backtracks: int = 50   # R11
+    screen_full_norm: bool = False  # R3
+    max_iters: int = 10000
+
+
+@dataclass
+class ALOptions:
+    feas_tol: float = 1e-6
+    rho0: float = 1.0
+    rho_factor: float = 2.0
+    rho_cap: float = 1e12
+    max_outer: int = 100
+
+
+class LSQ:
+    """f(x) = 1/2||M~x - b||^2 + c^T x + delta/2||x||^2 (+ AL terms of Eq. (3)).
+
+    M is m x ncols (numpy, any order; stored column-major); M~ = M diag(colscale),
+    or [M, -M] when ``split``.  Linear constraints: E^T x = e (E nvars x n_eq),
+    G^T x <= hv (G nvars x n_in).
+    """
+
+    def __init__(self, M, b=None, c=None, delta=0.0, colscale=None, split=False,
+                 E=None, e=None, G=None, hv=None):
+        self.M = np.asfortranarray(M, dtype=np.float64)
+        self.m, self.ncols = self.M.shape
+        self.split = bool(split)
+        self.nvars = 2 * self.ncols if split else self.ncols
+        self.b = None if b is None else _f64(b)
+        self.c = None if c is None else _f64(c)
+        self.delta = float(delta)
+        self.colscale = None if colscale is None else _f64(colscale)
+        self.E = None if E is None else np.asfortranarray(np.reshape(E, (self.nvars, -1)), dtype=np.float64)
+        self.e = None if e is None else _f64(np.atleast_1d(e))
+        self.G = None if G is None else np.asfortranarray(np.reshape(G, (self.nvars, -1)), dtype=np.float64)
+        self.hv = None if hv is None else _f64(np.atleast_1d(hv))
+        self.n_eq = 0 if self.E is None else self.E.shape[1]
+        self.n_in = 0 if self.G is None else self.G.shape[1]
+        self.lam = np.zeros(max(self.n_eq, 1))
+        self.mu = np.zeros(max(self.n_in, 1))
+        self.rho = 1.0
+        assert self.n_eq <= 64 and self.n_in <= 64
+
+    def _struct(self):
+        s = _Lsq()
+        s.m, s.ncols, s.lda = self.m, self.ncols, self.m
+        s.M = _ptr(self.M)
+        s.colscale = _ptr(self.colscale)
+        s.split = int(self.split)
+        s.b = _ptr(self.b); s.c = _ptr(self.c); s.delta = self.delta
+        s.n_eq = self.n_eq; s.E = _ptr(self.E); s.e = _ptr(self.e); s.lam = _ptr(self.lam)
+        s.n_in = self.n_in; s.G = _ptr(self.G); s.hv = _ptr(self.hv); s.mu = _ptr(self.mu)
+        s.rho = self.rho
+        return s
+
+    def value(self, x):
+        x = _f64(x); s = self._struct()
+        return _L().orc_lsq_value(C.byref(s), _ptr(x))
+
+    def grad(self, x):
+        x = _f64(x); s = self._struct(); g = np.empty(self.nvars)
+        _L().orc_lsq_grad(C.byref(s), _ptr(x), _ptr(g))
+        return g
+
+
+@dataclass
+class Result:
+    x: np.ndarray
+    f: float
+    pg_inf: float
+    gfree_inf: float
+    iters: int
+    n_fg: int
+    n_backtracks: int
+    n_free: int
+    status: int
+    last_branch: int
+    n_fallbacks: int
+
+
+def minimize_lsq(P: LSQ, l=None, u=None, x0=None, m_hist=5, opts: Options | None = None):
+    """Alg. 1 on the LSQ objective, with Alg. 2/3 and Armijo."""
+    o = opts or Options()
+    x = np.zeros(P.nvars) if x0 is None else _f64(x0).copy()
+    l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
+    u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
+    so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
+               o.max_iters)
+    res = _Res()
+    s = P._struct()
+    _L().orc_minimize_lsq(C.byref(s), _ptr(l), _ptr(u), m_hist, C.byref(so), _ptr(x),
+                          C.byref(res))
+    return Result(x, res.f, res.pg_inf, res.gfree_inf, res.iters, res.n_fg, res.n_backtracks,
+                  res.n_free, res.status, res.last_branch, res.n_fallbacks)
+
+
+@dataclass
+class ALResult:
+    x: np.ndarray
+    lam: np.ndarray
+    mu: np.ndarray
+    f: float
+    violation_inf: float
+    rho: float
+    outer_iters: int
+    inner_iters_total: int
+    status: int
+
+
+def al_solve(P: LSQ, l=None, u=None, m_hist=5, opts: Options | None = None,
+             al_opts: ALOptions | None = None):
+    """Alg. 4 for linear constraints."""
+    o = opts or Options(); ao = al_opts or ALOptions()
+    x = np.zeros(P.nvars)
+    l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
+    u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
+    lam = np.zeros(max(P.n_eq, 1)); mu = np.zeros(max(P.n_in, 1))
+    so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
+               o.max_iters)
+    sa = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer)
+    s = P._struct()
+    res = _AlRes()
+    _L().orc_al_solve(C.byref(s), _ptr(lam), _ptr(mu), _ptr(l), _ptr(u), m_hist, C.byref(so),
+                      C.byref(sa), _ptr(x), C.byref(res))
+    return ALResult(x, lam[:P.n_eq].copy(), mu[:P.n_in].copy(), res.f, res.violation_inf,
+                    res.rho, res.outer_iters, res.inner_iters_total, res.status)

@@ -1,0 +1,579 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for the modified
+ * (Cauchy-point-free) L-BFGS-B method of arXiv 2203.16340 and its augmented
+ * Lagrangian wrapper.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this file's
+ * shared library.  The product path (paper_2203_16340_b200/) never links,
+ * imports or executes anything under oracle/; the two share no code,
+ * headers, helpers or constants.
+ *
+ * Everything is fp64 with sequential loops, compiled with -O2
+ * -ffp-contract=off so that every fused multiply-add below is an explicit
+ * fma() call (reading R12) and nothing else is contracted.
+ * Matrices are column-major (element (i,j) at A[i + j*lda]).
+ *
+ * Citations: PAPER.md:N is a line of the paper's LaTeX source;
+ * "R<k>" is a reading of the paper recorded in DESIGN.md section 3.
+ *
+ * Parity pins: every function below is pinned by a -m "not gpu" test in
+ * tests/test_oracle_*.py against something other than itself (worked
+ * examples, closed forms, brute force, scipy).  No function is
+ * "parity unpinned" except the iteration COUNT of orc_minimize (the paper
+ * prints no trajectory; PAPER.md:438 gives only "30-40 iterations").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ */
+/* Elementwise pieces                                                  */
+/* ------------------------------------------------------------------ */
+
+/* clip(x) = min(max(x, l), u); Alg. 2 line 1 "project z^k onto feasible
+ * region".  l/u may be NULL meaning -inf/+inf. */
+static double clip1(double v, const double* l, const double* u, int64_t i)
+{
+    if (l && v < l[i]) v = l[i];
+    if (u && v > u[i]) v = u[i];
+    return v;
+}
+
+void orc_clip(int64_t n, const double* x, const double* l, const double* u, double* out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = clip1(x[i], l, u, i);
+}
+
+static double lo_of(const double* l, int64_t i) { return l ? l[i] : -INFINITY; }
+static double up_of(const double* u, int64_t i) { return u ? u[i] : INFINITY; }
+
+/* Eq. (1): i is FIXED iff
+ *   (x_i <= l_i + eps and g_i >= 0) or (x_i >= u_i - eps and g_i <= 0).
+ * free[i] = 1 for i in S^k.  Ties (g_i == 0 at a bound) are fixed (R17). */
+void orc_working_set(int64_t n, const double* x, const double* g, const double* l,
+                     const double* u, double eps, uint8_t* free_)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        int fixed_lo = (x[i] <= lo_of(l, i) + eps) && (g[i] >= 0.0);
+        int fixed_up = (x[i] >= up_of(u, i) - eps) && (g[i] <= 0.0);
+        free_[i] = (uint8_t)!(fixed_lo || fixed_up);
+    }
+}
+
+/* <u[S], v[S]> (Alg. 3 line 3), sequential order. */
+double orc_masked_dot(int64_t n, const double* u, const double* v, const uint8_t* free_)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+        if (!free_ || free_[i]) s += u[i] * v[i];
+    return s;
+}
+
+/* out = A x   (A m x n column-major), loop order: for j, for i. */
+void orc_matvec(int64_t m, int64_t n, const double* A, int64_t lda, const double* x, double* out)
+{
+    for (int64_t i = 0; i < m; ++i) out[i] = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        const double xj = x[j];
+        const double* a = A + j * lda;
+        for (int64_t i = 0; i < m; ++i) out[i] += a[i] * xj;
+    }
+}
+
+/* out = A^T r, out_j = sum_i A_ij r_i in increasing i. */
+void orc_matvec_t(int64_t m, int64_t n, const double* A, int64_t lda, const double* r, double* out)
+{
+    for (int64_t j = 0; j < n; ++j) {
+        const double* a = A + j * lda;
+        double s = 0.0;
+        for (int64_t i = 0; i < m; ++i) s += a[i] * r[i];
+        out[j] = s;
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* Alg. 3: modified two-loop recursion, literal.     */
+/* S, Y: nh pairs, pair i at S + i*n, OLDEST first (i = 0), newest     */
+/* last (i = nh-1) -- "i = k-1, ..., k-m" of PAPER.md:488 is newest     */
+/* first.  Returns d = -q on S, 0 off S (R5; Alg. 1 line 5 PAPER.md:73) */
+/* screen_full_norm = 0: ||y_i[S]||^2 (R3); 1: ||y_i||^2 literal.        */
+/* ------------------------------------------------------------------ */
+void orc_two_loop(int64_t n, const double* g, const uint8_t* free_, int32_t nh,
+                  const double* S, const double* Y, double eps, int32_t screen_full_norm,
+                  double* d_out)
+{
+    double* q = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double* a = (double*)malloc(sizeof(double) * (size_t)(nh > 0 ? nh : 1));
+    double* rho = (double*)malloc(sizeof(double) * (size_t)(nh > 0 ? nh : 1));
+    double* nu = (double*)malloc(sizeof(double) * (size_t)(nh > 0 ? nh : 1));
+    int* ok = (int*)malloc(sizeof(int) * (size_t)(nh > 0 ? nh : 1));
+
+    /* line 1: q = grad f(x^k)[S^k] */
+    for (int64_t j = 0; j < n; ++j) q[j] = free_[j] ? g[j] : 0.0;
+
+    /* lines 2-8: for i = k-1 ... k-m (newest to oldest) */
+    for (int32_t i = nh - 1; i >= 0; --i) {
+        const double* si = S + (int64_t)i * n;
+        const double* yi = Y + (int64_t)i * n;
+        rho[i] = orc_masked_dot(n, si, yi, free_);                       /* line 3 */
+        nu[i] = screen_full_norm ? orc_masked_dot(n, yi, yi, NULL)
+                                 : orc_masked_dot(n, yi, yi, free_);
+        ok[i] = rho[i] > eps * nu[i];                                    /* line 4 */
+        a[i] = 0.0;
+        if (ok[i]) {
+            a[i] = orc_masked_dot(n, si, q, free_) / rho[i];             /* line 5 */
+            for (int64_t j = 0; j < n; ++j)                              /* line 6 */
+                if (free_[j]) q[j] = q[j] - a[i] * yi[j];
+        }
+    }
+    /* lines 9-11: initial scaling from pair k-1 only (R4) */
+    if (nh > 0 && ok[nh - 1]) {
+        const double gam = rho[nh - 1] / nu[nh - 1];
+        for (int64_t j = 0; j < n; ++j)
+            if (free_[j]) q[j] = gam * q[j];
+    }
+    /* lines 12-17: for i = k-m ... k-1 (oldest to newest) */
+    for (int32_t i = 0; i < nh; ++i) {
+        if (!ok[i]) continue;
+        const double* si = S + (int64_t)i * n;
+        const double* yi = Y + (int64_t)i * n;
+        const double beta = orc_masked_dot(n, yi, q, free_) / rho[i];    /* line 14 */
+        const double coef = a[i] - beta;
+        for (int64_t j = 0; j < n; ++j)                                  /* line 15 */
+            if (free_[j]) q[j] = q[j] + coef * si[j];
+    }
+    for (int64_t j = 0; j < n; ++j) d_out[j] = free_[j] ? -q[j] : 0.0;
+    free(q); free(a); free(rho); free(nu); free(ok);
+}
+
+/* Alg. 2, projectDirection.  Returns 1 for the
+ * projected branch (line 3 test passed), 0 for the truncated branch.
+ * p_out receives the chosen direction.  Inequalities as printed (R9). */
+int32_t orc_project_direction(int64_t n, const double* x, const double* g, const double* d,
+                              const double* l, const double* u, double eps, double* p_out)
+{
+    double pg = 0.0, pp = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        const double z = clip1(x[j] + d[j], l, u, j);   /* line 1 */
+        p_out[j] = z - x[j];                           /* line 2 */
+        pg += p_out[j] * g[j];
+        pp += p_out[j] * p_out[j];
+    }
+    if (pg <= -eps * pp && pp >= eps) return 1;        /* line 3 */
+    for (int64_t j = 0; j < n; ++j) {                  /* lines 6-8 */
+        double pj = d[j];
+        if (d[j] < 0.0 && x[j] <= lo_of(l, j) + eps) pj = 0.0;
+        if (d[j] > 0.0 && x[j] >= up_of(u, j) - eps) pj = 0.0;
+        p_out[j] = pj;
+    }
+    return 0;
+}
+
+/* Largest alpha >= 0 with l <= x + alpha p <= u, as the minimum blocking
+ * ratio; +inf if nothing blocks (Alg. 1 line 7 "appropriate upper bound on
+ * alpha^k"; R10). */
+double orc_max_step(int64_t n, const double* x, const double* p, const double* l, const double* u)
+{
+    double amax = INFINITY;
+    for (int64_t j = 0; j < n; ++j) {
+        double t = INFINITY;
+        if (p[j] < 0.0) t = (lo_of(l, j) - x[j]) / p[j];
+        else if (p[j] > 0.0) t = (up_of(u, j) - x[j]) / p[j];
+        if (t < amax) amax = t;
+    }
+    if (amax < 0.0) amax = 0.0;
+    return amax;
+}
+
+/* ------------------------------------------------------------------ */
+/* The least-squares objective family (built-in objective) */
+/*   f(x) = 1/2 ||M~ x - b||^2 + c^T x + delta/2 ||x||^2               */
+/* plus the augmented-Lagrangian terms of Eq. (3)   */
+/* for LINEAR constraints h(x) = E^T x - e = 0, g(x) = G^T x - hv <= 0: */
+/*   + rho/2 ||h(x) + lam/rho||^2 + rho/2 ||(g(x) + mu/rho)_+||^2       */
+/* M~ = M diag(colscale) (colscale may be NULL), or [M, -M] if split.  */
+/* NNLS: M = A, b, l = 0, no c/delta/constraints; the    */
+/* 1/2 scaling is reading R16.                                          */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int64_t m, ncols, lda;       /* M is m x ncols column-major */
+    const double* M;
+    const double* colscale;      /* NULL or ncols */
+    int32_t split;               /* 1: variables (u, v), M~ = [M, -M] */
+    const double* b;             /* NULL or m */
+    const double* c;             /* NULL or nvars */
+    double delta;
+    int32_t n_eq;                /* E nvars x n_eq column-major, e host n_eq */
+    const double* E; const double* e; const double* lam;
+    int32_t n_in;                /* G nvars x n_in column-major, hv n_in */
+    const double* G; const double* hv; const double* mu;
+    double rho;
+} orc_lsq;
+
+static int64_t lsq_nvars(const orc_lsq* P) { return P->split ? 2 * P->ncols : P->ncols; }
+
+/* q = M~ p  (explicit loops, column order) */
+static void lsq_apply(const orc_lsq* P, const double* p, double* q)
+{
+    const int64_t nc = P->ncols;
+    double* pe = (double*)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+    for (int64_t j = 0; j < nc; ++j) {
+        double v = P->split ? (p[j] - p[nc + j]) : p[j];
+        if (P->colscale) v = P->colscale[j] * v;
+        pe[j] = v;
+    }
+    orc_matvec(P->m, nc, P->M, P->lda, pe, q);
+    free(pe);
+}
+
+/* r = M~ x - b */
+static void lsq_residual(const orc_lsq* P, const double* x, double* r)
+{
+    lsq_apply(P, x, r);
+    if (P->b)
+        for (int64_t i = 0; i < P->m; ++i) r[i] = r[i] - P->b[i];
+}
+
+/* constraint values at x */
+static void lsq_cons(const orc_lsq* P, const double* x, double* hval, double* gval)
+{
+    const int64_t nv = lsq_nvars(P);
+    for (int32_t k = 0; k < P->n_eq; ++k) {
+        double s = 0.0;
+        const double* Ek = P->E + (int64_t)k * nv;
+        for (int64_t j = 0; j < nv; ++j) s += Ek[j] * x[j];
+        hval[k] = s - P->e[k];
+    }
+    for (int32_t k = 0; k < P->n_in; ++k) {
+        double s = 0.0;
+        const double* Gk = P->G + (int64_t)k * nv;
+        for (int64_t j = 0; j < nv; ++j) s += Gk[j] * x[j];
+        gval[k] = s - P->hv[k];
+    }
+}
+
+/* Value of the non-residual part phi(x) = c^T x + delta/2 ||x||^2 + AL terms.
+ * Also returns the AL gradient coefficients (rho h + lam), (rho g + mu)_+. */
+static double lsq_phi(const orc_lsq* P, const double* x, double* coef_eq, double* coef_in)
+{
+    const int64_t nv = lsq_nvars(P);
+    double cx = 0.0, xx = 0.0;
+    for (int64_t j = 0; j < nv; ++j) {
+        if (P->c) cx += P->c[j] * x[j];
+        xx += x[j] * x[j];
+    }
+    double phi = cx + 0.5 * P->delta * xx;
+    double hval[64], gval[64];
+    lsq_cons(P, x, hval, gval);
+    for (int32_t k = 0; k < P->n_eq; ++k) {
+        const double t = hval[k] + P->lam[k] / P->rho;               /* Eq. (3) */
+        phi += 0.5 * P->rho * t * t;
+        if (coef_eq) coef_eq[k] = P->rho * hval[k] + P->lam[k];
+    }
+    for (int32_t k = 0; k < P->n_in; ++k) {
+        double t = gval[k] + P->mu[k] / P->rho;
+        if (t < 0.0) t = 0.0;                                          /* (v)_+ */
+        phi += 0.5 * P->rho * t * t;
+        if (coef_in) coef_in[k] = P->rho * t;                          /* (rho g + mu)_+ */
+    }
+    return phi;
+}
+
+/* g = M~^T r + c + delta x + E (rho h + lam) + G (rho g + mu)_+ */
+static void lsq_grad(const orc_lsq* P, const double* x, const double* r, double* g)
+{
+    const int64_t nc = P->ncols, nv = lsq_nvars(P);
+    double* t = (double*)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+    orc_matvec_t(P->m, nc, P->M, P->lda, r, t);
+    for (int64_t j = 0; j < nc; ++j) {
+        const double v = P->colscale ? P->colscale[j] * t[j] : t[j];
+        g[j] = v;
+        if (P->split) g[nc + j] = -v;
+    }
+    free(t);
+    double ce[64], ci[64];
+    lsq_phi(P, x, ce, ci);
+    for (int64_t j = 0; j < nv; ++j) {
+        double v = g[j];
+        if (P->c) v = v + P->c[j];
+        v = v + P->delta * x[j];
+        for (int32_t k = 0; k < P->n_eq; ++k) v = v + ce[k] * P->E[(int64_t)k * nv + j];
+        for (int32_t k = 0; k < P->n_in; ++k) v = v + ci[k] * P->G[(int64_t)k * nv + j];
+        g[j] = v;
+    }
+}
+
+static double half_sq(int64_t m, const double* r)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < m; ++i) s += r[i] * r[i];
+    return 0.5 * s;
+}
+
+/* ------------------------------------------------------------------ */
+/* Alg. 1 on the LSQ objective.                        */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    double eps, c1, shrink, tol;
+    int32_t max_backtracks, screen_full_norm;
+    int64_t max_iters;
+} orc_opts;
+
+typedef struct {
+    double f, pg_inf, gfree_inf;
+    int64_t iters, n_fg, n_backtracks, n_free;
+    int32_t status, last_branch;
+    int64_t n_fallbacks;
+} orc_result;
+
+enum { ORC_CONVERGED = 0, ORC_MAX_ITERS = 1, ORC_LINESEARCH_FAILURE = 2,
+       ORC_AL_MAX_OUTER = 3, ORC_AL_INNER_FAILURE = 4 };
+
+/* Armijo backtracking on the incremental residual (R10, R11, R13):
+ * alpha_0 = min(1, amax), alpha_t = shrink * alpha_{t-1};
+ * trial t: x_t = clip(fma(alpha_t, p, x)),
+ *          f_t = 1/2 ||fma(alpha_t, q, r)||^2 + phi(x_t);
+ * accept the first t with f_t <= f + c1 alpha_t <g, p>, t <= max_backtracks.
+ * Returns 1 on acceptance. */
+static int armijo_lsq(const orc_lsq* P, const orc_opts* o, int64_t nv, const double* x,
+                      const double* l, const double* u, const double* r, const double* q,
+                      const double* p, double f, double gp, double amax,
+                      double* x_t, double* r_t, double* f_out, double* alpha_out,
+                      int64_t* n_fg, int64_t* n_bt)
+{
+    double alpha = amax < 1.0 ? amax : 1.0;
+    for (int32_t t = 0; t <= o->max_backtracks; ++t) {
+        if (t > 0) alpha = o->shrink * alpha;
+        for (int64_t j = 0; j < nv; ++j) x_t[j] = clip1(fma(alpha, p[j], x[j]), l, u, j);
+        for (int64_t i = 0; i < P->m; ++i) r_t[i] = fma(alpha, q[i], r[i]);
+        const double ft = half_sq(P->m, r_t) + lsq_phi(P, x_t, NULL, NULL);
+        *n_fg += 1;
+        if (ft <= f + o->c1 * alpha * gp) {
+            *f_out = ft; *alpha_out = alpha;
+            return 1;
+        }
+        *n_bt += 1;
+    }
+    return 0;
+}
+
+/* Solve min f(x) s.t. l <= x <= u with Alg. 1.  x in: x0 (clipped),
+ * out: x*.  m_hist pairs, newest last. */
+void orc_minimize_lsq(const orc_lsq* P, const double* l, const double* u, int32_t m_hist,
+                      const orc_opts* o, double* x, orc_result* res)
+{
+    const int64_t nv = lsq_nvars(P), m = P->m;
+    const size_t nvb = sizeof(double) * (size_t)(nv > 0 ? nv : 1);
+    const size_t mb = sizeof(double) * (size_t)(m > 0 ? m : 1);
+    double *g = malloc(nvb), *gn = malloc(nvb), *d = malloc(nvb), *p = malloc(nvb);
+    double *xt = malloc(nvb), *r = malloc(mb), *rt = malloc(mb), *q = malloc(mb);
+    double *Sr = malloc(nvb * (size_t)(m_hist > 0 ? m_hist : 1));
+    double *Yr = malloc(nvb * (size_t)(m_hist > 0 ? m_hist : 1));
+    uint8_t* fr = malloc((size_t)(nv > 0 ? nv : 1));
+    int32_t nh = 0;
+
+    memset(res, 0, sizeof(*res));
+    orc_clip(nv, x, l, u, x);                                   /* feasible x^0 */
+    lsq_residual(P, x, r);
+    double f = half_sq(m, r) + lsq_phi(P, x, NULL, NULL);
+    lsq_grad(P, x, r, g);
+    res->n_fg = 1;
+
+    int64_t k = 0;
+    int32_t status = ORC_MAX_ITERS;
+    for (;;) {
+        orc_working_set(nv, x, g, l, u, o->eps, fr);             /* Alg. 1 line 3 */
+        double gfree = 0.0; int64_t nfree = 0;
+        for (int64_t j = 0; j < nv; ++j)
+            if (fr[j]) { ++nfree; if (fabs(g[j]) > gfree) gfree = fabs(g[j]); }
+        if (nfree == 0 || gfree <= o->tol) { status = ORC_CONVERGED; break; }  /* R15 */
+        if (k >= o->max_iters) { status = ORC_MAX_ITERS; break; }
+
+        int accepted = 0;
+        double alpha = 0.0, fnew = f;
+        for (int attempt = 0; attempt < 2 && !accepted; ++attempt) {
+            if (attempt == 1) { nh = 0; res->n_fallbacks += 1; }      /* R14 fallback */
+            orc_two_loop(nv, g, fr, nh, Sr, Yr, o->eps, o->screen_full_norm, d);  /* line 4 */
+            const int32_t br = orc_project_direction(nv, x, g, d, l, u, o->eps, p); /* line 6 */
+            res->last_branch = br;
+            double gp = 0.0;
+            for (int64_t j = 0; j < nv; ++j) gp += g[j] * p[j];
+            if (!(gp < 0.0)) continue;                                /* guard, R14 */
+            const double amax = br ? 1.0 : orc_max_step(nv, x, p, l, u);
+            lsq_apply(P, p, q);
+            accepted = armijo_lsq(P, o, nv, x, l, u, r, q, p, f, gp, amax, xt, rt, &fnew,
+                                  &alpha, &res->n_fg, &res->n_backtracks);
+        }
+        if (!accepted) { status = ORC_LINESEARCH_FAILURE; break; }
+
+        /* line 7: x^{k+1}; carried residual r^{k+1} = r + alpha q (R13) */
+        lsq_grad(P, xt, rt, gn);
+        /* lines 8-9: s = x^{k+1} - x^k, y = grad^{k+1} - grad^k, stored
+         * unconditionally (R8), oldest dropped */
+        if (m_hist > 0) {
+            if (nh == m_hist) {
+                memmove(Sr, Sr + nv, nvb * (size_t)(m_hist - 1));
+                memmove(Yr, Yr + nv, nvb * (size_t)(m_hist - 1));
+                nh = m_hist - 1;
+            }
+            for (int64_t j = 0; j < nv; ++j) {
+                Sr[(int64_t)nh * nv + j] = xt[j] - x[j];
+                Yr[(int64_t)nh * nv + j] = gn[j] - g[j];
+            }
+            nh += 1;
+        }
+        memcpy(x, xt, nvb); memcpy(g, gn, nvb); memcpy(r, rt, mb);
+        f = fnew;
+        ++k;
+    }
+
+    /* final refresh: r = M~x - b, g, f; pg = ||clip(x - g) - x||_inf */
+    lsq_residual(P, x, r);
+    f = half_sq(m, r) + lsq_phi(P, x, NULL, NULL);
+    lsq_grad(P, x, r, g);
+    orc_working_set(nv, x, g, l, u, o->eps, fr);
+    double pg = 0.0, gfree = 0.0; int64_t nfree = 0;
+    for (int64_t j = 0; j < nv; ++j) {
+        const double v = fabs(clip1(x[j] - g[j], l, u, j) - x[j]);
+        if (v > pg) pg = v;
+        if (fr[j]) { ++nfree; if (fabs(g[j]) > gfree) gfree = fabs(g[j]); }
+    }
+    res->f = f; res->pg_inf = pg; res->gfree_inf = gfree; res->n_free = nfree;
+    res->iters = k; res->status = status;
+    free(g); free(gn); free(d); free(p); free(xt); free(r); free(rt); free(q);
+    free(Sr); free(Yr); free(fr);
+}
+
+/* ------------------------------------------------------------------ */
+/* Alg. 4, augmented Lagrangian for LINEAR          */
+/* constraints E^T x = e, G^T x <= hv.  Readings R18-R22.               */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    double feas_tol, rho0, rho_factor, rho_cap;
+    int32_t max_outer;
+} orc_al_opts;
+
+typedef struct {
+    double violation_inf, rho, f;
+    int64_t outer_iters, inner_iters_total;
+    int32_t status;
+} orc_al_result;
+
+/* Constraint-violation measure of the rho rule and the stopping test
+ * ("infinity norm of the constraint violation"; reading R21):
+ *   v = max(||h||_inf, ||min(-g, mu/rho)||_inf)
+ * -- the complementarity-aware measure of Birgin & Martinez (2014), the
+ * reference PAPER.md:531 cites for the convergence of Alg. 4.  For equality
+ * constraints it is ||h||_inf; for an inequality it is the violation g_+
+ * when g > 0 and otherwise how far mu is from complementary slackness. */
+static double viol_inf(const orc_lsq* P, const double* x, const double* mu, double rho)
+{
+    double hval[64], gval[64], v = 0.0;
+    lsq_cons(P, x, hval, gval);
+    for (int32_t k = 0; k < P->n_eq; ++k) if (fabs(hval[k]) > v) v = fabs(hval[k]);
+    for (int32_t k = 0; k < P->n_in; ++k) {
+        double t = -gval[k];
+        const double mr = mu[k] / rho;
+        if (mr < t) t = mr;
+        if (fabs(t) > v) v = fabs(t);
+    }
+    return v;
+}
+
+/* P->lam, P->mu are read AND updated in place (they must point at writable
+ * arrays, cast away const by the caller-owned buffers lam_io / mu_io). */
+void orc_al_solve(orc_lsq* P, double* lam_io, double* mu_io, const double* l, const double* u,
+                  int32_t m_hist, const orc_opts* o, const orc_al_opts* ao, double* x,
+                  orc_al_result* res)
+{
+    const int64_t nv = lsq_nvars(P);
+    memset(res, 0, sizeof(*res));
+    for (int64_t j = 0; j < nv; ++j) x[j] = 0.0;                   /* x^0 = 0 (R19) */
+    orc_clip(nv, x, l, u, x);
+    for (int32_t k = 0; k < P->n_eq; ++k) lam_io[k] = 0.0;
+    for (int32_t k = 0; k < P->n_in; ++k) mu_io[k] = 0.0;
+    P->lam = lam_io; P->mu = mu_io;
+    double rho = ao->rho0;
+    double vprev = viol_inf(P, x, mu_io, rho);
+    res->status = ORC_AL_MAX_OUTER;
+    for (int32_t it = 0; it < ao->max_outer; ++it) {
+        orc_opts oi = *o;
+        const double tin = 0.1 * vprev;
+        oi.tol = tin > o->tol ? tin : o->tol;                      /* R22 */
+        P->rho = rho;
+        orc_result ir;
+        orc_minimize_lsq(P, l, u, m_hist, &oi, x, &ir);            /* Alg. 4 line 5 */
+        res->inner_iters_total += ir.iters;
+        res->outer_iters = it + 1;
+        if (ir.status == ORC_LINESEARCH_FAILURE) { res->status = ORC_AL_INNER_FAILURE; break; }
+        double hval[64], gval[64];
+        lsq_cons(P, x, hval, gval);
+        for (int32_t k = 0; k < P->n_eq; ++k) lam_io[k] = lam_io[k] + rho * hval[k];  /* line 6 */
+        for (int32_t k = 0; k < P->n_in; ++k) {                                        /* line 7 */
+            const double t = mu_io[k] + rho * gval[k];
+            mu_io[k] = t > 0.0 ? t : 0.0;
+        }
+        const double v = viol_inf(P, x, mu_io, rho);
+        if (v > 0.5 * vprev) {                                      /* line 8, R20 */
+            rho = rho * ao->rho_factor;
+            if (rho > ao->rho_cap) rho = ao->rho_cap;
+        }
+        vprev = v;
+        if (ir.status == ORC_CONVERGED && v <= ao->feas_tol && oi.tol == o->tol) {
+            res->status = ORC_CONVERGED;
+            break;
+        }
+    }
+    /* report the ORIGINAL objective f (no AL terms) at x */
+    {
+        orc_lsq Q = *P; Q.n_eq = 0; Q.n_in = 0;
+        double* r = malloc(sizeof(double) * (size_t)(P->m > 0 ? P->m : 1));
+        lsq_residual(&Q, x, r);
+        res->f = half_sq(P->m, r) + lsq_phi(&Q, x, NULL, NULL);
+        free(r);
+    }
+    res->violation_inf = viol_inf(P, x, mu_io, rho);
+    res->rho = rho;
+}
+
+/* Elementary helpers exposed for the pins (SPEC-style worked examples). */
+int32_t orc_check_convergence(int64_t n, const double* g, const uint8_t* free_, double tol)
+{
+    for (int64_t j = 0; j < n; ++j)
+        if (free_[j] && fabs(g[j]) > tol) return 0;
+    return 1;
+}
+
+double orc_lsq_value(const orc_lsq* P, const double* x)
+{
+    double* r = malloc(sizeof(double) * (size_t)(P->m > 0 ? P->m : 1));
+    lsq_residual(P, x, r);
+    const double f = half_sq(P->m, r) + lsq_phi(P, x, NULL, NULL);
+    free(r);
+    return f;
+}
+
+void orc_lsq_grad(const orc_lsq* P, const double* x, double* g)
+{
+    double* r = malloc(sizeof(double) * (size_t)(P->m > 0 ? P->m : 1));
+    lsq_residual(P, x, r);
+    lsq_grad(P, x, r, g);
+    free(r);
+}
+
+/* Armijo on a generic 1-D helper for the SPEC worked example f(x) = x^2:
+ * returns the accepted alpha or -1 (pins R11 independently of LSQ). */
+double orc_armijo_scalar_quadratic(double x, double p, double amax, double c1, double shrink,
+                                   int32_t max_bt)
+{
+    const double f = x * x, gp = 2.0 * x * p;
+    double alpha = amax < 1.0 ? amax : 1.0;
+    for (int32_t t = 0; t <= max_bt; ++t) {
+        if (t > 0) alpha = shrink * alpha;
+        const double xt = fma(alpha, p, x);
+        if (xt * xt <= f + c1 * alpha * gp) return alpha;
+    }
+    return -1.0;
+}

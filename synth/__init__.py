@@ -1,0 +1,143 @@
+"""Seeded synthetic workloads (inputs only).
+
+This module is shared by the tests, ``bench.py`` and ``__graft_entry__.smoke``;
+it holds NONE of the method's arithmetic (no working set, no two-loop, no
+projection, no line search): it only draws the problem data with numpy's
+seeded ``Generator`` and returns numpy arrays.  Both the oracle and the CUDA
+path receive the same arrays.
+
+Recipes follow SURVEY.md 8(d) and the paper's NNLS
+generators.  Every matrix is returned column-major
+(Fortran-ordered, shape (m, n)) because both implementations store A
+column-major.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def _gauss_colmajor(rng, m, n, scale=1.0):
+    # draw an (n, m) C-ordered block and view it transposed: column-major (m, n)
+    a = rng.standard_normal((n, m))
+    if scale != 1.0:
+        a *= scale
+    return a.T
+
+
+@dataclass
+class Problem:
+    """One synthetic instance.  ``kind`` in {"nnls", "lasso", "svm"}."""
+    kind: str
+    name: str
+    M: np.ndarray                      # (m, ncols) column-major
+    b: np.ndarray | None = None
+    c: np.ndarray | None = None        # length nvars
+    delta: float = 0.0
+    colscale: np.ndarray | None = None
+    split: bool = False
+    lower: np.ndarray | None = None    # length nvars, None = -inf
+    upper: np.ndarray | None = None    # length nvars, None = +inf
+    E: np.ndarray | None = None        # (nvars, n_eq)
+    e: np.ndarray | None = None
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def m(self):
+        return self.M.shape[0]
+
+    @property
+    def ncols(self):
+        return self.M.shape[1]
+
+    @property
+    def nvars(self):
+        return 2 * self.ncols if self.split else self.ncols
+
+
+def nnls_gaussian(m: int, n: int, seed: int, name: str = "") -> Problem:
+    """C1/C2: A_ij ~ N(0,1)/sqrt(m), b ~ N(0,1), l = 0, u = +inf.
+
+    The NNLS problem of PAPER.md:371 with the 1/2 scaling of reading R16.
+    Expected: ~50% of the variables at the bound at the optimum.
+    """
+    rng = np.random.default_rng(seed)
+    A = _gauss_colmajor(rng, m, n, 1.0 / np.sqrt(m))
+    b = rng.standard_normal(m)
+    return Problem("nnls", name or f"nnls_gaussian_{m}x{n}", A, b=b,
+                   lower=np.zeros(n), upper=None, meta=dict(m=m, n=n, seed=seed))
+
+
+def nnls_ds1(t: float, seed: int) -> Problem:
+    """Paper data set (i): A in R^{2000t x 6000t} uniform [0,1),
+    planted x with density 0.01 (half-normal, reading R23),
+    b = sqrt(0.003) A x + 0.003 z."""
+    rng = np.random.default_rng(seed)
+    m, n = int(round(2000 * t)), int(round(6000 * t))
+    A = rng.random((n, m)).T
+    x = np.zeros(n)
+    nz = rng.random(n) < 0.01
+    x[nz] = np.abs(rng.standard_normal(int(nz.sum())))
+    b = np.sqrt(0.003) * (A @ x) + 0.003 * rng.standard_normal(m)
+    return Problem("nnls", f"ds1_t{t}", A, b=b, lower=np.zeros(n), meta=dict(t=t, seed=seed))
+
+
+def nnls_ds2(t: float, seed: int) -> Problem:
+    """Paper data set (ii): A in R^{6000t x 3000t} Gaussian,
+    planted density 0.1 (half-normal, R23), b = sqrt(1/6000) A x + 0.003 z (R24)."""
+    rng = np.random.default_rng(seed)
+    m, n = int(round(6000 * t)), int(round(3000 * t))
+    A = _gauss_colmajor(rng, m, n)
+    x = np.zeros(n)
+    nz = rng.random(n) < 0.1
+    x[nz] = np.abs(rng.standard_normal(int(nz.sum())))
+    b = np.sqrt(1.0 / 6000.0) * (A @ x) + 0.003 * rng.standard_normal(m)
+    return Problem("nnls", f"ds2_t{t}", A, b=b, lower=np.zeros(n), meta=dict(t=t, seed=seed))
+
+
+def lasso_split(m: int, n: int, seed: int, alpha: float = 1.0, lam_frac: float = 0.1) -> Problem:
+    """C3: elastic-net / lasso via split variables x = u - v, u, v >= 0.
+
+    A ~ N(0,1)/sqrt(m); x_true 1% nonzeros +-N(0,1); b = A x_true + 0.01 z;
+    lam = lam_frac * ||A^T b||_inf;
+    f(u,v) = 1/2||A(u-v) - b||^2 + lam*alpha*1^T(u+v) + lam(1-alpha)/2 (||u||^2+||v||^2).
+    """
+    rng = np.random.default_rng(seed)
+    A = _gauss_colmajor(rng, m, n, 1.0 / np.sqrt(m))
+    xt = np.zeros(n)
+    nz = rng.random(n) < 0.01
+    xt[nz] = rng.standard_normal(int(nz.sum()))
+    b = A @ xt + 0.01 * rng.standard_normal(m)
+    lam = lam_frac * float(np.max(np.abs(A.T @ b)))
+    c = np.full(2 * n, lam * alpha)
+    return Problem("lasso", f"lasso_{m}x{n}_a{alpha}", A, b=b, c=c, delta=lam * (1 - alpha),
+                   split=True, lower=np.zeros(2 * n), upper=None,
+                   meta=dict(m=m, n=n, seed=seed, alpha=alpha, lam=lam))
+
+
+def svm_dual_linear(N: int, d: int, seed: int, C: float = 1.0, sep: float = 2.0) -> Problem:
+    """C4: linear-kernel dual SVM (PAPER.md:349-352 with K = X X^T).
+
+    y balanced +-1; x_i ~ N(y_i (sep/sqrt(d)) 1, I_d); C = 1.
+    f(a) = 1/2 ||X^T (a*y)||^2 - 1^T a, s.t. y^T a = 0, 0 <= a <= C.
+    Stored as M = X^T (d x N column-major == X row-major), colscale = y, c = -1.
+    """
+    rng = np.random.default_rng(seed)
+    y = np.where(np.arange(N) % 2 == 0, 1.0, -1.0)
+    rng.shuffle(y)
+    X_T = _gauss_colmajor(rng, d, N)            # column i = sample i
+    X_T += (y * (sep / np.sqrt(d)))[None, :]
+    return Problem("svm", f"svm_{N}x{d}", X_T, b=None, c=-np.ones(N), colscale=y,
+                   lower=np.zeros(N), upper=np.full(N, C), E=y.reshape(N, 1),
+                   e=np.zeros(1), meta=dict(N=N, d=d, seed=seed, C=C))
+
+
+# Named configurations of BASELINE.json "configs"
+CONFIGS = {
+    "C1": lambda seed=1: nnls_gaussian(200, 100, seed, "C1_nnls_200x100"),
+    "C2": lambda seed=2: nnls_gaussian(20000, 10000, seed, "C2_nnls_20000x10000"),
+    "C3": lambda seed=3: lasso_split(10000, 50000, seed, alpha=1.0),
+    "C3en": lambda seed=3: lasso_split(10000, 50000, seed, alpha=0.5),
+    "C4": lambda seed=4: svm_dual_linear(100000, 1000, seed),
+}
