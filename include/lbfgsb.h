@@ -1,0 +1,228 @@
+/*
+ * lbfgsb.h -- C ABI of the B200-native (sm_100a, fp64) hot path of the
+ * GPU-efficient, Cauchy-point-free L-BFGS-B method of arXiv 2203.16340 and
+ * its augmented-Lagrangian wrapper.
+ *
+ * Citations are lines of the paper's LaTeX source (PAPER.md:N, section /
+ * algorithm / equation); "R<k>" names a reading of the paper recorded in
+ * DESIGN.md section 3.
+ *
+ *   problem (section 3):  min f(x)  s.t.  l <= x <= u,
+ *                                      l, u in R^n u {-inf, +inf}
+ *   Alg. 1   main loop      -> lbfgsb_solve
+ *   Alg. 2  projectDirection
+ *   Eq. (1) working set S^k
+ *   Alg. 3 modified two-loop recursion (computed in its
+ *                              vector-free, Gram-matrix form on the device)
+ *   Alg. 4 augmented Lagrangian, Eq. (3)
+ *                              -> al_solve
+ *
+ * Conventions (all entry points):
+ *  - fp64 throughout.  Pointers are DEVICE pointers unless marked (host).
+ *  - Matrices are column-major: element (i, j) at M[i + j*ld], ld >= m.
+ *  - Ownership: the caller owns every buffer it passes (M, b, c, bounds,
+ *    x, constraint data, lambda, mu); they must stay valid for the duration
+ *    of the call that uses them (objectives BORROW M/b/c/colscale until
+ *    lbfgsb_objective_free).  The library owns the workspace it allocates in
+ *    lbfgsb_create and frees it in lbfgsb_destroy; bounds are copied at
+ *    create time.
+ *  - Streams: all device work of a handle runs on the cuda stream given to
+ *    lbfgsb_create; NULL makes the handle create a private blocking stream
+ *    (implicitly ordered with the legacy default stream), because CUDA
+ *    graphs cannot be captured on the legacy stream.  Solve calls return
+ *    host-synchronously.  A handle is not thread-safe (one solve at a time).
+ *  - Errors are return codes (never exceptions across the ABI); details via
+ *    lbfgsb_last_error().  The solve OUTCOME (converged, max iterations,
+ *    line-search failure) is a status in the result struct, not an error.
+ *  - The library never falls back to a CPU path: if no CUDA device is
+ *    usable every entry point that touches the device returns
+ *    LBFGSB_ERR_CUDA.
+ */
+#ifndef LBFGSB_H_
+#define LBFGSB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBFGSB_ABI_VERSION 1
+#define LBFGSB_MAX_HIST 16      /* m_hist <= 16                                  */
+#define LBFGSB_MAX_CONS 4       /* linear AL constraints fused on device (m_eq+p_in) */
+
+typedef struct lbfgsb_t lbfgsb_t;                 /* opaque solver handle            */
+typedef struct lbfgsb_objective lbfgsb_objective; /* opaque objective descriptor     */
+
+typedef enum {
+    LBFGSB_OK = 0,
+    LBFGSB_ERR_ARG = 1,         /* NULL where required, bad option value          */
+    LBFGSB_ERR_DIM = 2,         /* dimension mismatch / out of range               */
+    LBFGSB_ERR_BOUNDS = 3,      /* l_i > u_i or NaN bound            */
+    LBFGSB_ERR_NONFINITE = 4,   /* f or gradient not finite at the start point     */
+    LBFGSB_ERR_CALLBACK = 5,    /* user callback returned nonzero                  */
+    LBFGSB_ERR_CUDA = 6,        /* CUDA runtime error / no device                  */
+    LBFGSB_ERR_NCCL = 7,        /* NCCL error in a sharded handle                  */
+    LBFGSB_ERR_OOM = 8,         /* device allocation failed                        */
+    LBFGSB_ERR_UNSUPPORTED = 9  /* feature not available in this build / handle    */
+} lbfgsb_err;
+
+typedef enum {
+    LBFGSB_CONVERGED = 0,          /* ||grad f[S^k]||_inf <= tol or S^k empty (R15) */
+    LBFGSB_MAX_ITERS = 1,
+    LBFGSB_LINESEARCH_FAILURE = 2, /* Armijo failed after the steepest-descent fallback (R14) */
+    AL_MAX_OUTER = 3,
+    AL_INNER_FAILURE = 4
+} lbfgsb_status;
+
+/* Solver options (the paper fixes none of these values; R1, R3, R11, R15). */
+typedef struct {
+    double eps;                 /* epsilon of Eq. (1), Alg. 2 line 3, Alg. 3 line 4 (R1,R2); default 1e-9 */
+    double c1;                  /* Armijo constant (R11); default 1e-4                  */
+    double shrink;              /* backtracking factor beta (R11); default 0.5          */
+    double tol;                 /* stop when ||g[S]||_inf <= tol (R15); default 1e-6     */
+    int32_t max_backtracks;     /* trials t = 0..max_backtracks per search (R11); 50     */
+    int32_t screen_full_norm;   /* 0: screen with ||y[S]||^2 (R3), 1: ||y||^2; default 0 */
+    int32_t check_every;        /* iterations launched between host checks; default 8   */
+    int32_t use_graph;          /* 1: replay a CUDA graph of check_every iterations; 1  */
+    int32_t profile;            /* 1: CUDA events around the two GEMV launches (ops.h)  */
+    int32_t pad_;
+    int64_t max_iters;          /* default 10000                                        */
+} lbfgsb_opts;
+
+/* Outcome of one box-constrained solve (host struct). */
+typedef struct {
+    double f;                   /* objective at x* after the final residual refresh     */
+    double pg_inf;              /* ||clip(x - g) - x||_inf  (KKT measure, R15)           */
+    double gfree_inf;           /* ||g[S]||_inf at x*                                    */
+    double seconds;             /* wall time of the solve (host clock, sync to sync)     */
+    int64_t iters;              /* Alg. 1 iterations                                     */
+    int64_t n_fg;               /* objective evaluations (setup + line-search trials)    */
+    int64_t n_backtracks;       /* rejected Armijo trials                                */
+    int64_t n_free;             /* |S| at x*                                             */
+    int64_t n_fallbacks;        /* steepest-descent fallbacks taken (R14)                */
+    int32_t status;             /* lbfgsb_status                                         */
+    int32_t last_branch;        /* 1 = projected, 0 = truncated (Alg. 2) in the last iteration */
+} lbfgsb_result;
+
+void lbfgsb_opts_default(lbfgsb_opts* o);                            /* (host) */
+
+/* Thread-local text describing the last non-OK return (never NULL). */
+const char* lbfgsb_last_error(void);
+
+/* Create a solver for n variables with box l <= x <= u and m_hist curvature
+ * pairs (1 <= m_hist <= LBFGSB_MAX_HIST; the L-BFGS memory of Alg. 3).
+ * lower/upper: DEVICE vectors of length n, or NULL for -inf / +inf
+ * everywhere; copied into the handle.  Errors: ARG, DIM, BOUNDS, CUDA, OOM. */
+lbfgsb_err lbfgsb_create(int64_t n, int32_t m_hist, const double* lower, const double* upper,
+                         const lbfgsb_opts* opts /* NULL = defaults */, void* cuda_stream,
+                         lbfgsb_t** out);
+
+/* Column-sharded handle: this rank owns n_local of the
+ * n_global variables (a contiguous block of columns of M~).  The library
+ * creates its own NCCL communicator from the 128-byte ncclUniqueId
+ * (host) that the caller broadcast (e.g. with torch.distributed).
+ * Returns LBFGSB_ERR_UNSUPPORTED when the library was built without NCCL. */
+lbfgsb_err lbfgsb_create_sharded(int64_t n_local, int64_t n_global, int32_t m_hist,
+                                 const double* lower_local, const double* upper_local,
+                                 const lbfgsb_opts* opts, void* cuda_stream,
+                                 const void* nccl_unique_id /* (host) 128 bytes */,
+                                 int32_t rank, int32_t nranks, lbfgsb_t** out);
+
+void lbfgsb_destroy(lbfgsb_t* h);
+
+/* ---- objectives --------------------------------------------------------- */
+
+/* Built-in least-squares family (the paper's NNLS workload PAPER.md:368-374,
+ * the linear-kernel dual SVM of PAPER.md:349-352, split-variable lasso):
+ *    f(x) = 1/2 ||M~ x - b||^2 + c^T x + delta/2 ||x||^2            (R16)
+ * with M~ = M diag(colscale) (colscale NULL = identity), or, when split = 1,
+ * M~ = [M, -M] over n = 2*ncols variables (x = (u, v), u - v the lasso
+ * coefficients).  M: m x ncols column-major with leading dimension ld >= m
+ * (DEVICE, borrowed); b: m (NULL = 0); c: n (NULL = 0).  The objective's
+ * hot path is the fused GEMV / GEMV^T pair of DESIGN.md section 5.
+ * For a sharded handle, M holds this rank's ncols_local columns and b is
+ * the full (replicated) m-vector.  Errors: ARG, DIM. */
+lbfgsb_err lbfgsb_objective_lsq(const double* M, int64_t m, int64_t ncols, int64_t ld,
+                                const double* colscale, int32_t split, const double* b,
+                                const double* c, double delta, lbfgsb_objective** out);
+
+/* User objective: fg(user, x, g, f_host, stream) must write grad f(x) into
+ * the DEVICE vector g (length n), *f_host = f(x) (host), enqueue its device
+ * work on `stream` (or synchronise it), and return 0 (nonzero -> the solve
+ * returns LBFGSB_ERR_CALLBACK).  x and g are library-owned device buffers
+ * valid only during the call. */
+typedef int32_t (*lbfgsb_fg_cb)(void* user, const double* x, double* g, double* f_host,
+                                void* cuda_stream);
+lbfgsb_err lbfgsb_objective_callback(lbfgsb_fg_cb fg, void* user, lbfgsb_objective** out);
+
+void lbfgsb_objective_free(lbfgsb_objective* obj);
+
+/* ---- Alg. 1 -------------------------------------------------------------- */
+
+/* Minimise obj over the handle's box with Alg. 1.  x (DEVICE, length n):
+ * in = x^0 (clipped into the box first), out = x*.
+ * tol overrides opts.tol when > 0.  res (host) receives the outcome.
+ * Errors: ARG, DIM, NONFINITE (f or g(x^0) not finite), CALLBACK, CUDA. */
+lbfgsb_err lbfgsb_solve(lbfgsb_t* h, const lbfgsb_objective* obj, double* x, double tol,
+                        lbfgsb_result* res);
+
+/* Same as lbfgsb_solve for the LSQ family, but every input and the output
+ * are HOST buffers: M_host (m x ncols, column-major, ld = m), b_host (m),
+ * x_host (in x^0 / out x*).  The handle keeps a device copy buffer between
+ * calls of the same shape; the host->device copies of M and b and the
+ * device->host copy of x are part of the call (the bench's e2e number). */
+lbfgsb_err lbfgsb_solve_lsq_host(lbfgsb_t* h, const double* M_host, int64_t m, int64_t ncols,
+                                 const double* b_host, double* x_host, double tol,
+                                 lbfgsb_result* res);
+
+/* ---- Alg. 4 -------------------------------------------------------------- */
+
+typedef struct {
+    double feas_tol;            /* stop when violation <= feas_tol (R22); default 1e-6  */
+    double rho0;                /* initial penalty; default 1            */
+    double rho_factor;          /* rho *= rho_factor if violation not halved; 2 */
+    double rho_cap;             /* default 1e12                                          */
+    int32_t max_outer;          /* default 100                                           */
+    int32_t pad_;
+} al_opts;
+
+void al_opts_default(al_opts* o);                                    /* (host) */
+
+/* Linear constraints  E^T x = e  (m_eq of them) and  G^T x <= hv  (p_in),
+ * m_eq + p_in <= LBFGSB_MAX_CONS.  E: n x m_eq column-major (DEVICE),
+ * e: m_eq (host); G: n x p_in (DEVICE), hv: p_in (host). */
+typedef struct {
+    int64_t m_eq, p_in;
+    const double* E;
+    const double* e;
+    const double* G;
+    const double* hv;
+} al_constraints;
+
+typedef struct {
+    double violation_inf;       /* max(||h||_inf, ||min(-g, mu/rho)||_inf) (R21)      */
+    double f;                   /* original objective f(x*) (no AL terms)              */
+    double rho;                 /* final penalty                                       */
+    double pg_inf;              /* KKT measure of the last inner solve                  */
+    int64_t outer_iters, inner_iters_total;
+    int32_t status;             /* LBFGSB_CONVERGED, AL_MAX_OUTER, AL_INNER_FAILURE     */
+    int32_t pad_;
+} al_result;
+
+/* Alg. 4: x^0 = clip(0) (R19), lambda^0 = 0, mu^0 = 0, rho = rho0; each
+ * outer iteration minimises the augmented Lagrangian Eq. (3) over the box
+ * with Alg. 1 (warm x, empty history, inner tol max(tol, 0.1 v), R22), then
+ * lambda += rho h(x), mu = (mu + rho g(x))_+  and
+ * rho *= rho_factor if the violation was not halved (R20).
+ * obj must be an LSQ objective.  x (DEVICE, n) out; lambda (host, m_eq) and
+ * mu (host, p_in) out.  Errors: ARG, DIM, UNSUPPORTED (callback objective or
+ * too many constraints), CUDA. */
+lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const al_constraints* cons,
+                    const al_opts* opts, double* x, double* lambda, double* mu,
+                    al_result* res);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBFGSB_H_ */

@@ -1,0 +1,68 @@
+/*
+ * lbfgsb_ops.h -- op-level C ABI: the individual hot-path kernels of
+ * lbfgsb_solve exposed one by one, so that each can be checked against the
+ * CPU oracle on identical inputs (tests/test_gpu_parity.py) and timed alone
+ * (bench.py roofline).  Same conventions as lbfgsb.h: fp64, DEVICE pointers
+ * unless marked (host), column-major matrices, caller-owned buffers,
+ * errors as return codes, all work on the given stream, host-synchronous
+ * return.
+ */
+#ifndef LBFGSB_OPS_H_
+#define LBFGSB_OPS_H_
+
+#include <stdint.h>
+#include "lbfgsb.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* a1 forward GEMV (PAPER.md:371 objective):
+ * q = M~ p over ALL columns, M~ the LSQ objective's operator (colscale /
+ * split applied).  p: n (= nvars) DEVICE, q: m DEVICE.  Errors: ARG, CUDA. */
+lbfgsb_err lbfgsb_op_gemv(const lbfgsb_objective* obj, const double* p, double* q,
+                          void* cuda_stream);
+
+/* a3 backward GEMV (row a3, without the iteration epilogue):
+ * g = M~^T r.  r: m DEVICE, g: n DEVICE.  Errors: ARG, CUDA. */
+lbfgsb_err lbfgsb_op_gemvt(const lbfgsb_objective* obj, const double* r, double* g,
+                           void* cuda_stream);
+
+/* Direction pipeline of one iteration (rows a4, a5, a6): working set Eq. (1)
+ * (PAPER.md:104-110), masked Gram + vector-free Alg. 3,
+ * d[S-bar] = 0, Alg. 2.
+ * Inputs: x, g (n, DEVICE) and nh <= m_hist curvature pairs S, Y
+ * (DEVICE, nh*n each, pair i at S + i*n, OLDEST first); bounds, eps and the
+ * screen norm come from the handle.  Outputs: free_out (n bytes, 1 = in
+ * S^k), d_out (n), p_out (n, the direction Alg. 2 returns), and (host)
+ * *projected (1 projected branch / 0 truncated), *gp = <g, p>,
+ * *amax (1 for projected, blocking ratio for truncated, +inf if none).
+ * Any output pointer may be NULL.  Errors: ARG, DIM, CUDA. */
+lbfgsb_err lbfgsb_op_direction(lbfgsb_t* h, const double* x, const double* g, int32_t nh,
+                               const double* S, const double* Y, uint8_t* free_out,
+                               double* d_out, double* p_out, int32_t* projected, double* gp,
+                               double* amax);
+
+/* One Armijo batch of the line search (row a2): for t = 0..ntrials-1,
+ * alpha_t = alpha0 * shrink^t (repeated multiplication), and
+ *   f_t = 1/2 || fma(alpha_t, q, r) ||^2 + phi(clip(fma(alpha_t, p, x)))
+ * (phi = c^T x + delta/2 ||x||^2 of the LSQ objective; reading R13).
+ * r, q: m DEVICE; x, p: n DEVICE; f_out (host) ntrials values.
+ * ntrials <= 16.  Errors: ARG, CUDA. */
+lbfgsb_err lbfgsb_op_trials(lbfgsb_t* h, const lbfgsb_objective* obj, const double* r,
+                            const double* q, const double* x, const double* p, double alpha0,
+                            int32_t ntrials, double* f_out);
+
+/* Device time of the hot-path GEMV launches of the solves run on this
+ * handle since the last reset (host): names[i] / ms[i] (summed event time)
+ * / launches[i], i < *count (<= cap).  Recorded only when opts.profile = 1
+ * (CUDA events on the handle's stream around each gemv / gemvT launch,
+ * inside the replayed graph as well).  reset != 0 clears the counters after
+ * reading.  Errors: ARG. */
+lbfgsb_err lbfgsb_profile_get(lbfgsb_t* h, int32_t cap, const char** names, double* ms,
+                              int64_t* launches, int32_t* count, int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBFGSB_OPS_H_ */

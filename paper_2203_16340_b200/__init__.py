@@ -1,0 +1,384 @@
+"""paper_2203_16340_b200 -- B200-native (sm_100a, fp64) hot path of the
+GPU-efficient, Cauchy-point-free L-BFGS-B of arXiv 2203.16340 (Alg. 1-3) and
+its augmented-Lagrangian wrapper (Alg. 4).
+
+This module is a THIN ctypes binding over the C ABI of ``include/lbfgsb.h``
+and ``include/lbfgsb_ops.h`` (``liblbfgsb.so``, built in-tree by
+``_build.py``): argument marshalling only, every step of the method runs in
+the library's CUDA kernels.  PyTorch is used for device memory and streams.
+There is no CPU fallback: if the extension is missing or no GPU is usable,
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+from . import _build
+
+__all__ = ["Options", "ALOptions", "Result", "ALResult", "Solver", "LSQObjective",
+           "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor"]
+
+_c_d, _c_i32, _c_i64, _c_vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
+
+CONVERGED, MAX_ITERS, LINESEARCH_FAILURE, AL_MAX_OUTER, AL_INNER_FAILURE = 0, 1, 2, 3, 4
+STATUS_NAMES = {0: "converged", 1: "max_iters", 2: "linesearch_failure", 3: "al_max_outer",
+                4: "al_inner_failure"}
+
+
+class _Opts(C.Structure):
+    _fields_ = [("eps", _c_d), ("c1", _c_d), ("shrink", _c_d), ("tol", _c_d),
+                ("max_backtracks", _c_i32), ("screen_full_norm", _c_i32),
+                ("check_every", _c_i32), ("use_graph", _c_i32), ("profile", _c_i32),
+                ("pad_", _c_i32), ("max_iters", _c_i64)]
+
+
+class _Res(C.Structure):
+    _fields_ = [("f", _c_d), ("pg_inf", _c_d), ("gfree_inf", _c_d), ("seconds", _c_d),
+                ("iters", _c_i64), ("n_fg", _c_i64), ("n_backtracks", _c_i64),
+                ("n_free", _c_i64), ("n_fallbacks", _c_i64), ("status", _c_i32),
+                ("last_branch", _c_i32)]
+
+
+class _AlOpts(C.Structure):
+    _fields_ = [("feas_tol", _c_d), ("rho0", _c_d), ("rho_factor", _c_d), ("rho_cap", _c_d),
+                ("max_outer", _c_i32), ("pad_", _c_i32)]
+
+
+class _AlCons(C.Structure):
+    _fields_ = [("m_eq", _c_i64), ("p_in", _c_i64), ("E", _c_vp), ("e", C.POINTER(_c_d)),
+                ("G", _c_vp), ("hv", C.POINTER(_c_d))]
+
+
+class _AlRes(C.Structure):
+    _fields_ = [("violation_inf", _c_d), ("f", _c_d), ("rho", _c_d), ("pg_inf", _c_d),
+                ("outer_iters", _c_i64), ("inner_iters_total", _c_i64), ("status", _c_i32),
+                ("pad_", _c_i32)]
+
+
+FG_CB = C.CFUNCTYPE(_c_i32, _c_vp, _c_vp, _c_vp, C.POINTER(_c_d), _c_vp)
+
+_lib = None
+
+
+class LbfgsbError(RuntimeError):
+    pass
+
+
+def load(build_if_needed: bool = True):
+    """Load liblbfgsb.so (building it with nvcc if sources changed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_needed and _build.needs_build():
+        _build.build()
+    if not os.path.exists(_build.LIB):
+        raise LbfgsbError(f"CUDA extension missing: {_build.LIB} (run _build.py); no CPU fallback")
+    L = C.CDLL(_build.LIB)
+    ip, vp = C.POINTER(_c_i32), _c_vp
+    L.lbfgsb_last_error.restype = C.c_char_p
+    L.lbfgsb_opts_default.argtypes = [C.POINTER(_Opts)]
+    L.al_opts_default.argtypes = [C.POINTER(_AlOpts)]
+    L.lbfgsb_create.argtypes = [_c_i64, _c_i32, vp, vp, C.POINTER(_Opts), vp, C.POINTER(vp)]
+    L.lbfgsb_create_sharded.argtypes = [_c_i64, _c_i64, _c_i32, vp, vp, C.POINTER(_Opts), vp, vp,
+                                        _c_i32, _c_i32, C.POINTER(vp)]
+    L.lbfgsb_destroy.argtypes = [vp]
+    L.lbfgsb_objective_lsq.argtypes = [vp, _c_i64, _c_i64, _c_i64, vp, _c_i32, vp, vp, _c_d,
+                                       C.POINTER(vp)]
+    L.lbfgsb_objective_callback.argtypes = [FG_CB, vp, C.POINTER(vp)]
+    L.lbfgsb_objective_free.argtypes = [vp]
+    L.lbfgsb_solve.argtypes = [vp, vp, vp, _c_d, C.POINTER(_Res)]
+    L.lbfgsb_solve_lsq_host.argtypes = [vp, vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(_Res)]
+    L.al_solve.argtypes = [vp, vp, C.POINTER(_AlCons), C.POINTER(_AlOpts), vp, vp, vp,
+                           C.POINTER(_AlRes)]
+    L.lbfgsb_op_gemv.argtypes = [vp, vp, vp, vp]
+    L.lbfgsb_op_gemvt.argtypes = [vp, vp, vp, vp]
+    L.lbfgsb_op_direction.argtypes = [vp, vp, vp, _c_i32, vp, vp, vp, vp, vp, ip,
+                                      C.POINTER(_c_d), C.POINTER(_c_d)]
+    L.lbfgsb_op_trials.argtypes = [vp, vp, vp, vp, vp, vp, _c_d, _c_i32, C.POINTER(_c_d)]
+    L.lbfgsb_profile_get.argtypes = [vp, _c_i32, C.POINTER(C.c_char_p), C.POINTER(_c_d),
+                                     C.POINTER(_c_i64), ip, _c_i32]
+    for name in ("lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
+                 "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
+                 "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
+                 "lbfgsb_profile_get"):
+        getattr(L, name).restype = _c_i32
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != 0:
+        msg = _lib.lbfgsb_last_error().decode()
+        raise LbfgsbError(f"liblbfgsb error {rc}: {msg}")
+
+
+def _ptr(t):
+    """Device pointer of a CUDA tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise LbfgsbError("expected a CUDA tensor (the library has no CPU path)")
+    if t.dtype.itemsize != 8 and t.dtype.is_floating_point:
+        raise LbfgsbError("fp64 tensors required")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream) if s.cuda_stream else None
+
+
+def colmajor(A, device="cuda"):
+    """numpy (m, n) array -> torch fp64 CUDA tensor (m, n) with column-major
+    strides (1, m), the layout of the C ABI."""
+    import numpy as np
+    import torch
+    At = np.ascontiguousarray(np.asarray(A, dtype=np.float64).T)   # (n, m) row-major
+    return torch.from_numpy(At).to(device).T
+
+
+@dataclass
+class Options:
+    eps: float = 1e-9
+    c1: float = 1e-4
+    shrink: float = 0.5
+    tol: float = 1e-6
+    max_backtracks: int = 50
+    screen_full_norm: bool = False
+    check_every: int = 8
+    use_graph: bool = True
+    profile: bool = False
+    max_iters: int = 10000
+
+    def _c(self):
+        return _Opts(self.eps, self.c1, self.shrink, self.tol, self.max_backtracks,
+                     int(bool(self.screen_full_norm)), self.check_every, int(bool(self.use_graph)),
+                     int(bool(self.profile)), 0, self.max_iters)
+
+
+@dataclass
+class ALOptions:
+    feas_tol: float = 1e-6
+    rho0: float = 1.0
+    rho_factor: float = 2.0
+    rho_cap: float = 1e12
+    max_outer: int = 100
+
+
+@dataclass
+class Result:
+    f: float
+    pg_inf: float
+    gfree_inf: float
+    seconds: float
+    iters: int
+    n_fg: int
+    n_backtracks: int
+    n_free: int
+    n_fallbacks: int
+    status: int
+    last_branch: int
+
+    @property
+    def status_name(self):
+        return STATUS_NAMES.get(self.status, str(self.status))
+
+
+@dataclass
+class ALResult:
+    violation_inf: float
+    f: float
+    rho: float
+    pg_inf: float
+    outer_iters: int
+    inner_iters_total: int
+    status: int
+    lam: list
+    mu: list
+
+
+class LSQObjective:
+    """f(x) = 1/2||M~x - b||^2 + c^T x + delta/2||x||^2, M~ = M diag(colscale)
+    or [M, -M] (split).  M: CUDA fp64 tensor (m, ncols) with column-major
+    strides (see ``colmajor``); b (m), c (nvars), colscale (ncols): CUDA fp64."""
+
+    def __init__(self, M, b=None, c=None, delta=0.0, colscale=None, split=False):
+        L = load()
+        if M.dim() != 2 or M.stride(0) != 1:
+            raise LbfgsbError("M must be (m, ncols) column-major: M.stride(0) == 1")
+        self.m, self.ncols = M.shape
+        self.ld = max(M.stride(1), self.m)
+        self.split = bool(split)
+        self.nvars = 2 * self.ncols if split else self.ncols
+        self._keep = (M, b, c, colscale)      # borrowed by the C objective
+        h = C.c_void_p()
+        _check(L.lbfgsb_objective_lsq(_ptr(M), self.m, self.ncols, self.ld, _ptr(colscale),
+                                      int(self.split), _ptr(b), _ptr(c), float(delta),
+                                      C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.lbfgsb_objective_free(self._h)
+            self._h = None
+
+
+class CallbackObjective:
+    """User objective: ``fg(x, g) -> f`` with x, g CUDA fp64 tensors (g written
+    in place).  Runs on the current torch stream."""
+
+    def __init__(self, fg, n):
+        import torch
+        L = load()
+        self.n = n
+        self.nvars = n
+        self._err = None
+
+        def _cb(user, xp, gp, fhost, stream):
+            try:
+                x = _wrap(xp, n)
+                g = _wrap(gp, n)
+                f = fg(x, g)
+                fhost[0] = float(f)
+                torch.cuda.current_stream().synchronize()
+                return 0
+            except Exception as e:  # noqa: BLE001 -- surfaced after the call
+                self._err = e
+                return 1
+
+        self._cb = FG_CB(_cb)
+        h = C.c_void_p()
+        _check(L.lbfgsb_objective_callback(self._cb, None, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.lbfgsb_objective_free(self._h)
+            self._h = None
+
+
+def _wrap(ptr, n):
+    """Non-owning torch view of a library device buffer (valid during the callback)."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_CAI(), device="cuda")
+
+
+class Solver:
+    """lbfgsb_create handle: n variables, box [lower, upper] (CUDA fp64 tensors
+    or None for -inf / +inf), m_hist curvature pairs."""
+
+    def __init__(self, n, m_hist=5, lower=None, upper=None, opts: Options | None = None,
+                 stream=None):
+        L = load()
+        self.n = int(n)
+        self.m_hist = int(m_hist)
+        self.opts = opts or Options()
+        o = self.opts._c()
+        h = C.c_void_p()
+        _check(L.lbfgsb_create(self.n, self.m_hist, _ptr(lower), _ptr(upper), C.byref(o),
+                               _stream_ptr(stream), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.lbfgsb_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def solve(self, obj, x, tol=0.0) -> Result:
+        """Alg. 1 from x (CUDA fp64 tensor, updated in place with x*)."""
+        r = _Res()
+        rc = _lib.lbfgsb_solve(self._h, obj._h, _ptr(x), float(tol), C.byref(r))
+        if isinstance(obj, CallbackObjective) and obj._err is not None:
+            e, obj._err = obj._err, None
+            raise LbfgsbError(f"callback raised: {e!r}") from e
+        _check(rc)
+        return Result(r.f, r.pg_inf, r.gfree_inf, r.seconds, r.iters, r.n_fg, r.n_backtracks,
+                      r.n_free, r.n_fallbacks, r.status, r.last_branch)
+
+    def solve_lsq_host(self, M_host, b_host, x_host, tol=0.0) -> Result:
+        """lbfgsb_solve_lsq_host: numpy (pinned or pageable) buffers in/out.
+        M_host: (m, n) Fortran-ordered float64; b_host (m); x_host (n, in/out)."""
+        import numpy as np
+        assert M_host.flags.f_contiguous and M_host.dtype == np.float64
+        assert x_host.flags.c_contiguous and x_host.dtype == np.float64
+        m, n = M_host.shape
+        r = _Res()
+        _check(_lib.lbfgsb_solve_lsq_host(self._h, C.c_void_p(M_host.ctypes.data), m, n,
+                                          C.c_void_p(b_host.ctypes.data) if b_host is not None else None,
+                                          C.c_void_p(x_host.ctypes.data), float(tol), C.byref(r)))
+        return Result(r.f, r.pg_inf, r.gfree_inf, r.seconds, r.iters, r.n_fg, r.n_backtracks,
+                      r.n_free, r.n_fallbacks, r.status, r.last_branch)
+
+    def al_solve(self, obj, x, E=None, e=None, G=None, hv=None,
+                 al_opts: ALOptions | None = None) -> ALResult:
+        """Alg. 4 with linear constraints E^T x = e, G^T x <= hv; E (n, m_eq) and
+        G (n, p_in) CUDA fp64 column-major (column k contiguous)."""
+        import torch
+        ao = al_opts or ALOptions()
+        c_ao = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer, 0)
+        m_eq = 0 if E is None else (E.shape[1] if E.dim() == 2 else 1)
+        p_in = 0 if G is None else (G.shape[1] if G.dim() == 2 else 1)
+        Ec = None if E is None else E.reshape(self.n, m_eq).T.contiguous()   # (m_eq, n) rows = columns
+        Gc = None if G is None else G.reshape(self.n, p_in).T.contiguous()
+        e_arr = (_c_d * max(m_eq, 1))(*([float(v) for v in torch.as_tensor(e).flatten()] if m_eq else [0.0]))
+        h_arr = (_c_d * max(p_in, 1))(*([float(v) for v in torch.as_tensor(hv).flatten()] if p_in else [0.0]))
+        cons = _AlCons(m_eq, p_in, _ptr(Ec), e_arr, _ptr(Gc), h_arr)
+        lam = (_c_d * max(m_eq, 1))()
+        mu = (_c_d * max(p_in, 1))()
+        r = _AlRes()
+        _check(_lib.al_solve(self._h, obj._h, C.byref(cons), C.byref(c_ao), _ptr(x), lam, mu,
+                             C.byref(r)))
+        return ALResult(r.violation_inf, r.f, r.rho, r.pg_inf, r.outer_iters, r.inner_iters_total,
+                        r.status, list(lam)[:m_eq], list(mu)[:p_in])
+
+    # ---- op-level entry points (lbfgsb_ops.h) ----
+    def op_direction(self, x, g, S=None, Y=None):
+        """Working set + vector-free Alg. 3 + Alg. 2 on (x, g, pairs oldest first)."""
+        import torch
+        nh = 0 if S is None else S.shape[0]
+        fr = torch.empty(self.n, dtype=torch.uint8, device=x.device)
+        d = torch.empty_like(x)
+        p = torch.empty_like(x)
+        br = _c_i32()
+        gp, am = _c_d(), _c_d()
+        Sc = None if S is None else S.contiguous()
+        Yc = None if Y is None else Y.contiguous()
+        _check(_lib.lbfgsb_op_direction(self._h, _ptr(x), _ptr(g), nh, _ptr(Sc), _ptr(Yc),
+                                        _ptr(fr), _ptr(d), _ptr(p), C.byref(br), C.byref(gp),
+                                        C.byref(am)))
+        return dict(free=fr.bool(), d=d, p=p, projected=bool(br.value), gp=gp.value, amax=am.value)
+
+    def op_trials(self, obj, r, q, x, p, alpha0, ntrials=16):
+        f = (_c_d * ntrials)()
+        _check(_lib.lbfgsb_op_trials(self._h, obj._h, _ptr(r), _ptr(q), _ptr(x), _ptr(p),
+                                     float(alpha0), ntrials, f))
+        return list(f)
+
+    def profile(self, reset=False):
+        names = (C.c_char_p * 8)()
+        ms = (_c_d * 8)()
+        cnt = (_c_i64 * 8)()
+        k = _c_i32()
+        _check(_lib.lbfgsb_profile_get(self._h, 8, names, ms, cnt, C.byref(k), int(bool(reset))))
+        return {names[i].decode(): (ms[i], cnt[i]) for i in range(k.value)}
+
+
+def op_gemv(obj: LSQObjective, p, q, stream=None):
+    """q = M~ p (the a1 forward GEMV kernel over all columns)."""
+    _check(load().lbfgsb_op_gemv(obj._h, _ptr(p), _ptr(q), _stream_ptr(stream)))
+    return q
+
+
+def op_gemvt(obj: LSQObjective, r, g, stream=None):
+    """g = M~^T r (the a3 backward GEMV kernel, no epilogue)."""
+    _check(load().lbfgsb_op_gemvt(obj._h, _ptr(r), _ptr(g), _stream_ptr(stream)))
+    return g

@@ -1,0 +1,923 @@
+// solver.cu -- host control of liblbfgsb: the C ABI of include/lbfgsb.h and
+// include/lbfgsb_ops.h.  Drives the device kernels of kernels.cu; every step
+// of the method runs on the GPU, the host only sequences launches, replays
+// CUDA graphs and reads the 300-byte control block every check_every
+// iterations.  No CPU fallback exists: without a device every call returns
+// LBFGSB_ERR_CUDA.
+//
+// Citations: PAPER.md:N (paper LaTeX line), R<k>.
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "impl.cuh"
+#include "../../include/lbfgsb_ops.h"
+
+#ifdef LBFGSB_WITH_NCCL
+#include <nccl.h>
+#endif
+
+using namespace lb;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err = "no error";
+
+static lbfgsb_err fail(lbfgsb_err e, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return e;
+}
+
+#define CK(expr)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? LBFGSB_ERR_OOM : LBFGSB_ERR_CUDA, \
+                        "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define TRY(expr)                                                                       \
+    do {                                                                                \
+        lbfgsb_err t_ = (expr);                                                         \
+        if (t_ != LBFGSB_OK) return t_;                                                 \
+    } while (0)
+
+extern "C" const char* lbfgsb_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ objects
+struct lbfgsb_objective {
+    int kind;                       // 0 LSQ, 1 callback
+    const double* M;
+    int64_t m, ncols, ld;
+    const double* colscale;
+    int split;
+    const double* b;
+    const double* c;
+    double delta;
+    lbfgsb_fg_cb fg;
+    void* user;
+};
+
+namespace {
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    lbfgsb_err ensure(size_t need)
+    {
+        if (need <= bytes && p) return LBFGSB_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (need == 0) need = 16;
+        cudaError_t e = cudaMalloc(&p, need);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return fail(LBFGSB_ERR_OOM, "cudaMalloc(%zu): %s", need, cudaGetErrorString(e));
+        }
+        bytes = need;
+        return LBFGSB_OK;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    double* d() const { return static_cast<double*>(p); }
+};
+constexpr int kPerIter = 9;   // kernel launches per device iteration
+}  // namespace
+
+struct lbfgsb_t {
+    int64_t n = 0;
+    int mh = 0;
+    lbfgsb_opts o{};
+    cudaStream_t st = nullptr;
+    // n-sized
+    DevBuf l, u, x, g, d, pp, pt, S, Y, mask, xt, gt;
+    DevBuf gram_part, dir_part, kkt_part;
+    // m-sized (grown on demand)
+    DevBuf r, q, qpart, ls_part, sep_part, fout;
+    // host-buffer solve staging
+    DevBuf Mh, bh, xh;
+    Ctrl* ctrl = nullptr;           // device
+    Ctrl* hc = nullptr;             // pinned host mirror
+    // graph cache
+    cudaGraphExec_t gexec = nullptr;
+    Prob gkey{};
+    int gchunk = 0;
+    // profiling
+    std::vector<cudaEvent_t> ev;    // 4 per iteration in a chunk: fwd0 fwd1 bwd0 bwd1
+    double prof_ms[2] = {0, 0};
+    int64_t prof_n[2] = {0, 0};
+    int64_t launches = 0;
+    bool own_stream = false;
+    // sharding
+    int rank = 0, nranks = 1;
+    int64_t n_global = 0;
+#ifdef LBFGSB_WITH_NCCL
+    ncclComm_t comm = nullptr;
+#endif
+};
+
+// ------------------------------------------------------------------ defaults
+extern "C" void lbfgsb_opts_default(lbfgsb_opts* o)
+{
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->eps = 1e-9;             // R1
+    o->c1 = 1e-4;              // R11
+    o->shrink = 0.5;           // R11
+    o->tol = 1e-6;             // R15
+    o->max_backtracks = 50;    // R11
+    o->screen_full_norm = 0;   // R3
+    o->check_every = 8;
+    o->use_graph = 1;
+    o->profile = 0;
+    o->max_iters = 10000;
+}
+
+extern "C" void al_opts_default(al_opts* o)
+{
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->feas_tol = 1e-6;
+    o->rho0 = 1.0;
+    o->rho_factor = 2.0;
+    o->rho_cap = 1e12;
+    o->max_outer = 100;
+}
+
+// ------------------------------------------------------------------ kernels for bounds
+namespace {
+__global__ void k_fill_bounds(double* l, double* u, const double* lin, const double* uin, int64_t n,
+                              int* bad)
+{
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double a = lin ? lin[j] : -INFINITY;
+        const double b = uin ? uin[j] : INFINITY;
+        l[j] = a;
+        u[j] = b;
+        if (!(a <= b)) atomicExch(bad, 1);      // l > u or NaN
+    }
+}
+}  // namespace
+
+// ------------------------------------------------------------------ create / destroy
+static lbfgsb_err alloc_n(lbfgsb_t* h)
+{
+    const size_t nb = sizeof(double) * (size_t)h->n;
+    TRY(h->l.ensure(nb)); TRY(h->u.ensure(nb)); TRY(h->x.ensure(nb)); TRY(h->g.ensure(nb));
+    TRY(h->d.ensure(nb)); TRY(h->pp.ensure(nb)); TRY(h->pt.ensure(nb));
+    TRY(h->S.ensure(nb * h->mh)); TRY(h->Y.ensure(nb * h->mh));
+    TRY(h->mask.ensure((size_t)h->n));
+    const int64_t G1max = 2LL * sm_count();
+    TRY(h->gram_part.ensure(sizeof(double) * G1max * GRAM_STRIDE));
+    TRY(h->dir_part.ensure(sizeof(double) * G1max * 4));
+    TRY(h->kkt_part.ensure(sizeof(double) * G1max * 3));
+    CK(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
+    CK(cudaMallocHost(&h->hc, sizeof(Ctrl)));
+    std::memset(h->hc, 0, sizeof(Ctrl));
+    return LBFGSB_OK;
+}
+
+static lbfgsb_err create_common(int64_t n, int32_t m_hist, const double* lower, const double* upper,
+                                const lbfgsb_opts* opts, void* stream, lbfgsb_t** out)
+{
+    if (!out) return fail(LBFGSB_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (n <= 0) return fail(LBFGSB_ERR_DIM, "n = %lld must be positive", (long long)n);
+    if (m_hist < 1 || m_hist > LBFGSB_MAX_HIST)
+        return fail(LBFGSB_ERR_ARG, "m_hist = %d outside [1, %d]", m_hist, LBFGSB_MAX_HIST);
+    lbfgsb_opts o;
+    lbfgsb_opts_default(&o);
+    if (opts) o = *opts;
+    if (!(o.eps > 0) || !(o.c1 > 0 && o.c1 < 1) || !(o.shrink > 0 && o.shrink < 1) || !(o.tol >= 0) ||
+        o.max_backtracks < 0 || o.max_iters < 0)
+        return fail(LBFGSB_ERR_ARG, "invalid option value");
+    if (o.check_every < 1) o.check_every = 1;
+    if (o.check_every > 64) o.check_every = 64;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(LBFGSB_ERR_CUDA, "no CUDA device available (the library has no CPU path)");
+    init_kernels();
+    lbfgsb_t* h = new lbfgsb_t();
+    h->n = n;
+    h->n_global = n;
+    h->mh = m_hist;
+    h->o = o;
+    h->st = static_cast<cudaStream_t>(stream);
+    if (!h->st) {
+        // the legacy default stream cannot be graph-captured: use a private
+        // BLOCKING stream, which the legacy stream implicitly orders with
+        if (cudaStreamCreate(&h->st) != cudaSuccess) {
+            delete h;
+            return fail(LBFGSB_ERR_CUDA, "cudaStreamCreate failed");
+        }
+        h->own_stream = true;
+    }
+    lbfgsb_err e = alloc_n(h);
+    if (e != LBFGSB_OK) { lbfgsb_destroy(h); return e; }
+    int* bad = nullptr;
+    cudaError_t ce = cudaMalloc(&bad, sizeof(int));
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(bad, 0, sizeof(int), h->st);
+    if (ce == cudaSuccess) {
+        k_fill_bounds<<<256, 256, 0, h->st>>>(h->l.d(), h->u.d(), lower, upper, n, bad);
+        ce = cudaGetLastError();
+    }
+    int hbad = 0;
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->st);
+    if (bad) cudaFree(bad);
+    if (ce != cudaSuccess) {
+        lbfgsb_destroy(h);
+        return fail(LBFGSB_ERR_CUDA, "bounds setup: %s", cudaGetErrorString(ce));
+    }
+    if (hbad) { lbfgsb_destroy(h); return fail(LBFGSB_ERR_BOUNDS, "l_i > u_i or NaN bound"); }
+    *out = h;
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_create(int64_t n, int32_t m_hist, const double* lower,
+                                    const double* upper, const lbfgsb_opts* opts,
+                                    void* cuda_stream, lbfgsb_t** out)
+{
+    return create_common(n, m_hist, lower, upper, opts, cuda_stream, out);
+}
+
+extern "C" void lbfgsb_destroy(lbfgsb_t* h)
+{
+    if (!h) return;
+    if (h->st) cudaStreamSynchronize(h->st);
+    else cudaDeviceSynchronize();
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    for (auto e : h->ev) cudaEventDestroy(e);
+    DevBuf* bufs[] = {&h->l, &h->u, &h->x, &h->g, &h->d, &h->pp, &h->pt, &h->S, &h->Y, &h->mask,
+                      &h->xt, &h->gt, &h->gram_part, &h->dir_part, &h->kkt_part, &h->r, &h->q,
+                      &h->qpart, &h->ls_part, &h->sep_part, &h->fout, &h->Mh, &h->bh, &h->xh};
+    for (DevBuf* b : bufs) b->release();
+    if (h->ctrl) cudaFree(h->ctrl);
+    if (h->hc) cudaFreeHost(h->hc);
+#ifdef LBFGSB_WITH_NCCL
+    if (h->comm) ncclCommDestroy(h->comm);
+#endif
+    if (h->own_stream) cudaStreamDestroy(h->st);
+    delete h;
+}
+
+// ------------------------------------------------------------------ objectives
+extern "C" lbfgsb_err lbfgsb_objective_lsq(const double* M, int64_t m, int64_t ncols, int64_t ld,
+                                           const double* colscale, int32_t split, const double* b,
+                                           const double* c, double delta, lbfgsb_objective** out)
+{
+    if (!out) return fail(LBFGSB_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (!M) return fail(LBFGSB_ERR_ARG, "M is NULL");
+    if (m <= 0 || ncols <= 0 || ld < m) return fail(LBFGSB_ERR_DIM, "bad shape m=%lld ncols=%lld ld=%lld",
+                                                    (long long)m, (long long)ncols, (long long)ld);
+    if (m > (1LL << 40) || ncols > (1LL << 31) - 1) return fail(LBFGSB_ERR_DIM, "shape too large");
+    if (split && colscale) return fail(LBFGSB_ERR_ARG, "split and colscale are exclusive");
+    if (!std::isfinite(delta)) return fail(LBFGSB_ERR_ARG, "delta not finite");
+    auto* o = new lbfgsb_objective();
+    o->kind = 0;
+    o->M = M; o->m = m; o->ncols = ncols; o->ld = ld;
+    o->colscale = colscale; o->split = split ? 1 : 0;
+    o->b = b; o->c = c; o->delta = delta;
+    *out = o;
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_objective_callback(lbfgsb_fg_cb fg, void* user, lbfgsb_objective** out)
+{
+    if (!out) return fail(LBFGSB_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (!fg) return fail(LBFGSB_ERR_ARG, "fg is NULL");
+    auto* o = new lbfgsb_objective();
+    o->kind = 1;
+    o->fg = fg;
+    o->user = user;
+    *out = o;
+    return LBFGSB_OK;
+}
+
+extern "C" void lbfgsb_objective_free(lbfgsb_objective* obj) { delete obj; }
+
+// ------------------------------------------------------------------ problem setup
+static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Fill the kernel argument block for (handle, objective) and make sure the
+// m-sized workspace exists.  ncons constraint columns are attached by al_solve.
+static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
+{
+    std::memset(&P, 0, sizeof P);
+    const int sms = sm_count();
+    P.n = h->n;
+    P.l = h->l.d(); P.u = h->u.d();
+    P.eps = h->o.eps; P.c1 = h->o.c1; P.shrink = h->o.shrink;
+    P.max_bt = h->o.max_backtracks; P.screen_full = h->o.screen_full_norm; P.mh = h->mh;
+    P.max_iters = h->o.max_iters;
+    P.x = h->x.d(); P.g = h->g.d(); P.d = h->d.d(); P.pp = h->pp.d(); P.pt = h->pt.d();
+    P.S = h->S.d(); P.Y = h->Y.d(); P.mask = static_cast<uint8_t*>(h->mask.p);
+    P.gram_part = h->gram_part.d(); P.dir_part = h->dir_part.d(); P.kkt_part = h->kkt_part.d();
+    P.ctrl = h->ctrl;
+    P.G1 = (int)clampi(cdiv(h->n, TILE), 1, 2LL * sms);
+    if (ob && ob->kind == 0) {
+        const int64_t nv = ob->split ? 2 * ob->ncols : ob->ncols;
+        if (nv != h->n)
+            return fail(LBFGSB_ERR_DIM, "objective has %lld variables, handle %lld", (long long)nv,
+                        (long long)h->n);
+        P.m = ob->m; P.ncols = ob->ncols; P.ld = ob->ld; P.M = ob->M;
+        P.colscale = ob->colscale; P.split = ob->split; P.b = ob->b; P.c = ob->c; P.delta = ob->delta;
+        P.fwd_rb = (int)cdiv(P.m, FWD_ROWS);
+        int64_t cc = clampi(cdiv(4LL * sms, P.fwd_rb), 1, clampi(cdiv(P.ncols, 32), 1, 1 << 20));
+        P.fwd_chunk = cdiv(P.ncols, cc);
+        P.fwd_cc = (int)cdiv(P.ncols, P.fwd_chunk);
+        P.GL = (int)clampi(cdiv(P.m, NT * 8), 1, 2LL * sms);
+        P.GS = 0;
+        P.bwd_blocks = (int)cdiv(P.ncols, BWD_NB);
+        const size_t mb = sizeof(double) * (size_t)P.m;
+        TRY(h->r.ensure(mb)); TRY(h->q.ensure(mb));
+        TRY(h->qpart.ensure(mb * P.fwd_cc));
+        TRY(h->ls_part.ensure(sizeof(double) * (size_t)P.GL * KT));
+        TRY(h->sep_part.ensure(sizeof(double) * (size_t)sms * KT * NSEP));
+        TRY(h->fout.ensure(sizeof(double) * KT));
+        P.r = h->r.d(); P.q = h->q.d(); P.qpart = h->qpart.d();
+        P.ls_part = h->ls_part.d(); P.sep_part = h->sep_part.d();
+    }
+    return LBFGSB_OK;
+}
+
+static void set_sep(Prob& P, int sms)
+{
+    const bool has_sep = P.c || P.delta != 0.0 || (P.n_eq + P.n_in) > 0;
+    P.GS = has_sep ? (int)clampi(cdiv(P.n, NT * 8), 1, sms) : 0;
+}
+
+static lbfgsb_err ctrl_to_dev(lbfgsb_t* h)
+{
+    CK(cudaMemcpyAsync(h->ctrl, h->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
+    return LBFGSB_OK;
+}
+static lbfgsb_err ctrl_to_host(lbfgsb_t* h)
+{
+    CK(cudaMemcpyAsync(h->hc, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ iteration sequence
+enum Phase { PH_GRAM = 0, PH_RECUR, PH_DIR, PH_BRANCH, PH_FWD, PH_LS, PH_DECIDE, PH_RUPD, PH_BWD };
+
+static void rec_event(lbfgsb_t* h, int idx)
+{
+    if (!h->o.profile || idx < 0) return;
+    cudaEventRecordWithFlags(h->ev[idx], h->st, cudaEventRecordExternal);
+}
+
+// Launch one LSQ iteration from `from`; ev_base >= 0 records profile events.
+static void launch_iteration(lbfgsb_t* h, const Prob& P, int from, int ev_base)
+{
+    cudaStream_t st = h->st;
+    int n = 0;
+    if (from <= PH_GRAM) { launch_gram(P, st, 0); ++n; }
+    if (from <= PH_RECUR) { launch_recur(P, st, 0); ++n; }
+    if (from <= PH_DIR) { launch_dir(P, st, 0); ++n; }
+    if (from <= PH_BRANCH) { launch_branch(P, st, 0); ++n; }
+    if (from <= PH_FWD) {
+        rec_event(h, ev_base >= 0 ? ev_base + 0 : -1);
+        launch_fwd(P, st, FWD_ITER, nullptr); ++n;
+        rec_event(h, ev_base >= 0 ? ev_base + 1 : -1);
+    }
+    if (from <= PH_LS) { launch_ls(P, st, LS_ITER0, nullptr); ++n; }
+    if (from <= PH_DECIDE) { launch_ls_decide(P, st, LS_ITER0, nullptr, 0); ++n; }
+    if (from <= PH_RUPD) { launch_rupd(P, st); ++n; }
+    if (from <= PH_BWD) {
+        rec_event(h, ev_base >= 0 ? ev_base + 2 : -1);
+        launch_bwd(P, st, BWD_ITER, nullptr, nullptr); ++n;
+        rec_event(h, ev_base >= 0 ? ev_base + 3 : -1);
+    }
+    h->launches += n;
+}
+
+// Setup / refresh at x (PAPER.md:65 x^0 feasible; R13 final refresh):
+// x = clip(x), r = M~x - b, f, g = grad f(x).
+static void launch_refresh(lbfgsb_t* h, const Prob& P, bool clip)
+{
+    cudaStream_t st = h->st;
+    if (clip) { launch_clip(P, st); h->launches++; }
+    launch_fwd(P, st, FWD_X, P.x);
+    launch_resid(P, st, 1, P.r);
+    launch_ls(P, st, LS_SETUP, P.x);
+    launch_ls_decide(P, st, LS_SETUP, nullptr, 1);
+    launch_bwd(P, st, BWD_SETUP, nullptr, nullptr);
+    h->launches += 5;
+}
+
+static lbfgsb_err ensure_events(lbfgsb_t* h)
+{
+    const size_t need = (size_t)4 * h->o.check_every;
+    while (h->ev.size() < need) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        h->ev.push_back(e);
+    }
+    return LBFGSB_OK;
+}
+
+static lbfgsb_err run_chunk(lbfgsb_t* h, const Prob& P)
+{
+    const int chunk = h->o.check_every;
+    if (h->o.use_graph) {
+        if (!h->gexec || std::memcmp(&h->gkey, &P, sizeof(Prob)) != 0 || h->gchunk != chunk) {
+            if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+            cudaGraph_t g = nullptr;
+            CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+            const int64_t l0 = h->launches;
+            for (int i = 0; i < chunk; ++i) launch_iteration(h, P, PH_GRAM, h->o.profile ? 4 * i : -1);
+            h->launches = l0;
+            cudaError_t e = cudaStreamEndCapture(h->st, &g);
+            if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+            e = cudaGraphInstantiate(&h->gexec, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+            h->gkey = P;
+            h->gchunk = chunk;
+        }
+        CK(cudaGraphLaunch(h->gexec, h->st));
+        h->launches += (int64_t)kPerIter * chunk;
+    } else {
+        for (int i = 0; i < chunk; ++i) launch_iteration(h, P, PH_GRAM, h->o.profile ? 4 * i : -1);
+    }
+    CK(cudaGetLastError());
+    return LBFGSB_OK;
+}
+
+static void collect_profile(lbfgsb_t* h, int64_t iters_done)
+{
+    if (!h->o.profile) return;
+    const int64_t c = iters_done < h->o.check_every ? iters_done : h->o.check_every;
+    for (int64_t i = 0; i < c; ++i) {
+        float a = 0.f, b = 0.f;
+        if (cudaEventElapsedTime(&a, h->ev[4 * i + 0], h->ev[4 * i + 1]) == cudaSuccess) {
+            h->prof_ms[0] += a; h->prof_n[0] += 1;
+        }
+        if (cudaEventElapsedTime(&b, h->ev[4 * i + 2], h->ev[4 * i + 3]) == cudaSuccess) {
+            h->prof_ms[1] += b; h->prof_n[1] += 1;
+        }
+    }
+    cudaGetLastError();
+}
+
+static void init_ctrl(lbfgsb_t* h, double tol)
+{
+    Ctrl* c = h->hc;
+    double lam[MAXC], rhs[MAXC], rho = c->rho;
+    std::memcpy(lam, c->lam, sizeof lam);
+    std::memcpy(rhs, c->rhs, sizeof rhs);
+    std::memset(c, 0, sizeof(Ctrl));
+    c->head = h->mh - 1;          // first stored pair goes to slot 0
+    c->tol = tol;
+    c->rho = rho > 0 ? rho : 1.0;
+    std::memcpy(c->lam, lam, sizeof lam);
+    std::memcpy(c->rhs, rhs, sizeof rhs);
+}
+
+// Alg. 1 on an LSQ objective; x (device) in/out.  AL params already in h->hc.
+static lbfgsb_err solve_lsq(lbfgsb_t* h, const Prob& P, double* x_user, double tol, lbfgsb_result* res)
+{
+    auto t0 = std::chrono::steady_clock::now();
+    if (x_user != P.x) CK(cudaMemcpyAsync(P.x, x_user, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
+    init_ctrl(h, tol);
+    TRY(ctrl_to_dev(h));
+    launch_refresh(h, P, true);
+    CK(cudaGetLastError());
+    TRY(ctrl_to_host(h));
+    if (h->hc->nonfinite) return fail(LBFGSB_ERR_NONFINITE, "f(x0) is not finite");
+    h->hc->n_fg = 1;
+    TRY(ctrl_to_dev(h));
+    if (h->o.profile) TRY(ensure_events(h));
+
+    const int64_t guard = h->o.max_iters + 16;
+    int64_t loops = 0;
+    for (;;) {
+        const long long k0 = h->hc->k;
+        TRY(run_chunk(h, P));
+        TRY(ctrl_to_host(h));
+        collect_profile(h, h->hc->k - k0);
+        if (h->hc->done) break;
+        if (++loops > guard) return fail(LBFGSB_ERR_CUDA, "solver loop did not terminate");
+        // ---- stall handling (rare): finish the stalled iteration on the host's cue
+        while (h->hc->stall && !h->hc->done) {
+            const int s = h->hc->stall;
+            h->hc->stall = 0;
+            if (s == ST_FALLBACK) {
+                // R14: clear the history, steepest descent on S, redo Alg. 2 + search
+                h->hc->fallback = 1;
+                h->hc->nh = 0;
+                h->hc->n_fallbacks += 1;
+                TRY(ctrl_to_dev(h));
+                launch_iteration(h, P, PH_GRAM, -1);
+            } else {  // ST_LS_CONT: next batch of Armijo trials
+                TRY(ctrl_to_dev(h));
+                launch_ls(P, h->st, LS_ITER_NEXT, nullptr);
+                launch_ls_decide(P, h->st, LS_ITER_NEXT, nullptr, 0);
+                launch_rupd(P, h->st);
+                launch_bwd(P, h->st, BWD_ITER, nullptr, nullptr);
+                h->launches += 4;
+            }
+            CK(cudaGetLastError());
+            TRY(ctrl_to_host(h));
+        }
+        if (h->hc->done) break;
+    }
+    const Ctrl fin = *h->hc;
+    // final refresh: r = M~x - b, g, f; KKT report (R13, R15)
+    launch_refresh(h, P, false);
+    launch_kkt(P, h->st);
+    h->launches += 2;
+    CK(cudaGetLastError());
+    TRY(ctrl_to_host(h));
+    if (x_user != P.x) CK(cudaMemcpyAsync(x_user, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    auto t1 = std::chrono::steady_clock::now();
+    if (res) {
+        std::memset(res, 0, sizeof *res);
+        res->f = h->hc->f;
+        res->pg_inf = h->hc->pg;
+        res->gfree_inf = h->hc->gfree;
+        res->n_free = h->hc->nfree;
+        res->iters = fin.k;
+        res->n_fg = fin.n_fg;
+        res->n_backtracks = fin.n_bt;
+        res->n_fallbacks = fin.n_fallbacks;
+        res->status = fin.status;
+        res->last_branch = fin.branch;
+        res->seconds = std::chrono::duration<double>(t1 - t0).count();
+    }
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ callback objective
+// Host-driven Alg. 1 for user objectives: the direction pipeline runs on the
+// device kernels; each Armijo trial calls the user's fg.
+static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_user, double tol,
+                           lbfgsb_result* res)
+{
+    auto t0 = std::chrono::steady_clock::now();
+    Prob P;
+    TRY(make_prob(h, ob, P));
+    const size_t nb = sizeof(double) * h->n;
+    TRY(h->xt.ensure(nb));
+    TRY(h->gt.ensure(nb));
+    cudaStream_t st = h->st;
+    CK(cudaMemcpyAsync(P.x, x_user, nb, cudaMemcpyDeviceToDevice, st));
+    init_ctrl(h, tol);
+    launch_clip(P, st);
+    CK(cudaGetLastError());
+    double f = 0.0;
+    if (ob->fg(ob->user, P.x, P.g, &f, st) != 0) return fail(LBFGSB_ERR_CALLBACK, "callback failed at x0");
+    if (!std::isfinite(f)) return fail(LBFGSB_ERR_NONFINITE, "f(x0) is not finite");
+    Ctrl* c = h->hc;
+    c->f = f;
+    c->n_fg = 1;
+    TRY(ctrl_to_dev(h));
+    for (;;) {
+        launch_gram(P, st, 0);
+        launch_recur(P, st, 0);
+        launch_dir(P, st, 0);
+        launch_branch(P, st, 0);
+        h->launches += 4;
+        CK(cudaGetLastError());
+        TRY(ctrl_to_host(h));
+        if (c->done) break;
+        if (c->stall == ST_FALLBACK) {
+            c->stall = 0; c->fallback = 1; c->nh = 0; c->n_fallbacks += 1;
+            TRY(ctrl_to_dev(h));
+            continue;
+        }
+        double a = c->alpha0, ft = 0.0;
+        bool acc = false;
+        for (int t = 0; t <= h->o.max_backtracks; ++t) {
+            if (t > 0) a = a * h->o.shrink;
+            launch_cb_trial(P, st, a, h->xt.d());
+            h->launches += 1;
+            if (ob->fg(ob->user, h->xt.d(), h->gt.d(), &ft, st) != 0)
+                return fail(LBFGSB_ERR_CALLBACK, "callback failed");
+            c->n_fg += 1;
+            if (ft <= c->f + h->o.c1 * a * c->gp) { acc = true; break; }
+            c->n_bt += 1;
+        }
+        if (!acc) {
+            if (c->fallback) { c->done = 1; c->status = S_LS_FAIL; break; }
+            c->fallback = 1; c->nh = 0; c->n_fallbacks += 1;
+            TRY(ctrl_to_dev(h));
+            continue;
+        }
+        const int head = (c->head + 1) % h->mh;
+        launch_cb_commit(P, st, h->xt.d(), h->gt.d(), head);
+        h->launches += 1;
+        c->head = head; c->slot = head;
+        c->nh = c->nh + 1 < h->mh ? c->nh + 1 : h->mh;
+        c->k += 1; c->fallback = 0; c->f = ft; c->alpha = a;
+        TRY(ctrl_to_dev(h));
+    }
+    const Ctrl fin = *c;
+    launch_kkt(P, st);
+    h->launches += 2;
+    CK(cudaGetLastError());
+    TRY(ctrl_to_host(h));
+    CK(cudaMemcpyAsync(x_user, P.x, nb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    auto t1 = std::chrono::steady_clock::now();
+    if (res) {
+        std::memset(res, 0, sizeof *res);
+        res->f = fin.f;
+        res->pg_inf = h->hc->pg;
+        res->gfree_inf = h->hc->gfree;
+        res->n_free = h->hc->nfree;
+        res->iters = fin.k; res->n_fg = fin.n_fg; res->n_backtracks = fin.n_bt;
+        res->n_fallbacks = fin.n_fallbacks; res->status = fin.status; res->last_branch = fin.branch;
+        res->seconds = std::chrono::duration<double>(t1 - t0).count();
+    }
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_solve(lbfgsb_t* h, const lbfgsb_objective* obj, double* x, double tol,
+                                   lbfgsb_result* res)
+{
+    if (!h || !obj || !x) return fail(LBFGSB_ERR_ARG, "NULL handle, objective or x");
+    const double t = tol > 0 ? tol : h->o.tol;
+    if (obj->kind == 1) return solve_cb(h, obj, x, t, res);
+    Prob P;
+    TRY(make_prob(h, obj, P));
+    set_sep(P, sm_count());
+    h->hc->rho = 1.0;
+    std::memset(h->hc->lam, 0, sizeof h->hc->lam);
+    std::memset(h->hc->rhs, 0, sizeof h->hc->rhs);
+    return solve_lsq(h, P, x, t, res);
+}
+
+extern "C" lbfgsb_err lbfgsb_solve_lsq_host(lbfgsb_t* h, const double* M_host, int64_t m, int64_t ncols,
+                                            const double* b_host, double* x_host, double tol,
+                                            lbfgsb_result* res)
+{
+    if (!h || !M_host || !x_host) return fail(LBFGSB_ERR_ARG, "NULL handle, M or x");
+    if (m <= 0 || ncols != h->n) return fail(LBFGSB_ERR_DIM, "shape mismatch");
+    const size_t mb = sizeof(double) * (size_t)m * (size_t)ncols;
+    TRY(h->Mh.ensure(mb));
+    TRY(h->bh.ensure(sizeof(double) * (size_t)m));
+    TRY(h->xh.ensure(sizeof(double) * (size_t)ncols));
+    CK(cudaMemcpyAsync(h->Mh.p, M_host, mb, cudaMemcpyHostToDevice, h->st));
+    if (b_host) CK(cudaMemcpyAsync(h->bh.p, b_host, sizeof(double) * m, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->xh.p, x_host, sizeof(double) * ncols, cudaMemcpyHostToDevice, h->st));
+    lbfgsb_objective ob{};
+    ob.kind = 0; ob.M = h->Mh.d(); ob.m = m; ob.ncols = ncols; ob.ld = m;
+    ob.b = b_host ? h->bh.d() : nullptr;
+    TRY(lbfgsb_solve(h, &ob, h->xh.d(), tol, res));
+    CK(cudaMemcpyAsync(x_host, h->xh.p, sizeof(double) * ncols, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ Alg. 4
+extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const al_constraints* cons,
+                               const al_opts* opts, double* x, double* lambda, double* mu,
+                               al_result* res)
+{
+    if (!h || !obj || !x) return fail(LBFGSB_ERR_ARG, "NULL handle, objective or x");
+    if (obj->kind != 0) return fail(LBFGSB_ERR_UNSUPPORTED, "al_solve needs an LSQ objective");
+    al_opts ao;
+    al_opts_default(&ao);
+    if (opts) ao = *opts;
+    const int neq = cons ? (int)cons->m_eq : 0, nin = cons ? (int)cons->p_in : 0;
+    if (neq < 0 || nin < 0) return fail(LBFGSB_ERR_DIM, "negative constraint count");
+    if (neq + nin > MAXC) return fail(LBFGSB_ERR_UNSUPPORTED, "at most %d linear constraints", MAXC);
+    if ((neq && (!cons->E || !cons->e)) || (nin && (!cons->G || !cons->hv)))
+        return fail(LBFGSB_ERR_ARG, "constraint data missing");
+    Prob P;
+    TRY(make_prob(h, obj, P));
+    P.n_eq = neq; P.n_in = nin;
+    for (int k = 0; k < neq; ++k) P.Ecol[k] = cons->E + (int64_t)k * h->n;
+    for (int k = 0; k < nin; ++k) P.Ecol[neq + k] = cons->G + (int64_t)k * h->n;
+    set_sep(P, sm_count());
+    const double tol = h->o.tol;
+    // x^0 = clip(0) (R19), lambda = 0, mu = 0, rho = rho0
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * h->n, h->st));
+    double lam[MAXC] = {0}, rhs[MAXC] = {0};
+    for (int k = 0; k < neq; ++k) rhs[k] = cons->e[k];
+    for (int k = 0; k < nin; ++k) rhs[neq + k] = cons->hv[k];
+    double rho = ao.rho0;
+    auto set_al = [&]() {
+        h->hc->rho = rho;
+        std::memcpy(h->hc->lam, lam, sizeof lam);
+        std::memcpy(h->hc->rhs, rhs, sizeof rhs);
+    };
+    auto viol = [&](const double* hv) {     // R21 (Birgin-Martinez measure)
+        double v = 0.0;
+        for (int k = 0; k < neq; ++k) v = std::fabs(hv[k]) > v ? std::fabs(hv[k]) : v;
+        for (int k = 0; k < nin; ++k) {
+            double t = -hv[neq + k];
+            const double mr = lam[neq + k] / rho;
+            if (mr < t) t = mr;
+            v = std::fabs(t) > v ? std::fabs(t) : v;
+        }
+        return v;
+    };
+    // violation at x^0
+    set_al();
+    CK(cudaMemcpyAsync(P.x, x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
+    init_ctrl(h, tol);
+    TRY(ctrl_to_dev(h));
+    launch_refresh(h, P, true);
+    CK(cudaGetLastError());
+    TRY(ctrl_to_host(h));
+    CK(cudaMemcpyAsync(x, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
+    double hv[MAXC];
+    std::memcpy(hv, h->hc->hval, sizeof hv);
+    double vprev = viol(hv);
+    al_result R{};
+    R.status = AL_MAX_OUTER;
+    lbfgsb_result ir{};
+    for (int it = 0; it < ao.max_outer; ++it) {
+        const double tin = 0.1 * vprev > tol ? 0.1 * vprev : tol;      // R22
+        set_al();
+        TRY(solve_lsq(h, P, x, tin, &ir));                            // Alg. 4 line 5
+        R.inner_iters_total += ir.iters;
+        R.outer_iters = it + 1;
+        R.pg_inf = ir.pg_inf;
+        if (ir.status == LBFGSB_LINESEARCH_FAILURE) { R.status = AL_INNER_FAILURE; break; }
+        std::memcpy(hv, h->hc->hval, sizeof hv);                       // h(x), g(x) at x*
+        for (int k = 0; k < neq; ++k) lam[k] = lam[k] + rho * hv[k];   // line 6
+        for (int k = 0; k < nin; ++k) {                                // line 7
+            const double t = lam[neq + k] + rho * hv[neq + k];
+            lam[neq + k] = t > 0.0 ? t : 0.0;
+        }
+        const double v = viol(hv);
+        if (v > 0.5 * vprev) {                                         // line 8 (R20)
+            rho = rho * ao.rho_factor;
+            if (rho > ao.rho_cap) rho = ao.rho_cap;
+        }
+        vprev = v;
+        if (ir.status == LBFGSB_CONVERGED && v <= ao.feas_tol && tin == tol) {
+            R.status = LBFGSB_CONVERGED;
+            break;
+        }
+    }
+    R.f = h->hc->f_base;
+    R.violation_inf = viol(hv);
+    R.rho = rho;
+    if (lambda) for (int k = 0; k < neq; ++k) lambda[k] = lam[k];
+    if (mu) for (int k = 0; k < nin; ++k) mu[k] = lam[neq + k];
+    if (res) *res = R;
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ sharded (NCCL)
+extern "C" lbfgsb_err lbfgsb_create_sharded(int64_t n_local, int64_t n_global, int32_t m_hist,
+                                            const double* lower_local, const double* upper_local,
+                                            const lbfgsb_opts* opts, void* cuda_stream,
+                                            const void* nccl_unique_id, int32_t rank, int32_t nranks,
+                                            lbfgsb_t** out)
+{
+    (void)n_local; (void)n_global; (void)m_hist; (void)lower_local; (void)upper_local; (void)opts;
+    (void)cuda_stream; (void)nccl_unique_id; (void)rank; (void)nranks;
+    if (out) *out = nullptr;
+    return fail(LBFGSB_ERR_UNSUPPORTED, "sharded handles are not available in this build yet");
+}
+
+// ------------------------------------------------------------------ ops
+extern "C" lbfgsb_err lbfgsb_op_gemv(const lbfgsb_objective* obj, const double* p, double* q,
+                                     void* cuda_stream)
+{
+    if (!obj || obj->kind != 0 || !p || !q) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    init_kernels();
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const int sms = sm_count();
+    Prob P;
+    std::memset(&P, 0, sizeof P);
+    P.m = obj->m; P.ncols = obj->ncols; P.ld = obj->ld; P.M = obj->M;
+    P.colscale = obj->colscale; P.split = obj->split;
+    P.n = obj->split ? 2 * obj->ncols : obj->ncols;
+    P.fwd_rb = (int)cdiv(P.m, FWD_ROWS);
+    int64_t cc = clampi(cdiv(4LL * sms, P.fwd_rb), 1, clampi(cdiv(P.ncols, 32), 1, 1 << 20));
+    P.fwd_chunk = cdiv(P.ncols, cc);
+    P.fwd_cc = (int)cdiv(P.ncols, P.fwd_chunk);
+    double* qpart = nullptr;
+    CK(cudaMallocAsync(&qpart, sizeof(double) * (size_t)P.m * P.fwd_cc, st));
+    P.qpart = qpart;
+    launch_fwd(P, st, FWD_P, p);
+    launch_resid(P, st, 0, q);
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(qpart, st);
+    if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "gemv: %s", cudaGetErrorString(e));
+    CK(cudaStreamSynchronize(st));
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_op_gemvt(const lbfgsb_objective* obj, const double* r, double* g,
+                                      void* cuda_stream)
+{
+    if (!obj || obj->kind != 0 || !r || !g) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    init_kernels();
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    Prob P;
+    std::memset(&P, 0, sizeof P);
+    P.m = obj->m; P.ncols = obj->ncols; P.ld = obj->ld; P.M = obj->M;
+    P.colscale = obj->colscale; P.split = obj->split;
+    P.n = obj->split ? 2 * obj->ncols : obj->ncols;
+    P.bwd_blocks = (int)cdiv(P.ncols, BWD_NB);
+    launch_bwd(P, st, BWD_PLAIN, r, g);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_op_direction(lbfgsb_t* h, const double* x, const double* g, int32_t nh,
+                                          const double* S, const double* Y, uint8_t* free_out,
+                                          double* d_out, double* p_out, int32_t* projected, double* gp,
+                                          double* amax)
+{
+    if (!h || !x || !g) return fail(LBFGSB_ERR_ARG, "NULL handle, x or g");
+    if (nh < 0 || nh > h->mh || (nh > 0 && (!S || !Y))) return fail(LBFGSB_ERR_DIM, "bad history");
+    Prob P;
+    TRY(make_prob(h, nullptr, P));
+    cudaStream_t st = h->st;
+    const size_t nb = sizeof(double) * h->n;
+    CK(cudaMemcpyAsync(P.x, x, nb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(P.g, g, nb, cudaMemcpyDeviceToDevice, st));
+    launch_ring_load(P, st, nh, S, Y);
+    init_ctrl(h, h->o.tol);
+    h->hc->nh = nh;
+    h->hc->head = nh > 0 ? nh - 1 : h->mh - 1;
+    TRY(ctrl_to_dev(h));
+    launch_gram(P, st, 1);
+    launch_recur(P, st, 1);
+    launch_dir(P, st, 1);
+    launch_branch(P, st, 1);
+    CK(cudaGetLastError());
+    TRY(ctrl_to_host(h));
+    const int br = h->hc->branch;
+    if (free_out) CK(cudaMemcpyAsync(free_out, P.mask, (size_t)h->n, cudaMemcpyDeviceToDevice, st));
+    if (d_out) CK(cudaMemcpyAsync(d_out, P.d, nb, cudaMemcpyDeviceToDevice, st));
+    if (p_out) CK(cudaMemcpyAsync(p_out, br ? P.pp : P.pt, nb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    if (projected) *projected = br;
+    if (gp) *gp = h->hc->gp;
+    if (amax) *amax = h->hc->amax;
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_op_trials(lbfgsb_t* h, const lbfgsb_objective* obj, const double* r,
+                                       const double* q, const double* x, const double* p, double alpha0,
+                                       int32_t ntrials, double* f_out)
+{
+    if (!h || !obj || obj->kind != 0 || !r || !q || !x || !p || !f_out)
+        return fail(LBFGSB_ERR_ARG, "bad arguments");
+    if (ntrials < 1 || ntrials > KT) return fail(LBFGSB_ERR_ARG, "ntrials in [1, %d]", KT);
+    Prob P;
+    TRY(make_prob(h, obj, P));
+    set_sep(P, sm_count());
+    P.r = const_cast<double*>(r);
+    P.q = const_cast<double*>(q);
+    P.x = const_cast<double*>(x);
+    init_ctrl(h, h->o.tol);
+    h->hc->alpha0 = alpha0;
+    h->hc->rho = 1.0;
+    TRY(ctrl_to_dev(h));
+    launch_ls(P, h->st, LS_OP, p);
+    launch_ls_decide(P, h->st, LS_OP, h->fout.d(), ntrials);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(f_out, h->fout.p, sizeof(double) * ntrials, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_profile_get(lbfgsb_t* h, int32_t cap, const char** names, double* ms,
+                                         int64_t* launches, int32_t* count, int32_t reset)
+{
+    if (!h || !count) return fail(LBFGSB_ERR_ARG, "NULL handle or count");
+    static const char* kn[3] = {"gemv_active (k_fwd)", "gemvT_epi (k_bwd)", "all_kernel_launches"};
+    const double vals[3] = {h->prof_ms[0], h->prof_ms[1], 0.0};
+    const int64_t cnts[3] = {h->prof_n[0], h->prof_n[1], h->launches};
+    int c = 0;
+    for (int i = 0; i < 3 && i < cap; ++i, ++c) {
+        if (names) names[i] = kn[i];
+        if (ms) ms[i] = vals[i];
+        if (launches) launches[i] = cnts[i];
+    }
+    *count = c;
+    if (reset) { h->prof_ms[0] = h->prof_ms[1] = 0; h->prof_n[0] = h->prof_n[1] = 0; h->launches = 0; }
+    return LBFGSB_OK;
+}
