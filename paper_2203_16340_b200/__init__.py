@@ -207,10 +207,10 @@ class LSQObjective:
 
     def __init__(self, M, b=None, c=None, delta=0.0, colscale=None, split=False):
         L = load()
-        if M.dim() != 2 or M.stride(0) != 1:
+        if M.dim() != 2 or (M.stride(0) != 1 and M.shape[0] > 1):
             raise LbfgsbError("M must be (m, ncols) column-major: M.stride(0) == 1")
         self.m, self.ncols = M.shape
-        self.ld = max(M.stride(1), self.m)
+        self.ld = max(M.stride(1), self.m) if self.ncols > 1 else self.m
         self.split = bool(split)
         self.nvars = 2 * self.ncols if split else self.ncols
         self._keep = (M, b, c, colscale)      # borrowed by the C objective
