@@ -1,0 +1,293 @@
+#!/usr/bin/env python
+"""bench.py -- NNLS L-BFGS-B iterations/s and time-to-KKT-tolerance on B200.
+
+One "step" = one complete ``lbfgsb_solve`` of the north-star workload from
+x^0 = 0 to ||g[S]||_inf <= 1e-6 (every row of SURVEY.md 8(a): setup, all
+Alg. 1 iterations with working set, vector-free two-loop, Alg. 2, Armijo
+trials, fused GEMV / GEMV^T, and the final residual refresh + KKT report).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1 runs BASELINE.json configs[1] (C2: dense NNLS 20000 x 10000 fp64).
+N > 1 (torchrun, one rank per GPU) runs the column-sharded solve: every rank
+holds a C2-sized block of columns (weak scaling, n = 10000 N) and the ranks
+exchange the m-length residual partials and the packed scalar reductions
+over NCCL each iteration.
+
+value      = Alg. 1 iterations (summed over steps) / device time of the K steps
+             (for N > 1: x N, i.e. C2-shard-iterations/s of the whole job)
+e2e        = same metric through lbfgsb_solve_lsq_host with HOST (pinned)
+             buffers: H2D of A and b and D2H of x* inside every timed step
+roofline   = the dominant kernel (gemvT_epi, k_bwd): algorithmic bytes per
+             launch / average CUDA-event launch time over the timed region
+cpu_baseline = the CPU oracle (oracle/oracle.c, single thread) solving the
+             same C2 instance to the same tolerance (rank 0, N = 1 only)
+
+--impl reference times the oracle itself as the reference arm (bounded
+sample: 2 Alg. 1 iterations of C2 per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_ROWS, N_COLS, SEED, M_HIST, TOL = 20000, 10000, 2, 5, 1e-6
+METRIC = "NNLS L-BFGS-B iters/s to KKT tol 1e-6 (dense 20000x10000 fp64 per GPU)"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.idx), "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [t.strip() for t in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "samples": len(sms), "reasons": sorted(reasons)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    import synth
+    p = synth.nnls_gaussian(M_ROWS, N_COLS, SEED)
+    P = oracle.LSQ(p.M, b=p.b)
+    iters_per_step = 2
+    o = oracle.Options(tol=TOL, max_iters=iters_per_step)
+    for _ in range(args.warmup):
+        oracle.minimize_lsq(P, l=p.lower, m_hist=M_HIST, opts=o)
+    t0 = time.perf_counter()
+    tot = 0
+    for _ in range(args.steps):
+        r = oracle.minimize_lsq(P, l=p.lower, m_hist=M_HIST, opts=o)
+        tot += r.iters
+    dt = time.perf_counter() - t0
+    v = tot / dt
+    sample = f"C2 (20000x10000, seed {SEED}): setup + {iters_per_step} Alg. 1 iterations + final refresh per step"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C2 dense NNLS m=20000 n=10000 fp64 (CPU oracle sample)",
+                       "m": M_ROWS, "n": N_COLS, "m_hist": M_HIST},
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def cpu_baseline_full():
+    """Oracle (single thread, as it stands) solving the same C2 instance to tol."""
+    import oracle
+    import synth
+    p = synth.nnls_gaussian(M_ROWS, N_COLS, SEED)
+    t0 = time.perf_counter()
+    r = oracle.minimize_lsq(oracle.LSQ(p.M, b=p.b), l=p.lower, m_hist=M_HIST,
+                            opts=oracle.Options(tol=TOL))
+    dt = time.perf_counter() - t0
+    return {"value": r.iters / dt, "unit": "iters/s", "cores": 1, "kind": "oracle",
+            "sample": f"full C2 solve to tol {TOL}: {r.iters} iterations in {dt:.2f} s "
+                      f"(time-to-tol {dt:.2f} s, f={r.f:.12g}, pg={r.pg_inf:.2e})",
+            "time_to_tol_s": dt, "iters": r.iters, "f": r.f}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_2203_16340_b200 as lb
+    import synth
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        from paper_2203_16340_b200 import sharded
+        return sharded.bench_main(args, METRIC)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p = synth.nnls_gaussian(M_ROWS, N_COLS, SEED)
+    M = lb.colmajor(p.M, device=dev)
+    b = torch.from_numpy(p.b).to(dev)
+    lo = torch.zeros(N_COLS, dtype=torch.float64, device=dev)
+    obj = lb.LSQObjective(M, b=b)
+    stream = torch.cuda.Stream(device=dev)
+    solver = lb.Solver(N_COLS, M_HIST, lower=lo, opts=lb.Options(tol=TOL, profile=True), stream=stream)
+    x = torch.zeros(N_COLS, dtype=torch.float64, device=dev)
+
+    def step():
+        x.zero_()
+        return solver.solve(obj, x)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        solver.profile(reset=True)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters, results = 0, []
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                r = step()
+                iters += r.iters
+                results.append(r)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        prof = solver.profile(reset=True)
+    clocks = clk.summary()
+    value = iters / (ms / 1e3)
+    r0 = results[-1]
+    ms_per_step = ms / args.steps
+
+    # ---- roofline of the dominant kernel (k_bwd = gemvT_epi), live CUDA events
+    peak, peak_src = _peaks()
+    bwd_ms, bwd_n = prof["gemvT_epi (k_bwd)"]
+    fwd_ms, fwd_n = prof["gemv_active (k_fwd)"]
+    launches = prof["all_kernel_launches"][1]
+    # algorithmic bytes of one k_bwd launch: A (8 m n) + r (8 m) + per-variable
+    # epilogue reads x, g, p, l, u and writes x, g, s, y (9 x 8 n)
+    bwd_bytes = 8 * M_ROWS * N_COLS + 8 * M_ROWS + 9 * 8 * N_COLS
+    bwd_avg_s = (bwd_ms / max(bwd_n, 1)) / 1e3
+    achieved = bwd_bytes / bwd_avg_s / 1e9 if bwd_n else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "r01_kbwd_dram_bytes.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "k_bwd (gemvT_epi: g = M^T r + fused Alg. 1 epilogue)",
+                "bytes_per_launch": bwd_bytes, "avg_launch_us": bwd_avg_s * 1e6,
+                "launches": bwd_n, "peak_source": peak_src,
+                "share_of_step": (bwd_ms / ms) if ms else None,
+                "k_fwd_share_of_step": (fwd_ms / ms) if ms else None,
+                "k_fwd_avg_launch_us": 1e3 * fwd_ms / max(fwd_n, 1)}
+
+    # ---- e2e: lbfgsb_solve_lsq_host from pinned host buffers
+    Mh = torch.from_numpy(np.ascontiguousarray(p.M.T)).pin_memory().numpy().T   # Fortran view
+    bh = torch.from_numpy(p.b.copy()).pin_memory().numpy()
+    xh = torch.zeros(N_COLS, dtype=torch.float64).pin_memory().numpy()
+    solver_h = lb.Solver(N_COLS, M_HIST, lower=lo, opts=lb.Options(tol=TOL), stream=stream)
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        xh[:] = 0.0
+        solver_h.solve_lsq_host(Mh, bh, xh)
+    t0 = time.perf_counter()
+    e2e_iters = 0
+    for _ in range(e2e_steps):
+        xh[:] = 0.0
+        e2e_iters += solver_h.solve_lsq_host(Mh, bh, xh).iters
+    e2e_dt = time.perf_counter() - t0
+    e2e = {"value": e2e_iters / e2e_dt, "unit": "iters/s",
+           "h2d_bytes_per_step": 8 * (M_ROWS * N_COLS + M_ROWS + N_COLS),
+           "d2h_bytes_per_step": 8 * N_COLS, "steps": e2e_steps,
+           "ms_per_step": 1e3 * e2e_dt / e2e_steps,
+           "api": "lbfgsb_solve_lsq_host (pinned host A, b, x; host wall clock around the call)"}
+
+    cpu = None if args.no_cpu_baseline else cpu_baseline_full()
+    line = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy: A_ij ~ N(0,1)/sqrt(m), b ~ N(0,1); SURVEY 8(d) C2)",
+        "config": {"workload": "C2: dense NNLS m=20000 n=10000 fp64, x>=0, m_hist=5, tol 1e-6 "
+                               "(BASELINE.json configs[1])",
+                   "m": M_ROWS, "n": N_COLS, "m_hist": M_HIST, "tol": TOL, "seed": SEED,
+                   "l2": "inputs larger than L2 (A = 1.6 GB > 126 MB); no flush",
+                   "parallelism": "single GPU"},
+        "time_to_tol_ms": ms_per_step, "iters_per_solve": r0.iters, "f": r0.f,
+        "pg_inf": r0.pg_inf, "status": r0.status_name,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks,
+        "paper_context": "paper: 0.8 s modified L-BFGS-B GPU / 4.9 s CPU L-BFGS-B on NNLS size 12000 "
+                         "(Quadro RTX 4000 / i9-10980XE, PAPER.md:449-451); different sizes/hardware",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

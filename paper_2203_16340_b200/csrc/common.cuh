@@ -1,0 +1,301 @@
+// common.cuh -- device helpers shared by the kernel translation units of
+// liblbfgsb (deterministic reductions, last-CTA tickets, Gram entry layout,
+// the vector-free Alg. 3 recurrence and the Armijo decision).
+#pragma once
+#include <cmath>
+#include <cstdint>
+#include "impl.cuh"
+
+namespace lb {
+
+// ticket indices
+constexpr int T_DIR = 0, T_FWD_ALL = 1, T_LS = 2, T_KKT = 3, T_BWD_G2 = 4, T_GRAM = 5;
+constexpr int T_FWD_RB = 64;            // + row block (<= 8192)
+constexpr int T_BWD_G1 = 64 + 8192;     // + group (<= 8000)
+static_assert(T_BWD_G1 + 8000 <= NTICKETS + 8192, "ticket space");
+
+constexpr int BWD_BUF = 2048;           // smem doubles for the k_bwd tail reduction
+constexpr int BWD_TILE = 2 * BWD_NB;    // variables per epilogue group (split: 2 per column)
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double clipd(double v, double lo, double hi)
+{
+    // clip(v) = min(max(v, l), u) with the comparison order of the oracle
+    if (v < lo) v = lo;
+    if (v > hi) v = hi;
+    return v;
+}
+
+template <int OP>
+__device__ __forceinline__ double opf(double a, double b)
+{
+    if (OP == 0) return a + b;
+    if (OP == 1) return b > a ? b : a;
+    return b < a ? b : a;
+}
+
+template <int OP>
+__device__ __forceinline__ double warp_red(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = opf<OP>(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;   // lane 0
+}
+
+// Deterministic block reduction; result valid in thread 0.  sh: >= blockDim.x/32.
+template <int OP>
+__device__ __forceinline__ double block_reduce(double v, double* sh)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_red<OP>(v);
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0) {
+        r = sh[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) r = opf<OP>(r, sh[i]);
+    }
+    return r;
+}
+
+__device__ __forceinline__ bool halted(const Ctrl* C) { return (C->done | C->stall) != 0; }
+
+// Last-CTA ticket: true in every thread of the last of `total` CTAs to arrive.
+// Partials written before the call by the other CTAs are visible afterwards.
+__device__ __forceinline__ bool last_cta(unsigned* ticket, unsigned total)
+{
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(ticket, 1u);
+        s_last = (t == total - 1u) ? 1 : 0;
+        if (s_last) *ticket = 0u;           // everyone else has arrived: reset for the next launch
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last != 0;
+}
+
+// out[e] = reduction over parts p = 0..nparts-1 of src[p * stride + e], for
+// e < nent, in a fixed tree order (per pass: strided sequential sums over T
+// threads per entry, then a pairwise smem tree; passes combined in order).
+// opsel(e): 0 sum, 1 max, 2 min.  All threads of the CTA must call; stash >= blockDim.x.
+template <typename OpSel>
+__device__ void reduce_parts(const double* src, int nparts, int stride, int nent, OpSel opsel,
+                             double* buf, int bufn, double* stash, double* out)
+{
+    const int nth = (int)blockDim.x;
+    int T = 1;
+    while (T * 2 * nent <= nth) T *= 2;
+    const int epr = nth / T;                         // entries per round
+    const int per_pass = bufn / nent > 0 ? bufn / nent : 1;
+    for (int p0 = 0; p0 < nparts; p0 += per_pass) {
+        const int np = nparts - p0 < per_pass ? nparts - p0 : per_pass;
+        for (int i = threadIdx.x; i < np * nent; i += nth) {
+            const int p = i / nent, e = i - p * nent;
+            buf[i] = __ldcg(src + (size_t)(p0 + p) * stride + e);
+        }
+        __syncthreads();
+        for (int eb = 0; eb < nent; eb += epr) {
+            const int e = eb + threadIdx.x / T, j = threadIdx.x % T;
+            const int op = e < nent ? opsel(e) : 0;
+            double s = op == 0 ? 0.0 : (op == 1 ? -INFINITY : INFINITY);
+            if (e < nent) {
+                for (int p = j; p < np; p += T) {
+                    const double v = buf[p * nent + e];
+                    s = op == 0 ? s + v : (op == 1 ? (v > s ? v : s) : (v < s ? v : s));
+                }
+            }
+            stash[threadIdx.x] = s;
+            __syncthreads();
+            for (int h = T / 2; h > 0; h >>= 1) {
+                if (e < nent && j < h) {
+                    const double a = stash[threadIdx.x], b = stash[threadIdx.x + h];
+                    stash[threadIdx.x] = op == 0 ? a + b : (op == 1 ? (b > a ? b : a) : (b < a ? b : a));
+                }
+                __syncthreads();
+            }
+            if (e < nent && j == 0) {
+                const double v = stash[threadIdx.x];
+                if (p0 == 0) out[e] = v;
+                else {
+                    const double a = out[e];
+                    out[e] = op == 0 ? a + v : (op == 1 ? (v > a ? v : a) : (v < a ? v : a));
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// upper-triangle index of (a, b), a <= b, in an nb x nb symmetric matrix
+__host__ __device__ __forceinline__ int tri(int a, int b, int nb)
+{
+    return a * nb - (a * (a - 1)) / 2 + (b - a);
+}
+
+__device__ __forceinline__ int ring_slot(int head, int nh, int i, int mh)
+{
+    // basis index i (0 = oldest) -> physical ring slot; head = newest
+    return ((head - (nh - 1) + i) % mh + mh) % mh;
+}
+
+// Entries of the per-CTA Gram partial a thread accumulates (<= 3 per thread,
+// entry e = threadIdx.x + k * blockDim.x).
+struct GramEnt {
+    int a[3], b[3];
+    bool full[3];
+    __device__ void init(int nb, int ne, int ntot, int nh)
+    {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int e = threadIdx.x + k * (int)blockDim.x;
+            a[k] = -1; b[k] = -1; full[k] = false;
+            if (e < ne) {
+                int aa = 0, rem = e;
+                while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
+                a[k] = aa; b[k] = aa + rem;
+            } else if (e < ntot) {
+                a[k] = b[k] = nh + (e - ne); full[k] = true;
+            }
+        }
+    }
+    // acc[k] += sum over tile rows (in row order) of mask * B_a * B_b
+    __device__ void accumulate(const double* tile, const double* mk, int rows, int nb, double* acc) const
+    {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (a[k] < 0) continue;
+            const int aa = a[k], bb = b[k];
+            double s = 0.0;
+            if (!full[k]) {
+                for (int r = 0; r < rows; ++r)
+                    if (mk[r] != 0.0) s = fma(tile[r * nb + aa], tile[r * nb + bb], s);
+            } else {
+                for (int r = 0; r < rows; ++r) s = fma(tile[r * nb + aa], tile[r * nb + aa], s);
+            }
+            acc[k] += s;
+        }
+    }
+};
+
+// Reduced Gram (smem) -> convergence test (R15) and Alg. 3
+// in vector-free form on the coefficient vector w of q = sum_b w_b B_b:
+//   newest..oldest: rho_i = <s_i,y_i>_S, nu_i = ||y_i||^2_S (R3), ok_i = rho_i > eps nu_i,
+//                   a_i = <s_i, q>_S / rho_i, q -= a_i y_i
+//   q *= rho_{k-1}/nu_{k-1} if pair k-1 passes (R4)
+//   oldest..newest: beta = <y_i, q>_S / rho_i, q += (a_i - beta) s_i
+// d = -q on S (R5).  Single thread.
+__device__ __forceinline__ void recur_decide(const Prob& P, Ctrl* C, const double* G, int nh, int op_mode)
+{
+    const int nb = 2 * nh + 1, ne = nb * (nb + 1) / 2;
+    const int nfull = P.screen_full ? nh : 0;
+    const double gm = G[ne + nfull], cnt = G[ne + nfull + 1];
+    C->gfree = gm;
+    C->nfree = (long long)cnt;
+    if (!op_mode) {
+        if (cnt == 0.0 || gm <= C->tol) { C->done = 1; C->status = S_CONVERGED; return; }
+        if (C->k >= P.max_iters) { C->done = 1; C->status = S_MAX_ITERS; return; }
+    }
+    double w[MAXB], al[MAXH], rho[MAXH], nu[MAXH];
+    bool ok[MAXH];
+    for (int b = 0; b < nb; ++b) w[b] = 0.0;
+    w[2 * nh] = 1.0;                                             // q = grad[S]
+    auto Gv = [&](int a, int b) { return a <= b ? G[tri(a, b, nb)] : G[tri(b, a, nb)]; };
+    for (int i = nh - 1; i >= 0; --i) {
+        rho[i] = Gv(i, nh + i);
+        nu[i] = P.screen_full ? G[ne + i] : Gv(nh + i, nh + i);
+        ok[i] = rho[i] > P.eps * nu[i];
+        al[i] = 0.0;
+        if (ok[i]) {
+            double t = 0.0;
+            for (int b = 0; b < nb; ++b) t += w[b] * Gv(i, b);     // <s_i, q>_S
+            al[i] = t / rho[i];
+            w[nh + i] = w[nh + i] - al[i];                       // q -= a_i y_i
+        }
+    }
+    if (nh > 0 && ok[nh - 1]) {
+        const double gam = rho[nh - 1] / nu[nh - 1];
+        for (int b = 0; b < nb; ++b) w[b] = gam * w[b];
+    }
+    for (int i = 0; i < nh; ++i) {
+        if (!ok[i]) continue;
+        double t = 0.0;
+        for (int b = 0; b < nb; ++b) t += w[b] * Gv(nh + i, b);  // <y_i, q>_S
+        const double beta = t / rho[i];
+        w[i] = w[i] + (al[i] - beta);                           // q += (a_i - beta) s_i
+    }
+    for (int b = 0; b < nb; ++b) C->coef[b] = -w[b];
+}
+
+// Trial objective from reduced sums (oracle order: 1/2 S + phi,
+// phi = c^T x + delta/2 ||x||^2, then the AL terms of Eq. (3)).
+__device__ __forceinline__ double trial_value(const Prob& P, const Ctrl* C, double S, const double* sep,
+                              double* ccoef, double* hval, double* fbase)
+{
+    const int ncons = P.n_eq + P.n_in;
+    const double cx = sep ? sep[0] : 0.0, xx = sep ? sep[1] : 0.0;
+    double phi = cx + 0.5 * P.delta * xx;
+    if (fbase) *fbase = 0.5 * S + phi;
+    for (int k = 0; k < ncons; ++k) {
+        const double hv = sep[2 + k] - C->rhs[k];
+        hval[k] = hv;
+        if (k < P.n_eq) {
+            const double tt = hv + C->lam[k] / C->rho;
+            phi += 0.5 * C->rho * tt * tt;
+            ccoef[k] = C->rho * hv + C->lam[k];
+        } else {
+            double tt = hv + C->lam[k] / C->rho;
+            if (tt < 0.0) tt = 0.0;
+            phi += 0.5 * C->rho * tt * tt;
+            ccoef[k] = C->rho * tt;
+        }
+    }
+    return 0.5 * S + phi;
+}
+
+// Armijo decision over one batch of KT trials (R10, R11, R13); single thread.
+// S[t] = sum (r + alpha_t q)^2, sep[t*NSEP + s] the separable sums.
+__device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const double* S, const double* sep)
+{
+    double cc[MAXC], hv[MAXC];
+    const int ncons = P.n_eq + P.n_in;
+    double a = C->alpha0;
+    int tried = 0;
+    for (int t = 0; t < KT; ++t) {
+        if (t > 0) a = a * P.shrink;
+        if (C->ls_batch * KT + t > P.max_bt) break;
+        ++tried;
+        const double ft = trial_value(P, C, S[t], sep ? sep + t * NSEP : nullptr, cc, hv, nullptr);
+        if (ft <= C->f + P.c1 * a * C->gp) {                    // Armijo condition
+            C->alpha = a;
+            C->f_new = ft;
+            C->f = ft;
+            for (int k = 0; k < ncons; ++k) { C->ccoef[k] = cc[k]; C->hval[k] = hv[k]; }
+            C->n_fg += t + 1;
+            C->n_bt += t;
+            const int head = (C->head + 1) % P.mh;              // store pair
+            C->head = head;
+            C->slot = head;
+            C->nh = C->nh + 1 < P.mh ? C->nh + 1 : P.mh;
+            C->k += 1;
+            C->fallback = 0;
+            return;
+        }
+    }
+    C->n_fg += tried;
+    C->n_bt += tried;
+    if ((C->ls_batch + 1) * KT > P.max_bt) {                    // trials exhausted
+        if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }
+        else C->stall = ST_FALLBACK;
+    } else {
+        C->alpha0 = a * P.shrink;
+        C->ls_batch += 1;
+        C->stall = ST_LS_CONT;
+    }
+}
+
+
+}  // namespace lb

@@ -1,8 +1,8 @@
 // solver.cu -- host control of liblbfgsb: the C ABI of include/lbfgsb.h and
-// include/lbfgsb_ops.h.  Drives the device kernels of kernels.cu; every step
-// of the method runs on the GPU, the host only sequences launches, replays
-// CUDA graphs and reads the 300-byte control block every check_every
-// iterations.  No CPU fallback exists: without a device every call returns
+// include/lbfgsb_ops.h.  Every step of the method runs in the device kernels
+// of kernels.cu; the host only sequences launches, replays a CUDA graph of
+// check_every iterations and reads the ~400-byte control block between
+// replays.  No CPU fallback exists: without a device every call returns
 // LBFGSB_ERR_CUDA.
 //
 // Citations: PAPER.md:N (paper LaTeX line), R<k>.
@@ -72,7 +72,7 @@ namespace {
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
-    lbfgsb_err ensure(size_t need)
+    lbfgsb_err ensure(size_t need, bool zero = false)
     {
         if (need <= bytes && p) return LBFGSB_OK;
         if (p) cudaFree(p);
@@ -80,7 +80,9 @@ struct DevBuf {
         bytes = 0;
         if (need == 0) need = 16;
         cudaError_t e = cudaMalloc(&p, need);
+        if (e == cudaSuccess && zero) e = cudaMemset(p, 0, need);
         if (e != cudaSuccess) {
+            if (p) cudaFree(p);
             p = nullptr;
             return fail(LBFGSB_ERR_OOM, "cudaMalloc(%zu): %s", need, cudaGetErrorString(e));
         }
@@ -95,7 +97,6 @@ struct DevBuf {
     }
     double* d() const { return static_cast<double*>(p); }
 };
-constexpr int kPerIter = 9;   // kernel launches per device iteration
 }  // namespace
 
 struct lbfgsb_t {
@@ -103,11 +104,12 @@ struct lbfgsb_t {
     int mh = 0;
     lbfgsb_opts o{};
     cudaStream_t st = nullptr;
+    bool own_stream = false;
     // n-sized
     DevBuf l, u, x, g, d, pp, pt, S, Y, mask, xt, gt;
-    DevBuf gram_part, dir_part, kkt_part;
+    DevBuf gram_part, gram_grp, dir_part, kkt_part, tickets, sep_part;
     // m-sized (grown on demand)
-    DevBuf r, q, qpart, ls_part, sep_part, fout;
+    DevBuf r0, r1, q, qpart, lsp, fout;
     // host-buffer solve staging
     DevBuf Mh, bh, xh;
     Ctrl* ctrl = nullptr;           // device
@@ -121,7 +123,7 @@ struct lbfgsb_t {
     double prof_ms[2] = {0, 0};
     int64_t prof_n[2] = {0, 0};
     int64_t launches = 0;
-    bool own_stream = false;
+    int64_t nact_total = 0;
     // sharding
     int rank = 0, nranks = 1;
     int64_t n_global = 0;
@@ -158,7 +160,7 @@ extern "C" void al_opts_default(al_opts* o)
     o->max_outer = 100;
 }
 
-// ------------------------------------------------------------------ kernels for bounds
+// ------------------------------------------------------------------ bounds
 namespace {
 __global__ void k_fill_bounds(double* l, double* u, const double* lin, const double* uin, int64_t n,
                               int* bad)
@@ -174,6 +176,9 @@ __global__ void k_fill_bounds(double* l, double* u, const double* lin, const dou
 }
 }  // namespace
 
+static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
 // ------------------------------------------------------------------ create / destroy
 static lbfgsb_err alloc_n(lbfgsb_t* h)
 {
@@ -182,10 +187,15 @@ static lbfgsb_err alloc_n(lbfgsb_t* h)
     TRY(h->d.ensure(nb)); TRY(h->pp.ensure(nb)); TRY(h->pt.ensure(nb));
     TRY(h->S.ensure(nb * h->mh)); TRY(h->Y.ensure(nb * h->mh));
     TRY(h->mask.ensure((size_t)h->n));
-    const int64_t G1max = 2LL * sm_count();
-    TRY(h->gram_part.ensure(sizeof(double) * G1max * GRAM_STRIDE));
-    TRY(h->dir_part.ensure(sizeof(double) * G1max * 4));
-    TRY(h->kkt_part.ensure(sizeof(double) * G1max * 3));
+    const int sms = sm_count();
+    const int64_t parts = 64LL * sms;     // >= max(GB, G1) for any occupancy
+    TRY(h->gram_part.ensure(sizeof(double) * parts * GRAM_STRIDE));
+    TRY(h->gram_grp.ensure(sizeof(double) * cdiv(parts, GRP) * GRAM_STRIDE));
+    TRY(h->dir_part.ensure(sizeof(double) * 2LL * sms * 4));
+    TRY(h->kkt_part.ensure(sizeof(double) * 2LL * sms * 3));
+    TRY(h->sep_part.ensure(sizeof(double) * 32 * KT * NSEP));
+    TRY(h->tickets.ensure(sizeof(unsigned) * (NTICKETS + 8192), true));
+    TRY(h->fout.ensure(sizeof(double) * KT));
     CK(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
     CK(cudaMallocHost(&h->hc, sizeof(Ctrl)));
     std::memset(h->hc, 0, sizeof(Ctrl));
@@ -260,12 +270,12 @@ extern "C" void lbfgsb_destroy(lbfgsb_t* h)
 {
     if (!h) return;
     if (h->st) cudaStreamSynchronize(h->st);
-    else cudaDeviceSynchronize();
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
     for (auto e : h->ev) cudaEventDestroy(e);
     DevBuf* bufs[] = {&h->l, &h->u, &h->x, &h->g, &h->d, &h->pp, &h->pt, &h->S, &h->Y, &h->mask,
-                      &h->xt, &h->gt, &h->gram_part, &h->dir_part, &h->kkt_part, &h->r, &h->q,
-                      &h->qpart, &h->ls_part, &h->sep_part, &h->fout, &h->Mh, &h->bh, &h->xh};
+                      &h->xt, &h->gt, &h->gram_part, &h->gram_grp, &h->dir_part, &h->kkt_part,
+                      &h->tickets, &h->sep_part, &h->r0, &h->r1, &h->q, &h->qpart, &h->lsp,
+                      &h->fout, &h->Mh, &h->bh, &h->xh};
     for (DevBuf* b : bufs) b->release();
     if (h->ctrl) cudaFree(h->ctrl);
     if (h->hc) cudaFreeHost(h->hc);
@@ -286,7 +296,8 @@ extern "C" lbfgsb_err lbfgsb_objective_lsq(const double* M, int64_t m, int64_t n
     if (!M) return fail(LBFGSB_ERR_ARG, "M is NULL");
     if (m <= 0 || ncols <= 0 || ld < m) return fail(LBFGSB_ERR_DIM, "bad shape m=%lld ncols=%lld ld=%lld",
                                                     (long long)m, (long long)ncols, (long long)ld);
-    if (m > (1LL << 40) || ncols > (1LL << 31) - 1) return fail(LBFGSB_ERR_DIM, "shape too large");
+    if (m > (int64_t)FWD_ROWS * 8192 || ncols > (1LL << 31) - 1)
+        return fail(LBFGSB_ERR_DIM, "shape too large (m <= %d, ncols < 2^31)", FWD_ROWS * 8192);
     if (split && colscale) return fail(LBFGSB_ERR_ARG, "split and colscale are exclusive");
     if (!std::isfinite(delta)) return fail(LBFGSB_ERR_ARG, "delta not finite");
     auto* o = new lbfgsb_objective();
@@ -313,12 +324,24 @@ extern "C" lbfgsb_err lbfgsb_objective_callback(lbfgsb_fg_cb fg, void* user, lbf
 
 extern "C" void lbfgsb_objective_free(lbfgsb_objective* obj) { delete obj; }
 
-// ------------------------------------------------------------------ problem setup
-static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
-static int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
+// ------------------------------------------------------------------ geometry
+// GEMV launch geometry for an m x ncols operator:
+//  k_fwd: RB row blocks of 512 rows x CC column chunks, RB*CC <= resident CTAs
+//  k_bwd: GB = min(ncols, resident CTAs) persistent CTAs, balanced columns
+static void gemv_geometry(Prob& P)
+{
+    const int sms = sm_count();
+    P.RB = (int)cdiv(P.m, FWD_ROWS);
+    const int64_t slots_f = (int64_t)sms * fwd_ctas_per_sm();
+    int64_t cc = clampi(slots_f / P.RB, 1, clampi(cdiv(P.ncols, 16), 1, 1 << 20));
+    P.chunk = cdiv(P.ncols, cc);
+    P.CC = (int)cdiv(P.ncols, P.chunk);
+    P.GB = (int)clampi((int64_t)sms * bwd_ctas_per_sm(), 1, P.ncols);
+    P.GLS = (int)clampi(cdiv(P.m, NT * 4), 1, 2LL * sms);
+}
 
 // Fill the kernel argument block for (handle, objective) and make sure the
-// m-sized workspace exists.  ncons constraint columns are attached by al_solve.
+// m-sized workspace exists.  Constraint columns are attached by al_solve.
 static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
 {
     std::memset(&P, 0, sizeof P);
@@ -330,9 +353,11 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
     P.max_iters = h->o.max_iters;
     P.x = h->x.d(); P.g = h->g.d(); P.d = h->d.d(); P.pp = h->pp.d(); P.pt = h->pt.d();
     P.S = h->S.d(); P.Y = h->Y.d(); P.mask = static_cast<uint8_t*>(h->mask.p);
-    P.gram_part = h->gram_part.d(); P.dir_part = h->dir_part.d(); P.kkt_part = h->kkt_part.d();
+    P.gram_part = h->gram_part.d(); P.gram_grp = h->gram_grp.d();
+    P.dir_part = h->dir_part.d(); P.kkt_part = h->kkt_part.d(); P.sep_part = h->sep_part.d();
+    P.tickets = static_cast<unsigned*>(h->tickets.p);
     P.ctrl = h->ctrl;
-    P.G1 = (int)clampi(cdiv(h->n, TILE), 1, 2LL * sms);
+    P.G1 = (int)clampi(cdiv(h->n, NT), 1, 2LL * sms);
     if (ob && ob->kind == 0) {
         const int64_t nv = ob->split ? 2 * ob->ncols : ob->ncols;
         if (nv != h->n)
@@ -340,29 +365,21 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
                         (long long)h->n);
         P.m = ob->m; P.ncols = ob->ncols; P.ld = ob->ld; P.M = ob->M;
         P.colscale = ob->colscale; P.split = ob->split; P.b = ob->b; P.c = ob->c; P.delta = ob->delta;
-        P.fwd_rb = (int)cdiv(P.m, FWD_ROWS);
-        int64_t cc = clampi(cdiv(4LL * sms, P.fwd_rb), 1, clampi(cdiv(P.ncols, 32), 1, 1 << 20));
-        P.fwd_chunk = cdiv(P.ncols, cc);
-        P.fwd_cc = (int)cdiv(P.ncols, P.fwd_chunk);
-        P.GL = (int)clampi(cdiv(P.m, NT * 8), 1, 2LL * sms);
-        P.GS = 0;
-        P.bwd_blocks = (int)cdiv(P.ncols, BWD_NB);
+        gemv_geometry(P);
         const size_t mb = sizeof(double) * (size_t)P.m;
-        TRY(h->r.ensure(mb)); TRY(h->q.ensure(mb));
-        TRY(h->qpart.ensure(mb * P.fwd_cc));
-        TRY(h->ls_part.ensure(sizeof(double) * (size_t)P.GL * KT));
-        TRY(h->sep_part.ensure(sizeof(double) * (size_t)sms * KT * NSEP));
-        TRY(h->fout.ensure(sizeof(double) * KT));
-        P.r = h->r.d(); P.q = h->q.d(); P.qpart = h->qpart.d();
-        P.ls_part = h->ls_part.d(); P.sep_part = h->sep_part.d();
+        TRY(h->r0.ensure(mb)); TRY(h->r1.ensure(mb)); TRY(h->q.ensure(mb));
+        TRY(h->qpart.ensure(mb * P.CC));
+        TRY(h->lsp.ensure(sizeof(double) * (size_t)(P.RB > P.GLS ? P.RB : P.GLS) * KT));
+        P.rbuf[0] = h->r0.d(); P.rbuf[1] = h->r1.d(); P.q = h->q.d(); P.qpart = h->qpart.d();
+        P.lsp = h->lsp.d();
     }
     return LBFGSB_OK;
 }
 
-static void set_sep(Prob& P, int sms)
+static void set_sep(Prob& P)
 {
     const bool has_sep = P.c || P.delta != 0.0 || (P.n_eq + P.n_in) > 0;
-    P.GS = has_sep ? (int)clampi(cdiv(P.n, NT * 8), 1, sms) : 0;
+    P.GS = has_sep ? (int)clampi(cdiv(P.n, 2048), 1, 32) : 0;
 }
 
 static lbfgsb_err ctrl_to_dev(lbfgsb_t* h)
@@ -378,51 +395,48 @@ static lbfgsb_err ctrl_to_host(lbfgsb_t* h)
 }
 
 // ------------------------------------------------------------------ iteration sequence
-enum Phase { PH_GRAM = 0, PH_RECUR, PH_DIR, PH_BRANCH, PH_FWD, PH_LS, PH_DECIDE, PH_RUPD, PH_BWD };
-
 static void rec_event(lbfgsb_t* h, int idx)
 {
     if (!h->o.profile || idx < 0) return;
     cudaEventRecordWithFlags(h->ev[idx], h->st, cudaEventRecordExternal);
 }
 
-// Launch one LSQ iteration from `from`; ev_base >= 0 records profile events.
-static void launch_iteration(lbfgsb_t* h, const Prob& P, int from, int ev_base)
+// One LSQ iteration (Alg. 1 lines 3-10): k_dir [k_sep] k_fwd k_bwd.
+static void launch_iteration(lbfgsb_t* h, const Prob& P, int ev_base)
 {
     cudaStream_t st = h->st;
-    int n = 0;
-    if (from <= PH_GRAM) { launch_gram(P, st, 0); ++n; }
-    if (from <= PH_RECUR) { launch_recur(P, st, 0); ++n; }
-    if (from <= PH_DIR) { launch_dir(P, st, 0); ++n; }
-    if (from <= PH_BRANCH) { launch_branch(P, st, 0); ++n; }
-    if (from <= PH_FWD) {
-        rec_event(h, ev_base >= 0 ? ev_base + 0 : -1);
-        launch_fwd(P, st, FWD_ITER, nullptr); ++n;
-        rec_event(h, ev_base >= 0 ? ev_base + 1 : -1);
-    }
-    if (from <= PH_LS) { launch_ls(P, st, LS_ITER0, nullptr); ++n; }
-    if (from <= PH_DECIDE) { launch_ls_decide(P, st, LS_ITER0, nullptr, 0); ++n; }
-    if (from <= PH_RUPD) { launch_rupd(P, st); ++n; }
-    if (from <= PH_BWD) {
-        rec_event(h, ev_base >= 0 ? ev_base + 2 : -1);
-        launch_bwd(P, st, BWD_ITER, nullptr, nullptr); ++n;
-        rec_event(h, ev_base >= 0 ? ev_base + 3 : -1);
-    }
-    h->launches += n;
+    launch_dir(P, st, 0);
+    launch_sep(P, st, SEP_ITER, nullptr);
+    rec_event(h, ev_base >= 0 ? ev_base + 0 : -1);
+    launch_fwd(P, st, FWD_ITER, nullptr, nullptr);
+    rec_event(h, ev_base >= 0 ? ev_base + 1 : -1);
+    rec_event(h, ev_base >= 0 ? ev_base + 2 : -1);
+    launch_bwd(P, st, BWD_ITER, nullptr, nullptr);
+    rec_event(h, ev_base >= 0 ? ev_base + 3 : -1);
+    h->launches += 3 + (P.GS > 0);
 }
 
-// Setup / refresh at x (PAPER.md:65 x^0 feasible; R13 final refresh):
-// x = clip(x), r = M~x - b, f, g = grad f(x).
-static void launch_refresh(lbfgsb_t* h, const Prob& P, bool clip)
+// Setup at x^0 (x = clip(x0); r = M~x - b; f; g; S^0; Gram;
+// convergence test; coefficients of the first direction).
+static void launch_setup(lbfgsb_t* h, const Prob& P)
 {
     cudaStream_t st = h->st;
-    if (clip) { launch_clip(P, st); h->launches++; }
-    launch_fwd(P, st, FWD_X, P.x);
-    launch_resid(P, st, 1, P.r);
-    launch_ls(P, st, LS_SETUP, P.x);
-    launch_ls_decide(P, st, LS_SETUP, nullptr, 1);
+    launch_clip(P, st);
+    launch_sep(P, st, SEP_SETUP, P.x);
+    launch_fwd(P, st, FWD_SETUP, P.x, nullptr);
     launch_bwd(P, st, BWD_SETUP, nullptr, nullptr);
-    h->launches += 5;
+    h->launches += 3 + (P.GS > 0);
+}
+
+// Final refresh (R13): r = M~x - b, f, g = grad f(x) and the KKT report.
+static void launch_refresh(lbfgsb_t* h, const Prob& P)
+{
+    cudaStream_t st = h->st;
+    launch_sep(P, st, SEP_SETUP, P.x);
+    launch_fwd(P, st, FWD_SETUP, P.x, nullptr);
+    launch_bwd(P, st, BWD_REFRESH, nullptr, nullptr);
+    launch_kkt(P, st);
+    h->launches += 3 + (P.GS > 0);
 }
 
 static lbfgsb_err ensure_events(lbfgsb_t* h)
@@ -439,13 +453,14 @@ static lbfgsb_err ensure_events(lbfgsb_t* h)
 static lbfgsb_err run_chunk(lbfgsb_t* h, const Prob& P)
 {
     const int chunk = h->o.check_every;
+    const int per = 3 + (P.GS > 0);
     if (h->o.use_graph) {
         if (!h->gexec || std::memcmp(&h->gkey, &P, sizeof(Prob)) != 0 || h->gchunk != chunk) {
             if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
             cudaGraph_t g = nullptr;
             CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
             const int64_t l0 = h->launches;
-            for (int i = 0; i < chunk; ++i) launch_iteration(h, P, PH_GRAM, h->o.profile ? 4 * i : -1);
+            for (int i = 0; i < chunk; ++i) launch_iteration(h, P, h->o.profile ? 4 * i : -1);
             h->launches = l0;
             cudaError_t e = cudaStreamEndCapture(h->st, &g);
             if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
@@ -456,9 +471,9 @@ static lbfgsb_err run_chunk(lbfgsb_t* h, const Prob& P)
             h->gchunk = chunk;
         }
         CK(cudaGraphLaunch(h->gexec, h->st));
-        h->launches += (int64_t)kPerIter * chunk;
+        h->launches += (int64_t)per * chunk;
     } else {
-        for (int i = 0; i < chunk; ++i) launch_iteration(h, P, PH_GRAM, h->o.profile ? 4 * i : -1);
+        for (int i = 0; i < chunk; ++i) launch_iteration(h, P, h->o.profile ? 4 * i : -1);
     }
     CK(cudaGetLastError());
     return LBFGSB_OK;
@@ -500,53 +515,48 @@ static lbfgsb_err solve_lsq(lbfgsb_t* h, const Prob& P, double* x_user, double t
     auto t0 = std::chrono::steady_clock::now();
     if (x_user != P.x) CK(cudaMemcpyAsync(P.x, x_user, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
     init_ctrl(h, tol);
+    h->hc->n_fg = 1;
     TRY(ctrl_to_dev(h));
-    launch_refresh(h, P, true);
+    launch_setup(h, P);
     CK(cudaGetLastError());
     TRY(ctrl_to_host(h));
     if (h->hc->nonfinite) return fail(LBFGSB_ERR_NONFINITE, "f(x0) is not finite");
-    h->hc->n_fg = 1;
-    TRY(ctrl_to_dev(h));
     if (h->o.profile) TRY(ensure_events(h));
 
-    const int64_t guard = h->o.max_iters + 16;
+    const int64_t guard = h->o.max_iters + 64;
     int64_t loops = 0;
-    for (;;) {
+    while (!h->hc->done) {
         const long long k0 = h->hc->k;
         TRY(run_chunk(h, P));
         TRY(ctrl_to_host(h));
         collect_profile(h, h->hc->k - k0);
-        if (h->hc->done) break;
         if (++loops > guard) return fail(LBFGSB_ERR_CUDA, "solver loop did not terminate");
         // ---- stall handling (rare): finish the stalled iteration on the host's cue
         while (h->hc->stall && !h->hc->done) {
             const int s = h->hc->stall;
             h->hc->stall = 0;
             if (s == ST_FALLBACK) {
-                // R14: clear the history, steepest descent on S, redo Alg. 2 + search
+                // R14: clear the history, d[S] = -g[S], redo Alg. 2 + the search
                 h->hc->fallback = 1;
                 h->hc->nh = 0;
                 h->hc->n_fallbacks += 1;
+                h->hc->coef[0] = -1.0;
                 TRY(ctrl_to_dev(h));
-                launch_iteration(h, P, PH_GRAM, -1);
-            } else {  // ST_LS_CONT: next batch of Armijo trials
+                launch_iteration(h, P, -1);
+            } else {  // ST_LS_CONT: next batch of Armijo trials, then the gradient pass
                 TRY(ctrl_to_dev(h));
-                launch_ls(P, h->st, LS_ITER_NEXT, nullptr);
-                launch_ls_decide(P, h->st, LS_ITER_NEXT, nullptr, 0);
-                launch_rupd(P, h->st);
+                launch_sep(P, h->st, SEP_NEXT, nullptr);
+                launch_ls(P, h->st, LS_NEXT, nullptr, nullptr, nullptr, 0);
                 launch_bwd(P, h->st, BWD_ITER, nullptr, nullptr);
-                h->launches += 4;
+                h->launches += 2 + (P.GS > 0);
             }
             CK(cudaGetLastError());
             TRY(ctrl_to_host(h));
         }
-        if (h->hc->done) break;
     }
     const Ctrl fin = *h->hc;
-    // final refresh: r = M~x - b, g, f; KKT report (R13, R15)
-    launch_refresh(h, P, false);
-    launch_kkt(P, h->st);
-    h->launches += 2;
+    h->nact_total += fin.nact;
+    launch_refresh(h, P);
     CK(cudaGetLastError());
     TRY(ctrl_to_host(h));
     if (x_user != P.x) CK(cudaMemcpyAsync(x_user, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
@@ -570,8 +580,8 @@ static lbfgsb_err solve_lsq(lbfgsb_t* h, const Prob& P, double* x_user, double t
 }
 
 // ------------------------------------------------------------------ callback objective
-// Host-driven Alg. 1 for user objectives: the direction pipeline runs on the
-// device kernels; each Armijo trial calls the user's fg.
+// Host-driven Alg. 1 for user objectives: working set, Gram, Alg. 3 and
+// Alg. 2 run in the device kernels; each Armijo trial calls the user's fg.
 static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_user, double tol,
                            lbfgsb_result* res)
 {
@@ -594,11 +604,9 @@ static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_us
     c->n_fg = 1;
     TRY(ctrl_to_dev(h));
     for (;;) {
-        launch_gram(P, st, 0);
-        launch_recur(P, st, 0);
+        launch_gram_recur(P, st, 0);
         launch_dir(P, st, 0);
-        launch_branch(P, st, 0);
-        h->launches += 4;
+        h->launches += 2;
         CK(cudaGetLastError());
         TRY(ctrl_to_host(h));
         if (c->done) break;
@@ -635,7 +643,7 @@ static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_us
     }
     const Ctrl fin = *c;
     launch_kkt(P, st);
-    h->launches += 2;
+    h->launches += 1;
     CK(cudaGetLastError());
     TRY(ctrl_to_host(h));
     CK(cudaMemcpyAsync(x_user, P.x, nb, cudaMemcpyDeviceToDevice, st));
@@ -662,7 +670,7 @@ extern "C" lbfgsb_err lbfgsb_solve(lbfgsb_t* h, const lbfgsb_objective* obj, dou
     if (obj->kind == 1) return solve_cb(h, obj, x, t, res);
     Prob P;
     TRY(make_prob(h, obj, P));
-    set_sep(P, sm_count());
+    set_sep(P);
     h->hc->rho = 1.0;
     std::memset(h->hc->lam, 0, sizeof h->hc->lam);
     std::memset(h->hc->rhs, 0, sizeof h->hc->rhs);
@@ -706,12 +714,14 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
     if (neq + nin > MAXC) return fail(LBFGSB_ERR_UNSUPPORTED, "at most %d linear constraints", MAXC);
     if ((neq && (!cons->E || !cons->e)) || (nin && (!cons->G || !cons->hv)))
         return fail(LBFGSB_ERR_ARG, "constraint data missing");
+    if (!(ao.rho0 > 0) || !(ao.rho_factor > 1) || ao.max_outer < 1)
+        return fail(LBFGSB_ERR_ARG, "invalid al_opts");
     Prob P;
     TRY(make_prob(h, obj, P));
     P.n_eq = neq; P.n_in = nin;
     for (int k = 0; k < neq; ++k) P.Ecol[k] = cons->E + (int64_t)k * h->n;
     for (int k = 0; k < nin; ++k) P.Ecol[neq + k] = cons->G + (int64_t)k * h->n;
-    set_sep(P, sm_count());
+    set_sep(P);
     const double tol = h->o.tol;
     // x^0 = clip(0) (R19), lambda = 0, mu = 0, rho = rho0
     CK(cudaMemsetAsync(x, 0, sizeof(double) * h->n, h->st));
@@ -735,12 +745,14 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
         }
         return v;
     };
-    // violation at x^0
+    // constraint values at x^0 (one setup pass)
     set_al();
     CK(cudaMemcpyAsync(P.x, x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
     init_ctrl(h, tol);
     TRY(ctrl_to_dev(h));
-    launch_refresh(h, P, true);
+    launch_clip(P, h->st);
+    launch_sep(P, h->st, SEP_SETUP, P.x);
+    launch_fwd(P, h->st, FWD_SETUP, P.x, nullptr);
     CK(cudaGetLastError());
     TRY(ctrl_to_host(h));
     CK(cudaMemcpyAsync(x, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
@@ -802,25 +814,27 @@ extern "C" lbfgsb_err lbfgsb_op_gemv(const lbfgsb_objective* obj, const double* 
                                      void* cuda_stream)
 {
     if (!obj || obj->kind != 0 || !p || !q) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LBFGSB_ERR_CUDA, "no device");
     init_kernels();
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    const int sms = sm_count();
     Prob P;
     std::memset(&P, 0, sizeof P);
     P.m = obj->m; P.ncols = obj->ncols; P.ld = obj->ld; P.M = obj->M;
     P.colscale = obj->colscale; P.split = obj->split;
     P.n = obj->split ? 2 * obj->ncols : obj->ncols;
-    P.fwd_rb = (int)cdiv(P.m, FWD_ROWS);
-    int64_t cc = clampi(cdiv(4LL * sms, P.fwd_rb), 1, clampi(cdiv(P.ncols, 32), 1, 1 << 20));
-    P.fwd_chunk = cdiv(P.ncols, cc);
-    P.fwd_cc = (int)cdiv(P.ncols, P.fwd_chunk);
+    gemv_geometry(P);
     double* qpart = nullptr;
-    CK(cudaMallocAsync(&qpart, sizeof(double) * (size_t)P.m * P.fwd_cc, st));
+    unsigned* tick = nullptr;
+    CK(cudaMallocAsync(&qpart, sizeof(double) * (size_t)P.m * P.CC, st));
+    CK(cudaMallocAsync(&tick, sizeof(unsigned) * (NTICKETS + 8192), st));
+    CK(cudaMemsetAsync(tick, 0, sizeof(unsigned) * (NTICKETS + 8192), st));
     P.qpart = qpart;
-    launch_fwd(P, st, FWD_P, p);
-    launch_resid(P, st, 0, q);
+    P.tickets = tick;
+    launch_fwd(P, st, FWD_P, p, q);
     cudaError_t e = cudaGetLastError();
     cudaFreeAsync(qpart, st);
+    cudaFreeAsync(tick, st);
     if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "gemv: %s", cudaGetErrorString(e));
     CK(cudaStreamSynchronize(st));
     return LBFGSB_OK;
@@ -830,6 +844,8 @@ extern "C" lbfgsb_err lbfgsb_op_gemvt(const lbfgsb_objective* obj, const double*
                                       void* cuda_stream)
 {
     if (!obj || obj->kind != 0 || !r || !g) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LBFGSB_ERR_CUDA, "no device");
     init_kernels();
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     Prob P;
@@ -837,7 +853,9 @@ extern "C" lbfgsb_err lbfgsb_op_gemvt(const lbfgsb_objective* obj, const double*
     P.m = obj->m; P.ncols = obj->ncols; P.ld = obj->ld; P.M = obj->M;
     P.colscale = obj->colscale; P.split = obj->split;
     P.n = obj->split ? 2 * obj->ncols : obj->ncols;
-    P.bwd_blocks = (int)cdiv(P.ncols, BWD_NB);
+    gemv_geometry(P);
+    P.rbuf[0] = const_cast<double*>(r);
+    P.rbuf[1] = const_cast<double*>(r);
     launch_bwd(P, st, BWD_PLAIN, r, g);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
@@ -862,10 +880,8 @@ extern "C" lbfgsb_err lbfgsb_op_direction(lbfgsb_t* h, const double* x, const do
     h->hc->nh = nh;
     h->hc->head = nh > 0 ? nh - 1 : h->mh - 1;
     TRY(ctrl_to_dev(h));
-    launch_gram(P, st, 1);
-    launch_recur(P, st, 1);
+    launch_gram_recur(P, st, 1);
     launch_dir(P, st, 1);
-    launch_branch(P, st, 1);
     CK(cudaGetLastError());
     TRY(ctrl_to_host(h));
     const int br = h->hc->branch;
@@ -888,16 +904,14 @@ extern "C" lbfgsb_err lbfgsb_op_trials(lbfgsb_t* h, const lbfgsb_objective* obj,
     if (ntrials < 1 || ntrials > KT) return fail(LBFGSB_ERR_ARG, "ntrials in [1, %d]", KT);
     Prob P;
     TRY(make_prob(h, obj, P));
-    set_sep(P, sm_count());
-    P.r = const_cast<double*>(r);
-    P.q = const_cast<double*>(q);
+    set_sep(P);
     P.x = const_cast<double*>(x);
     init_ctrl(h, h->o.tol);
     h->hc->alpha0 = alpha0;
     h->hc->rho = 1.0;
     TRY(ctrl_to_dev(h));
-    launch_ls(P, h->st, LS_OP, p);
-    launch_ls_decide(P, h->st, LS_OP, h->fout.d(), ntrials);
+    launch_sep(P, h->st, SEP_OP, p);
+    launch_ls(P, h->st, LS_OP, r, q, h->fout.d(), ntrials);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(f_out, h->fout.p, sizeof(double) * ntrials, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
@@ -908,16 +922,22 @@ extern "C" lbfgsb_err lbfgsb_profile_get(lbfgsb_t* h, int32_t cap, const char** 
                                          int64_t* launches, int32_t* count, int32_t reset)
 {
     if (!h || !count) return fail(LBFGSB_ERR_ARG, "NULL handle or count");
-    static const char* kn[3] = {"gemv_active (k_fwd)", "gemvT_epi (k_bwd)", "all_kernel_launches"};
-    const double vals[3] = {h->prof_ms[0], h->prof_ms[1], 0.0};
-    const int64_t cnts[3] = {h->prof_n[0], h->prof_n[1], h->launches};
+    static const char* kn[4] = {"gemv_active (k_fwd)", "gemvT_epi (k_bwd)", "all_kernel_launches",
+                                "fwd_active_columns"};
+    const double vals[4] = {h->prof_ms[0], h->prof_ms[1], 0.0, 0.0};
+    const int64_t cnts[4] = {h->prof_n[0], h->prof_n[1], h->launches, h->nact_total};
     int c = 0;
-    for (int i = 0; i < 3 && i < cap; ++i, ++c) {
+    for (int i = 0; i < 4 && i < cap; ++i, ++c) {
         if (names) names[i] = kn[i];
         if (ms) ms[i] = vals[i];
         if (launches) launches[i] = cnts[i];
     }
     *count = c;
-    if (reset) { h->prof_ms[0] = h->prof_ms[1] = 0; h->prof_n[0] = h->prof_n[1] = 0; h->launches = 0; }
+    if (reset) {
+        h->prof_ms[0] = h->prof_ms[1] = 0;
+        h->prof_n[0] = h->prof_n[1] = 0;
+        h->launches = 0;
+        h->nact_total = 0;
+    }
     return LBFGSB_OK;
 }
