@@ -215,6 +215,7 @@ def run_ours(args):
     bwd_ms, bwd_n = prof["gemvT_epi (k_bwd)"]
     fwd_ms, fwd_n = prof["gemv_active (k_fwd)"]
     launches = prof["all_kernel_launches"][1]
+    nact = prof.get("fwd_active_columns", (0, 0))[1]
     # algorithmic bytes of one k_bwd launch: A (8 m n) + r (8 m) + per-variable
     # epilogue reads x, g, p, l, u and writes x, g, s, y (9 x 8 n)
     bwd_bytes = 8 * M_ROWS * N_COLS + 8 * M_ROWS + 9 * 8 * N_COLS
@@ -226,12 +227,22 @@ def run_ours(args):
         traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "k_bwd (gemvT_epi: g = M^T r + fused Alg. 1 epilogue)",
+                "kernel": "k_bwd_s (gemvT_epi: g = M^T r + fused Alg. 1 epilogue, Gram, Alg. 3 tail)",
                 "bytes_per_launch": bwd_bytes, "avg_launch_us": bwd_avg_s * 1e6,
                 "launches": bwd_n, "peak_source": peak_src,
                 "share_of_step": (bwd_ms / ms) if ms else None,
                 "k_fwd_share_of_step": (fwd_ms / ms) if ms else None,
                 "k_fwd_avg_launch_us": 1e3 * fwd_ms / max(fwd_n, 1)}
+    if fwd_n and nact:
+        # k_fwd reads only the active columns: 8 m n_p + qpart / r / q vectors
+        cols = nact / fwd_n
+        fb = 8 * M_ROWS * cols + 8 * M_ROWS * 4 + 8 * 3 * N_COLS
+        roofline["k_fwd_active_cols_avg"] = cols
+        roofline["k_fwd_bytes_per_launch"] = fb
+        roofline["k_fwd_achieved_gbs"] = fb / (fwd_ms / fwd_n / 1e3) / 1e9
+        # whole-iteration algorithmic bandwidth (B_it = 8 m (n + n_p) + V)
+        v_bytes = 8 * ((4 * M_HIST + 16) * N_COLS + 8 * M_ROWS)
+        roofline["iteration_bytes_avg"] = 8 * M_ROWS * (N_COLS + cols) + v_bytes
 
     # ---- e2e: lbfgsb_solve_lsq_host from pinned host buffers
     Mh = torch.from_numpy(np.ascontiguousarray(p.M.T)).pin_memory().numpy().T   # Fortran view

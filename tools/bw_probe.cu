@@ -1,0 +1,161 @@
+// bw_probe.cu -- achievable HBM READ bandwidth on this B200 (the ceiling the
+// GEMV kernels stream against).  Variants:
+//   ldg<U>  : grid-stride LDG.128 sum, 148*k CTAs, U loads in flight per thread
+//   bulk    : 1 CTA/SM, cp.async.bulk (TMA 1-D) ring of S stages x B bytes
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bw_probe tools/bw_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+template <int U>
+__global__ void ldg_sum(const double2* __restrict__ a, size_t n2, double* out)
+{
+    double s = 0.0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < n2; i += U * stride) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(a + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += v[u].x + v[u].y;
+    }
+    for (; i < n2; i += stride) { double2 v = a[i]; s += v.x + v.y; }
+    if (s == 123.456) out[0] = s;
+}
+
+// contiguous chunk per CTA (like a persistent column range)
+template <int U>
+__global__ void ldg_chunk(const double2* __restrict__ a, size_t n2, double* out)
+{
+    const size_t per = (n2 + gridDim.x - 1) / gridDim.x;
+    const size_t b0 = blockIdx.x * per, b1 = b0 + per < n2 ? b0 + per : n2;
+    double s = 0.0;
+    size_t i = b0 + threadIdx.x;
+    const size_t stride = blockDim.x;
+    for (; i + (U - 1) * stride < b1; i += U * stride) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(a + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += v[u].x + v[u].y;
+    }
+    for (; i < b1; i += stride) { double2 v = a[i]; s += v.x + v.y; }
+    if (s == 123.456) out[0] = s;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
+{
+    asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}" :: "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(phase));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                    "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+template <int STAGES, int BYTES>
+__global__ void bulk_sum(const double* __restrict__ a, size_t n, double* out)
+{
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t full[STAGES];
+    const size_t per = (n + gridDim.x - 1) / gridDim.x;
+    const size_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+    const size_t elems = BYTES / 8;
+    const size_t nchunks = (b1 - b0 + elems - 1) / elems;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    auto issue = [&](size_t c) {
+        const int s = c % STAGES;
+        const size_t e0 = b0 + c * elems;
+        const size_t cnt = e0 + elems < b1 ? elems : b1 - e0;
+        mbar_expect_tx(&full[s], (unsigned)(cnt * 8));
+        bulk_g2s(sm + (size_t)s * BYTES, a + e0, (unsigned)(cnt * 8), &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (size_t c = 0; c < (size_t)STAGES && c < nchunks; ++c) issue(c);
+    double acc = 0.0;
+    for (size_t c = 0; c < nchunks; ++c) {
+        const int s = c % STAGES;
+        mbar_wait(&full[s], (unsigned)((c / STAGES) & 1));
+        const size_t e0 = b0 + c * elems;
+        const size_t cnt = e0 + elems < b1 ? elems : b1 - e0;
+        const double* buf = reinterpret_cast<const double*>(sm + (size_t)s * BYTES);
+        for (size_t k = threadIdx.x; k < cnt; k += blockDim.x) acc += buf[k];
+        __syncthreads();
+        if (threadIdx.x == 0 && c + STAGES < nchunks) issue(c + STAGES);
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
+template <typename F>
+float timeit(F f, int reps)
+{
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    f();
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) f();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+    return ms / reps;
+}
+
+int main()
+{
+    const size_t bytes = 1600000000ull;     // the C2 matrix
+    const size_t n = bytes / 8;
+    double* a; double* out;
+    cudaMalloc(&a, bytes); cudaMalloc(&out, 8);
+    cudaMemset(a, 0, bytes);
+    int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    auto rep = [&](const char* name, float ms) { printf("%-36s %8.1f us  %7.1f GB/s\n", name, ms * 1e3, bytes / (ms * 1e-3) / 1e9); };
+    for (int k : {1, 2, 4, 8}) {
+        char nm[64];
+        snprintf(nm, 64, "ldg_sum<4> grid=%dx%d tpb=256", sms, k);
+        rep(nm, timeit([&] { ldg_sum<4><<<sms * k, 256>>>(a2, n / 2, out); }, 10));
+        snprintf(nm, 64, "ldg_sum<8> grid=%dx%d tpb=256", sms, k);
+        rep(nm, timeit([&] { ldg_sum<8><<<sms * k, 256>>>(a2, n / 2, out); }, 10));
+        snprintf(nm, 64, "ldg_chunk<8> grid=%dx%d tpb=256", sms, k);
+        rep(nm, timeit([&] { ldg_chunk<8><<<sms * k, 256>>>(a2, n / 2, out); }, 10));
+    }
+    rep("ldg_chunk<8> grid=148 tpb=512", timeit([&] { ldg_chunk<8><<<sms, 512>>>(a2, n / 2, out); }, 10));
+    rep("ldg_chunk<16> grid=148 tpb=512", timeit([&] { ldg_chunk<16><<<sms, 512>>>(a2, n / 2, out); }, 10));
+    rep("ldg_chunk<8> grid=148 tpb=1024", timeit([&] { ldg_chunk<8><<<sms, 1024>>>(a2, n / 2, out); }, 10));
+    {
+        constexpr int S = 4, B = 32768;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 4x32KB 1CTA/SM tpb=256", timeit([&] { bulk_sum<S, B><<<sms, 256, S * B>>>(a, n, out); }, 10));
+    }
+    {
+        constexpr int S = 6, B = 32768;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 6x32KB 1CTA/SM tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+    }
+    {
+        constexpr int S = 4, B = 16384;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 4x16KB 2CTA/SM tpb=256", timeit([&] { bulk_sum<S, B><<<sms * 2, 256, S * B>>>(a, n, out); }, 10));
+    }
+    // copy reference (cudaMemcpy D2D, read+write counted)
+    double* b; cudaMalloc(&b, bytes / 2);
+    float ms = timeit([&] { cudaMemcpyAsync(b, a, bytes / 2, cudaMemcpyDeviceToDevice); }, 10);
+    printf("%-36s %8.1f us  %7.1f GB/s (read+write)\n", "memcpy D2D 0.8GB", ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+    printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
