@@ -118,16 +118,27 @@ lbfgsb_err lbfgsb_create(int64_t n, int32_t m_hist, const double* lower, const d
                          const lbfgsb_opts* opts /* NULL = defaults */, void* cuda_stream,
                          lbfgsb_t** out);
 
-/* Column-sharded handle: this rank owns n_local of the
- * n_global variables (a contiguous block of columns of M~).  The library
- * creates its own NCCL communicator from the 128-byte ncclUniqueId
- * (host) that the caller broadcast (e.g. with torch.distributed).
- * Returns LBFGSB_ERR_UNSUPPORTED when the library was built without NCCL. */
+/* Column-sharded handle: this rank
+ * owns n_local of the n_global variables (a contiguous block of columns of
+ * M~; for split objectives the u and v halves of those columns).  M, c,
+ * bounds, x and the constraint columns passed later are this rank's block;
+ * b is the full (replicated) m-vector.  Each iteration all-gathers, over
+ * NCCL, the m-length partial of q = M~p and small packed reductions (Alg. 2
+ * sums, separable trial sums, the Gram of Alg. 3), and every rank reduces
+ * them in rank order, so all ranks take bit-identical decisions.  The library
+ * creates its own NCCL communicator from the 128-byte ncclUniqueId (host)
+ * obtained on rank 0 with lbfgsb_nccl_unique_id and broadcast by the caller
+ * (e.g. with torch.distributed); the calling thread's current CUDA device is
+ * used.  Returns LBFGSB_ERR_UNSUPPORTED when built without NCCL, NCCL on
+ * communicator errors. */
 lbfgsb_err lbfgsb_create_sharded(int64_t n_local, int64_t n_global, int32_t m_hist,
                                  const double* lower_local, const double* upper_local,
                                  const lbfgsb_opts* opts, void* cuda_stream,
                                  const void* nccl_unique_id /* (host) 128 bytes */,
                                  int32_t rank, int32_t nranks, lbfgsb_t** out);
+
+/* Fill out (host, 128 bytes) with a fresh ncclUniqueId (call on rank 0). */
+lbfgsb_err lbfgsb_nccl_unique_id(void* out);
 
 void lbfgsb_destroy(lbfgsb_t* h);
 

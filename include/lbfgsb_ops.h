@@ -53,6 +53,17 @@ lbfgsb_err lbfgsb_op_trials(lbfgsb_t* h, const lbfgsb_objective* obj, const doub
                             const double* q, const double* x, const double* p, double alpha0,
                             int32_t ntrials, double* f_out);
 
+/* Loopback verification of the column-sharded path on ONE device: the nranks
+ * handles hs[p] (created with lbfgsb_create, n = that shard's variables, all
+ * on the same device) act as logical ranks p = 0..nranks-1 of a sharded
+ * solve of the concatenated problem, objs[p] / xs[p] their column blocks.
+ * The cross-rank exchange is the same rank-ordered all-gather of packs that
+ * lbfgsb_create_sharded performs over NCCL, done with device copies, and all
+ * work runs on hs[0]'s stream.  res (host) is rank 0's outcome (all ranks
+ * decide identically).  Errors: ARG, DIM, CUDA. */
+lbfgsb_err lbfgsb_solve_loopback(lbfgsb_t* const* hs, const lbfgsb_objective* const* objs,
+                                 double* const* xs, int32_t nranks, double tol, lbfgsb_result* res);
+
 /* Device time of the hot-path GEMV launches of the solves run on this
  * handle since the last reset (host): names[i] / ms[i] (summed event time)
  * / launches[i], i < *count (<= cap).  Recorded only when opts.profile = 1

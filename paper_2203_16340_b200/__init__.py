@@ -18,7 +18,8 @@ from dataclasses import dataclass
 from . import _build
 
 __all__ = ["Options", "ALOptions", "Result", "ALResult", "Solver", "LSQObjective",
-           "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor"]
+           "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor",
+           "solve_loopback", "nccl_unique_id"]
 
 _c_d, _c_i32, _c_i64, _c_vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
 
@@ -99,10 +100,13 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_op_trials.argtypes = [vp, vp, vp, vp, vp, vp, _c_d, _c_i32, C.POINTER(_c_d)]
     L.lbfgsb_profile_get.argtypes = [vp, _c_i32, C.POINTER(C.c_char_p), C.POINTER(_c_d),
                                      C.POINTER(_c_i64), ip, _c_i32]
+    L.lbfgsb_solve_loopback.argtypes = [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), _c_i32, _c_d,
+                                        C.POINTER(_Res)]
+    L.lbfgsb_nccl_unique_id.argtypes = [vp]
     for name in ("lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
                  "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
-                 "lbfgsb_profile_get"):
+                 "lbfgsb_profile_get", "lbfgsb_solve_loopback", "lbfgsb_nccl_unique_id"):
         getattr(L, name).restype = _c_i32
     _lib = L
     return L
@@ -272,18 +276,27 @@ def _wrap(ptr, n):
 
 class Solver:
     """lbfgsb_create handle: n variables, box [lower, upper] (CUDA fp64 tensors
-    or None for -inf / +inf), m_hist curvature pairs."""
+    or None for -inf / +inf), m_hist curvature pairs.  With ``nccl_id`` (the
+    128-byte ncclUniqueId), ``rank`` and ``nranks`` it is an
+    lbfgsb_create_sharded handle owning n of ``n_global`` variables."""
 
     def __init__(self, n, m_hist=5, lower=None, upper=None, opts: Options | None = None,
-                 stream=None):
+                 stream=None, nccl_id: bytes | None = None, rank=0, nranks=1, n_global=None):
         L = load()
         self.n = int(n)
         self.m_hist = int(m_hist)
         self.opts = opts or Options()
         o = self.opts._c()
         h = C.c_void_p()
-        _check(L.lbfgsb_create(self.n, self.m_hist, _ptr(lower), _ptr(upper), C.byref(o),
-                               _stream_ptr(stream), C.byref(h)))
+        if nccl_id is None:
+            _check(L.lbfgsb_create(self.n, self.m_hist, _ptr(lower), _ptr(upper), C.byref(o),
+                                   _stream_ptr(stream), C.byref(h)))
+        else:
+            idb = C.create_string_buffer(bytes(nccl_id), 128)
+            _check(L.lbfgsb_create_sharded(self.n, int(n_global if n_global is not None else n),
+                                           self.m_hist, _ptr(lower), _ptr(upper), C.byref(o),
+                                           _stream_ptr(stream), C.cast(idb, C.c_void_p), int(rank),
+                                           int(nranks), C.byref(h)))
         self._h = h
 
     def close(self):
@@ -370,6 +383,26 @@ class Solver:
         k = _c_i32()
         _check(_lib.lbfgsb_profile_get(self._h, 8, names, ms, cnt, C.byref(k), int(bool(reset))))
         return {names[i].decode(): (ms[i], cnt[i]) for i in range(k.value)}
+
+
+def nccl_unique_id() -> bytes:
+    """lbfgsb_nccl_unique_id: 128 bytes to broadcast from rank 0."""
+    buf = C.create_string_buffer(128)
+    _check(load().lbfgsb_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
+
+
+def solve_loopback(solvers, objs, xs, tol=0.0) -> Result:
+    """lbfgsb_solve_loopback: the column-sharded path with len(solvers) logical
+    ranks on one GPU (verification of the NCCL path's exchange and decisions)."""
+    R = len(solvers)
+    hs = (_c_vp * R)(*[s._h.value for s in solvers])
+    os_ = (_c_vp * R)(*[o._h.value for o in objs])
+    xp = (_c_vp * R)(*[x.data_ptr() for x in xs])
+    r = _Res()
+    _check(load().lbfgsb_solve_loopback(hs, os_, xp, R, float(tol), C.byref(r)))
+    return Result(r.f, r.pg_inf, r.gfree_inf, r.seconds, r.iters, r.n_fg, r.n_backtracks,
+                  r.n_free, r.n_fallbacks, r.status, r.last_branch)
 
 
 def op_gemv(obj: LSQObjective, p, q, stream=None):

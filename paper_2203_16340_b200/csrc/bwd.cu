@@ -230,8 +230,34 @@ __device__ void gram_tail(const Prob& P, Ctrl* C, const EpiCtx& E, const double*
     for (int e = threadIdx.x; e < nent; e += blockDim.x) P.gram_grp[(int64_t)grp * GRAM_STRIDE + e] = Gs[e];
     if (!last_cta(P.tickets + T_BWD_G2, ngrp)) return;
     reduce_parts(P.gram_grp, ngrp, GRAM_STRIDE, nent, sel, buf, bufn, stash, Gs);
+    if (P.sharded) {                                         // sharded: local Gram pack
+        for (int e = threadIdx.x; e < nent; e += blockDim.x) P.pk_loc[off_gram(P) + e] = Gs[e];
+        return;
+    }
     if (threadIdx.x != 0) return;
     if (E.iter) C->rsel = C->rsel ^ 1;
+    recur_decide(P, C, Gs, nh, 0);
+}
+
+// Sharded: reduce the all-gathered Gram packs in rank order, then Alg. 3.
+__global__ void __launch_bounds__(NT) k_gram_decide(Prob P, int mode)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    __shared__ double Gs[MAXE + MAXH + 2];
+    const int nh = C->nh, nb = 2 * nh + 1, ne = nb * (nb + 1) / 2;
+    const int ntot = ne + (P.screen_full ? nh : 0), nent = ntot + 2;
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        double s = e == ntot ? -INFINITY : 0.0;
+        for (int p = 0; p < P.nranks; ++p) {
+            const double v = P.gram_all[(int64_t)p * GRAM_STRIDE + e];
+            s = e == ntot ? (v > s ? v : s) : s + v;
+        }
+        Gs[e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (mode == BWD_ITER) C->rsel = C->rsel ^ 1;
     recur_decide(P, C, Gs, nh, 0);
 }
 
@@ -422,6 +448,11 @@ static void bwd_init()
 }
 
 int bwd_ctas_per_sm() { bwd_init(); return g_bwd_occ; }
+
+void launch_gram_decide(const Prob& P, cudaStream_t st, int bwd_mode)
+{
+    k_gram_decide<<<1, NT, 0, st>>>(P, bwd_mode);
+}
 
 // smem bytes k_bwd_s needs for this problem (0 = does not fit)
 static size_t bwd_s_smem(const Prob& P, int G)

@@ -9,7 +9,7 @@
 namespace lb {
 
 // ticket indices
-constexpr int T_DIR = 0, T_FWD_ALL = 1, T_LS = 2, T_KKT = 3, T_BWD_G2 = 4, T_GRAM = 5;
+constexpr int T_DIR = 0, T_FWD_ALL = 1, T_LS = 2, T_KKT = 3, T_BWD_G2 = 4, T_GRAM = 5, T_SEP = 6;
 constexpr int T_FWD_RB = 64;            // + row block (<= 8192)
 constexpr int T_BWD_G1 = 64 + 8192;     // + group (<= 8000)
 static_assert(T_BWD_G1 + 8000 <= NTICKETS + 8192, "ticket space");

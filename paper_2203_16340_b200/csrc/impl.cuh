@@ -111,13 +111,29 @@ struct Prob {
     int GB;                 // k_bwd persistent CTAs
     int GS;                 // k_sep CTAs (0: no separable part)
     int GLS;                // k_ls CTAs (host-driven trial batches)
+    // column sharding: nranks > 1 makes every tail write
+    // a LOCAL pack; the host all-gathers the packs and a *_decide kernel
+    // reduces them in rank order, so all ranks take identical decisions.
+    int nranks;
+    int sharded;            // 1: sharded protocol (nranks > 1, or a 1-rank NCCL handle)
+    double* pk_loc;         // [QS: m + KT*NSEP][DIR: 4][GRAM: GRAM_STRIDE][KKT: 4]
+    double* qs_all;         // [nranks][m + KT*NSEP]   (q partial | separable trial sums)
+    double* dir_all;        // [nranks][4]
+    double* gram_all;       // [nranks][GRAM_STRIDE]
+    double* kkt_all;        // [nranks][4]
 };
+
+__host__ __device__ inline int64_t qs_len(const Prob& P) { return P.m + (int64_t)KT * NSEP; }
+__host__ __device__ inline int64_t off_dir(const Prob& P) { return qs_len(P); }
+__host__ __device__ inline int64_t off_gram(const Prob& P) { return qs_len(P) + 4; }
+__host__ __device__ inline int64_t off_kkt(const Prob& P) { return qs_len(P) + 4 + GRAM_STRIDE; }
+__host__ __device__ inline int64_t pk_len(const Prob& P) { return qs_len(P) + 4 + GRAM_STRIDE + 4; }
 
 // ---- launch modes
 enum FwdMode : int { FWD_ITER = 0, FWD_SETUP = 1, FWD_P = 2 };
 enum BwdMode : int { BWD_ITER = 0, BWD_SETUP = 1, BWD_PLAIN = 2, BWD_REFRESH = 3 };
 enum SepMode : int { SEP_ITER = 0, SEP_NEXT = 1, SEP_SETUP = 2, SEP_OP = 3 };
-enum LsMode : int { LS_NEXT = 0, LS_OP = 1 };
+enum LsMode : int { LS_NEXT = 0, LS_OP = 1, LS_SH_ITER = 2, LS_SH_SETUP = 3 };
 
 // ---- launchers (kernels.cu)
 void init_kernels();
@@ -133,6 +149,10 @@ void launch_ls(const Prob& P, cudaStream_t st, int mode, const double* r, const 
 void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, double* gout);
 void launch_gram_recur(const Prob& P, cudaStream_t st, int op_mode);
 void launch_kkt(const Prob& P, cudaStream_t st);
+// sharded decisions (after the host's all-gather of the local packs)
+void launch_dir_decide(const Prob& P, cudaStream_t st);
+void launch_gram_decide(const Prob& P, cudaStream_t st, int bwd_mode);
+void launch_kkt_decide(const Prob& P, cudaStream_t st);
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);
 void launch_cb_trial(const Prob& P, cudaStream_t st, double alpha, double* xt);
 void launch_cb_commit(const Prob& P, cudaStream_t st, const double* xt, const double* gt, int slot);

@@ -25,6 +25,27 @@ __global__ void k_clip(Prob P)
         P.x[j] = clipd(P.x[j], P.l[j], P.u[j]);          // feasible x^0
 }
 
+// Alg. 2 line 3 decision (R9) and the line-search bound alpha_0 (R10).
+__device__ __forceinline__ void dir_decide(const Prob& P, Ctrl* C, const double* res, int op_mode)
+{
+    const double eps = P.eps;
+    const double Spg = res[0], Spp = res[1], Stg = res[2], amin_all = res[3];
+    const int projected = (Spg <= -eps * Spp && Spp >= eps) ? 1 : 0;    // Alg. 2 line 3
+    double amax = projected ? 1.0 : amin_all;
+    if (amax < 0.0) amax = 0.0;
+    const double gp = projected ? Spg : Stg;
+    C->branch = projected;
+    C->gp = gp;
+    C->amax = amax;
+    C->alpha0 = amax < 1.0 ? amax : 1.0;                        // R10
+    C->ls_batch = 0;
+    if (op_mode) return;
+    if (!(gp < 0.0)) {                                          // guard (R14)
+        if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }
+        else C->stall = ST_FALLBACK;
+    }
+}
+
 // ------------------------------------------------------------------ a6: direction + Alg. 2
 // d = sum_b coef_b B_b on S, 0 off S; Alg. 2:
 // projected candidate pp = clip(x + d) - x, truncated candidate pt = d with
@@ -91,22 +112,26 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
     if (!last_cta(P.tickets + T_DIR, gridDim.x)) return;
     reduce_parts(P.dir_part, gridDim.x, 4, 4, [](int e) { return e == 3 ? 2 : 0; }, buf, 1024,
                  stash, res);
-    if (threadIdx.x != 0) return;
-    const double Spg = res[0], Spp = res[1], Stg = res[2], amin_all = res[3];
-    const int projected = (Spg <= -eps * Spp && Spp >= eps) ? 1 : 0;    // Alg. 2 line 3
-    double amax = projected ? 1.0 : amin_all;
-    if (amax < 0.0) amax = 0.0;
-    const double gp = projected ? Spg : Stg;
-    C->branch = projected;
-    C->gp = gp;
-    C->amax = amax;
-    C->alpha0 = amax < 1.0 ? amax : 1.0;                        // R10
-    C->ls_batch = 0;
-    if (op_mode) return;
-    if (!(gp < 0.0)) {                                          // guard (R14)
-        if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }
-        else C->stall = ST_FALLBACK;
+    if (P.sharded) {                                         // sharded: local pack
+        if (threadIdx.x < 4) P.pk_loc[off_dir(P) + threadIdx.x] = res[threadIdx.x];
+        return;
     }
+    if (threadIdx.x != 0) return;
+    dir_decide(P, C, res, op_mode);
+}
+
+// Sharded: reduce the all-gathered Alg. 2 packs in rank order, then decide.
+__global__ void k_dir_decide(Prob P)
+{
+    Ctrl* C = P.ctrl;
+    if (halted(C) || threadIdx.x != 0) return;
+    double res[4] = {0.0, 0.0, 0.0, INFINITY};
+    for (int p = 0; p < P.nranks; ++p) {
+        const double* o = P.dir_all + (int64_t)p * 4;
+        res[0] += o[0]; res[1] += o[1]; res[2] += o[2];
+        res[3] = o[3] < res[3] ? o[3] : res[3];
+    }
+    dir_decide(P, C, res, 0);
 }
 
 // ------------------------------------------------------------------ a2: separable trial part
@@ -157,12 +182,26 @@ __global__ void __launch_bounds__(NT) k_sep(Prob P, int mode, const double* pvec
             }
         }
     }
+    if (!P.sharded || mode == SEP_OP) return;
+    // sharded: local reduction of the GS partials into the QS pack (after q)
+    __shared__ double buf[1024];
+    __shared__ double stash[NT];
+    if (!last_cta(P.tickets + T_SEP, gridDim.x)) return;
+    for (int i = threadIdx.x; i < KT * NSEP; i += NT) P.pk_loc[P.m + i] = 0.0;
+    __syncthreads();
+    reduce_parts(P.sep_part, gridDim.x, KT * NSEP, ntr * NSEP, [](int) { return 0; }, buf, 1024, stash,
+                 P.pk_loc + P.m);
 }
 
 // reduce the separable partials of GS CTAs into sm[KT * NSEP]
 __device__ void reduce_sep(const Prob& P, int ntr, double* buf, int bufn, double* stash, double* out)
 {
     if (P.GS == 0) return;
+    if (P.sharded) {                                         // rank order over the gathered packs
+        reduce_parts(P.qs_all + P.m, P.nranks, (int)qs_len(P), ntr * NSEP, [](int) { return 0; }, buf,
+                     bufn, stash, out);
+        return;
+    }
     reduce_parts(P.sep_part, P.GS, KT * NSEP, ntr * NSEP, [](int) { return 0; }, buf, bufn, stash, out);
 }
 
@@ -286,6 +325,11 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
         if (r1ok) qout[row + 1] = q1;
         return;
     }
+    if (P.sharded) {                                         // sharded: local q partial
+        if (r0ok) P.pk_loc[row] = q0;
+        if (r1ok) P.pk_loc[row + 1] = q1;
+        return;
+    }
     const int rsel = C->rsel;
     double* rcur = P.rbuf[rsel];
     double acc[KT];
@@ -339,19 +383,37 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
                                            double* f_out, int ntr_op)
 {
     Ctrl* C = P.ctrl;
-    if (mode == LS_NEXT && halted(C)) return;
+    if (mode != LS_OP && halted(C)) return;
     __shared__ double red[NT / 32];
     __shared__ double buf[1024];
     __shared__ double stash[NT];
     __shared__ double Ssum[KT];
     __shared__ double sepv[KT * NSEP];
-    const double* r = mode == LS_NEXT ? P.rbuf[C->rsel] : rv;
-    const double* q = mode == LS_NEXT ? P.q : qv;
+    const bool op = mode == LS_OP, setup = mode == LS_SH_SETUP, gather = mode == LS_SH_ITER || setup;
+    double* rcur = op ? nullptr : P.rbuf[C->rsel];
+    const double* r = op ? rv : rcur;
+    const double* q = op ? qv : P.q;
+    const int64_t qsl = qs_len(P);
+    const int ntr = setup ? 1 : KT;
     double acc[KT];
 #pragma unroll
     for (int t = 0; t < KT; ++t) acc[t] = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * NT) {
-        const double qi = q[i], ri = r[i];
+        double qi;
+        if (gather) {                                           // q = sum over ranks, rank order
+            qi = 0.0;
+            for (int p = 0; p < P.nranks; ++p) qi += P.qs_all[(int64_t)p * qsl + i];
+        } else {
+            qi = q[i];
+        }
+        if (setup) {                                            // r = M~x - b, ||r||^2
+            const double ri = P.b ? qi - P.b[i] : qi;
+            rcur[i] = ri;
+            acc[0] += ri * ri;
+            continue;
+        }
+        if (mode == LS_SH_ITER) P.q[i] = qi;
+        const double ri = r[i];
         double al = C->alpha0;
 #pragma unroll
         for (int t = 0; t < KT; ++t) {
@@ -360,15 +422,25 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
             acc[t] += v * v;
         }
     }
-    for (int t = 0; t < KT; ++t) {
+    for (int t = 0; t < ntr; ++t) {
         const double s = block_reduce<0>(acc[t], red);
         if (threadIdx.x == 0) P.lsp[(int64_t)blockIdx.x * KT + t] = s;
     }
     if (!last_cta(P.tickets + T_LS, gridDim.x)) return;
-    reduce_parts(P.lsp, gridDim.x, KT, KT, [](int) { return 0; }, buf, 1024, stash, Ssum);
-    reduce_sep(P, KT, buf, 1024, stash, sepv);
+    reduce_parts(P.lsp, gridDim.x, KT, ntr, [](int) { return 0; }, buf, 1024, stash, Ssum);
+    reduce_sep(P, ntr, buf, 1024, stash, sepv);
     if (threadIdx.x != 0) return;
     const double* sp = P.GS ? sepv : nullptr;
+    if (setup) {
+        double cc[MAXC], hv[MAXC], fb = 0.0;
+        const double f = trial_value(P, C, Ssum[0], sp, cc, hv, &fb);
+        const int ncons = P.n_eq + P.n_in;
+        C->f = f;
+        C->f_base = fb;
+        for (int k = 0; k < ncons; ++k) { C->ccoef[k] = cc[k]; C->hval[k] = hv[k]; }
+        C->nonfinite = isfinite(f) ? 0 : 1;
+        return;
+    }
     if (mode == LS_OP) {
         double cc[MAXC], hv[MAXC];
         for (int t = 0; t < ntr_op; ++t)
@@ -474,10 +546,29 @@ __global__ void __launch_bounds__(NT) k_kkt(Prob P)
     }
     if (!last_cta(P.tickets + T_KKT, gridDim.x)) return;
     reduce_parts(P.kkt_part, gridDim.x, 3, 3, [](int e) { return e < 2 ? 1 : 0; }, buf, 1024, stash, res);
+    if (P.sharded) {
+        if (threadIdx.x < 3) P.pk_loc[off_kkt(P) + threadIdx.x] = res[threadIdx.x];
+        return;
+    }
     if (threadIdx.x != 0) return;
     P.ctrl->pg = res[0];
     P.ctrl->gfree = res[1];
     P.ctrl->nfree = (long long)res[2];
+}
+
+__global__ void k_kkt_decide(Prob P)
+{
+    if (threadIdx.x != 0) return;
+    double pg = 0.0, gm = 0.0, cnt = 0.0;
+    for (int p = 0; p < P.nranks; ++p) {
+        const double* o = P.kkt_all + (int64_t)p * 4;
+        pg = o[0] > pg ? o[0] : pg;
+        gm = o[1] > gm ? o[1] : gm;
+        cnt += o[2];
+    }
+    P.ctrl->pg = pg;
+    P.ctrl->gfree = gm;
+    P.ctrl->nfree = (long long)cnt;
 }
 
 // ------------------------------------------------------------------ op / callback helpers
@@ -576,6 +667,8 @@ void launch_gram_recur(const Prob& P, cudaStream_t st, int op_mode)
     k_gram_recur<<<P.G1, NT, kGramSmem, st>>>(P, op_mode);
 }
 void launch_kkt(const Prob& P, cudaStream_t st) { k_kkt<<<P.G1, NT, 0, st>>>(P); }
+void launch_dir_decide(const Prob& P, cudaStream_t st) { k_dir_decide<<<1, 32, 0, st>>>(P); }
+void launch_kkt_decide(const Prob& P, cudaStream_t st) { k_kkt_decide<<<1, 32, 0, st>>>(P); }
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y)
 {
     if (nh > 0) k_ring_load<<<grid_for((int64_t)nh * P.n, NT), NT, 0, st>>>(P, nh, S, Y);

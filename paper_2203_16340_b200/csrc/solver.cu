@@ -110,6 +110,8 @@ struct lbfgsb_t {
     DevBuf gram_part, gram_grp, dir_part, kkt_part, tickets, sep_part;
     // m-sized (grown on demand)
     DevBuf r0, r1, q, qpart, lsp, fout;
+    // sharded packs
+    DevBuf pk_loc, qs_all, dir_all, gram_all, kkt_all;
     // host-buffer solve staging
     DevBuf Mh, bh, xh;
     Ctrl* ctrl = nullptr;           // device
@@ -118,6 +120,7 @@ struct lbfgsb_t {
     cudaGraphExec_t gexec = nullptr;
     Prob gkey{};
     int gchunk = 0;
+    cudaStream_t gstream = nullptr;
     // profiling
     std::vector<cudaEvent_t> ev;    // 4 per iteration in a chunk: fwd0 fwd1 bwd0 bwd1
     double prof_ms[2] = {0, 0};
@@ -127,6 +130,8 @@ struct lbfgsb_t {
     // sharding
     int rank = 0, nranks = 1;
     int64_t n_global = 0;
+    bool comm_owned = false;
+    bool sharded = false;
 #ifdef LBFGSB_WITH_NCCL
     ncclComm_t comm = nullptr;
 #endif
@@ -275,12 +280,13 @@ extern "C" void lbfgsb_destroy(lbfgsb_t* h)
     DevBuf* bufs[] = {&h->l, &h->u, &h->x, &h->g, &h->d, &h->pp, &h->pt, &h->S, &h->Y, &h->mask,
                       &h->xt, &h->gt, &h->gram_part, &h->gram_grp, &h->dir_part, &h->kkt_part,
                       &h->tickets, &h->sep_part, &h->r0, &h->r1, &h->q, &h->qpart, &h->lsp,
-                      &h->fout, &h->Mh, &h->bh, &h->xh};
+                      &h->fout, &h->Mh, &h->bh, &h->xh, &h->pk_loc, &h->qs_all, &h->dir_all,
+                      &h->gram_all, &h->kkt_all};
     for (DevBuf* b : bufs) b->release();
     if (h->ctrl) cudaFree(h->ctrl);
     if (h->hc) cudaFreeHost(h->hc);
 #ifdef LBFGSB_WITH_NCCL
-    if (h->comm) ncclCommDestroy(h->comm);
+    if (h->comm && h->comm_owned) ncclCommDestroy(h->comm);
 #endif
     if (h->own_stream) cudaStreamDestroy(h->st);
     delete h;
@@ -358,6 +364,8 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
     P.tickets = static_cast<unsigned*>(h->tickets.p);
     P.ctrl = h->ctrl;
     P.G1 = (int)clampi(cdiv(h->n, NT), 1, 2LL * sms);
+    P.nranks = h->nranks;
+    P.sharded = h->sharded ? 1 : 0;
     if (ob && ob->kind == 0) {
         const int64_t nv = ob->split ? 2 * ob->ncols : ob->ncols;
         if (nv != h->n)
@@ -372,6 +380,16 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
         TRY(h->lsp.ensure(sizeof(double) * (size_t)(P.RB > P.GLS ? P.RB : P.GLS) * KT));
         P.rbuf[0] = h->r0.d(); P.rbuf[1] = h->r1.d(); P.q = h->q.d(); P.qpart = h->qpart.d();
         P.lsp = h->lsp.d();
+        if (h->sharded) {
+            const int R = h->nranks;
+            TRY(h->pk_loc.ensure(sizeof(double) * (size_t)pk_len(P), true));
+            TRY(h->qs_all.ensure(sizeof(double) * (size_t)R * qs_len(P)));
+            TRY(h->dir_all.ensure(sizeof(double) * (size_t)R * 4));
+            TRY(h->gram_all.ensure(sizeof(double) * (size_t)R * GRAM_STRIDE));
+            TRY(h->kkt_all.ensure(sizeof(double) * (size_t)R * 4));
+            P.pk_loc = h->pk_loc.d(); P.qs_all = h->qs_all.d(); P.dir_all = h->dir_all.d();
+            P.gram_all = h->gram_all.d(); P.kkt_all = h->kkt_all.d();
+        }
     }
     return LBFGSB_OK;
 }
@@ -382,61 +400,188 @@ static void set_sep(Prob& P)
     P.GS = has_sep ? (int)clampi(cdiv(P.n, 2048), 1, 32) : 0;
 }
 
-static lbfgsb_err ctrl_to_dev(lbfgsb_t* h)
+static lbfgsb_err ctrl_to_dev(lbfgsb_t* h, cudaStream_t st)
 {
-    CK(cudaMemcpyAsync(h->ctrl, h->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->ctrl, h->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     return LBFGSB_OK;
 }
-static lbfgsb_err ctrl_to_host(lbfgsb_t* h)
+static lbfgsb_err ctrl_to_host(lbfgsb_t* h, cudaStream_t st)
 {
-    CK(cudaMemcpyAsync(h->hc, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
+    CK(cudaMemcpyAsync(h->hc, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     return LBFGSB_OK;
 }
 
-// ------------------------------------------------------------------ iteration sequence
-static void rec_event(lbfgsb_t* h, int idx)
+// ------------------------------------------------------------------ groups
+// A Group is the set of handles that take part in one solve: one handle (a
+// single-GPU solve, or this rank of an NCCL-sharded solve), or nranks
+// handles acting as logical ranks of a loopback-sharded solve on one device.
+// All launches of a group go to one stream.
+namespace {
+enum Section { SEC_QS = 0, SEC_DIR, SEC_GRAM, SEC_KKT };
+struct Group {
+    std::vector<lbfgsb_t*> hs;
+    std::vector<Prob> Ps;
+    cudaStream_t st = nullptr;
+    bool sharded = false;     // local packs + exchange + *_decide
+    bool loopback = false;    // exchange by device copies between the handles
+    lbfgsb_t* h0() const { return hs[0]; }
+};
+}  // namespace
+
+static lbfgsb_err ctrl_to_dev(Group& g)
 {
+    for (auto* h : g.hs) TRY(ctrl_to_dev(h, g.st));
+    return LBFGSB_OK;
+}
+static lbfgsb_err ctrl_to_host(Group& g)
+{
+    for (auto* h : g.hs) TRY(ctrl_to_host(h, g.st));
+    return LBFGSB_OK;
+}
+
+// All-gather one pack section across the ranks (rank order).
+static lbfgsb_err xchg(Group& g, Section sec)
+{
+    const Prob& P0 = g.Ps[0];
+    int64_t off = 0, cnt = 0;
+    switch (sec) {
+        case SEC_QS: off = 0; cnt = qs_len(P0); break;
+        case SEC_DIR: off = off_dir(P0); cnt = 4; break;
+        case SEC_GRAM: off = off_gram(P0); cnt = GRAM_STRIDE; break;
+        case SEC_KKT: off = off_kkt(P0); cnt = 4; break;
+    }
+    auto recv_of = [&](const Prob& P) {
+        return sec == SEC_QS ? P.qs_all : sec == SEC_DIR ? P.dir_all : sec == SEC_GRAM ? P.gram_all : P.kkt_all;
+    };
+    if (g.loopback) {
+        const int R = (int)g.hs.size();
+        for (int q = 0; q < R; ++q)
+            for (int p = 0; p < R; ++p)
+                CK(cudaMemcpyAsync(recv_of(g.Ps[q]) + (int64_t)p * cnt, g.Ps[p].pk_loc + off,
+                                   sizeof(double) * (size_t)cnt, cudaMemcpyDeviceToDevice, g.st));
+        return LBFGSB_OK;
+    }
+#ifdef LBFGSB_WITH_NCCL
+    ncclResult_t r = ncclAllGather(P0.pk_loc + off, recv_of(P0), (size_t)cnt, ncclDouble, g.h0()->comm, g.st);
+    if (r != ncclSuccess) return fail(LBFGSB_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+    return LBFGSB_OK;
+#else
+    return fail(LBFGSB_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
+#define FOR_RANKS for (size_t i_ = 0; i_ < g.hs.size(); ++i_)
+#define PR g.Ps[i_]
+
+static void rec_event(Group& g, int idx)
+{
+    lbfgsb_t* h = g.h0();
     if (!h->o.profile || idx < 0) return;
-    cudaEventRecordWithFlags(h->ev[idx], h->st, cudaEventRecordExternal);
+    cudaEventRecordWithFlags(h->ev[idx], g.st, cudaEventRecordExternal);
 }
 
-// One LSQ iteration (Alg. 1 lines 3-10): k_dir [k_sep] k_fwd k_bwd.
-static void launch_iteration(lbfgsb_t* h, const Prob& P, int ev_base)
+static int per_iteration_launches(const Group& g)
 {
-    cudaStream_t st = h->st;
-    launch_dir(P, st, 0);
-    launch_sep(P, st, SEP_ITER, nullptr);
-    rec_event(h, ev_base >= 0 ? ev_base + 0 : -1);
-    launch_fwd(P, st, FWD_ITER, nullptr, nullptr);
-    rec_event(h, ev_base >= 0 ? ev_base + 1 : -1);
-    rec_event(h, ev_base >= 0 ? ev_base + 2 : -1);
-    launch_bwd(P, st, BWD_ITER, nullptr, nullptr);
-    rec_event(h, ev_base >= 0 ? ev_base + 3 : -1);
-    h->launches += 3 + (P.GS > 0);
+    const int sep = g.Ps[0].GS > 0;
+    return g.sharded ? (int)g.hs.size() * (6 + sep) : 3 + sep;
+}
+
+// One LSQ iteration (Alg. 1 lines 3-10).  Single GPU: k_dir [k_sep] k_fwd
+// k_bwd with fused decisions.  Sharded: each decision point becomes local
+// pack -> all-gather -> *_decide.
+static lbfgsb_err launch_iteration(Group& g, int ev_base)
+{
+    cudaStream_t st = g.st;
+    if (!g.sharded) {
+        const Prob& P = g.Ps[0];
+        launch_dir(P, st, 0);
+        launch_sep(P, st, SEP_ITER, nullptr);
+        rec_event(g, ev_base >= 0 ? ev_base + 0 : -1);
+        launch_fwd(P, st, FWD_ITER, nullptr, nullptr);
+        rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);
+        rec_event(g, ev_base >= 0 ? ev_base + 2 : -1);
+        launch_bwd(P, st, BWD_ITER, nullptr, nullptr);
+        rec_event(g, ev_base >= 0 ? ev_base + 3 : -1);
+    } else {
+        FOR_RANKS launch_dir(PR, st, 0);
+        TRY(xchg(g, SEC_DIR));
+        FOR_RANKS launch_dir_decide(PR, st);
+        FOR_RANKS launch_sep(PR, st, SEP_ITER, nullptr);
+        rec_event(g, ev_base >= 0 ? ev_base + 0 : -1);
+        FOR_RANKS launch_fwd(PR, st, FWD_ITER, nullptr, nullptr);
+        rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);
+        TRY(xchg(g, SEC_QS));
+        FOR_RANKS launch_ls(PR, st, LS_SH_ITER, nullptr, nullptr, nullptr, 0);
+        rec_event(g, ev_base >= 0 ? ev_base + 2 : -1);
+        FOR_RANKS launch_bwd(PR, st, BWD_ITER, nullptr, nullptr);
+        rec_event(g, ev_base >= 0 ? ev_base + 3 : -1);
+        TRY(xchg(g, SEC_GRAM));
+        FOR_RANKS launch_gram_decide(PR, st, BWD_ITER);
+    }
+    g.h0()->launches += per_iteration_launches(g);
+    return LBFGSB_OK;
+}
+
+// f(x), r = M~x - b, and the constraint values at x (setup / AL start).
+static lbfgsb_err launch_fval(Group& g, bool clip)
+{
+    cudaStream_t st = g.st;
+    FOR_RANKS {
+        if (clip) launch_clip(PR, st);
+        launch_sep(PR, st, SEP_SETUP, PR.x);
+        launch_fwd(PR, st, FWD_SETUP, PR.x, nullptr);
+    }
+    if (g.sharded) {
+        TRY(xchg(g, SEC_QS));
+        FOR_RANKS launch_ls(PR, st, LS_SH_SETUP, nullptr, nullptr, nullptr, 0);
+    }
+    return LBFGSB_OK;
 }
 
 // Setup at x^0 (x = clip(x0); r = M~x - b; f; g; S^0; Gram;
 // convergence test; coefficients of the first direction).
-static void launch_setup(lbfgsb_t* h, const Prob& P)
+static lbfgsb_err launch_setup(Group& g)
 {
-    cudaStream_t st = h->st;
-    launch_clip(P, st);
-    launch_sep(P, st, SEP_SETUP, P.x);
-    launch_fwd(P, st, FWD_SETUP, P.x, nullptr);
-    launch_bwd(P, st, BWD_SETUP, nullptr, nullptr);
-    h->launches += 3 + (P.GS > 0);
+    TRY(launch_fval(g, true));
+    FOR_RANKS launch_bwd(PR, g.st, BWD_SETUP, nullptr, nullptr);
+    if (g.sharded) {
+        TRY(xchg(g, SEC_GRAM));
+        FOR_RANKS launch_gram_decide(PR, g.st, BWD_SETUP);
+    }
+    g.h0()->launches += 4;
+    return LBFGSB_OK;
 }
 
 // Final refresh (R13): r = M~x - b, f, g = grad f(x) and the KKT report.
-static void launch_refresh(lbfgsb_t* h, const Prob& P)
+static lbfgsb_err launch_refresh(Group& g)
 {
-    cudaStream_t st = h->st;
-    launch_sep(P, st, SEP_SETUP, P.x);
-    launch_fwd(P, st, FWD_SETUP, P.x, nullptr);
-    launch_bwd(P, st, BWD_REFRESH, nullptr, nullptr);
-    launch_kkt(P, st);
-    h->launches += 3 + (P.GS > 0);
+    TRY(launch_fval(g, false));
+    FOR_RANKS {
+        launch_bwd(PR, g.st, BWD_REFRESH, nullptr, nullptr);
+        launch_kkt(PR, g.st);
+    }
+    if (g.sharded) {
+        TRY(xchg(g, SEC_KKT));
+        FOR_RANKS launch_kkt_decide(PR, g.st);
+    }
+    g.h0()->launches += 4;
+    return LBFGSB_OK;
+}
+
+// Stall continuation: next Armijo batch, then the gradient pass.
+static lbfgsb_err launch_ls_cont(Group& g)
+{
+    FOR_RANKS launch_sep(PR, g.st, SEP_NEXT, nullptr);
+    if (g.sharded && g.Ps[0].GS > 0) TRY(xchg(g, SEC_QS));
+    FOR_RANKS launch_ls(PR, g.st, LS_NEXT, nullptr, nullptr, nullptr, 0);
+    FOR_RANKS launch_bwd(PR, g.st, BWD_ITER, nullptr, nullptr);
+    if (g.sharded) {
+        TRY(xchg(g, SEC_GRAM));
+        FOR_RANKS launch_gram_decide(PR, g.st, BWD_ITER);
+    }
+    g.h0()->launches += 3;
+    return LBFGSB_OK;
 }
 
 static lbfgsb_err ensure_events(lbfgsb_t* h)
@@ -450,30 +595,35 @@ static lbfgsb_err ensure_events(lbfgsb_t* h)
     return LBFGSB_OK;
 }
 
-static lbfgsb_err run_chunk(lbfgsb_t* h, const Prob& P)
+static lbfgsb_err run_chunk(Group& g)
 {
+    lbfgsb_t* h = g.h0();
     const int chunk = h->o.check_every;
-    const int per = 3 + (P.GS > 0);
-    if (h->o.use_graph) {
-        if (!h->gexec || std::memcmp(&h->gkey, &P, sizeof(Prob)) != 0 || h->gchunk != chunk) {
+    const bool graph = h->o.use_graph && !g.loopback;
+    if (graph) {
+        if (!h->gexec || std::memcmp(&h->gkey, &g.Ps[0], sizeof(Prob)) != 0 || h->gchunk != chunk ||
+            h->gstream != g.st) {
             if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
-            cudaGraph_t g = nullptr;
-            CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+            cudaGraph_t gr = nullptr;
+            CK(cudaStreamBeginCapture(g.st, cudaStreamCaptureModeThreadLocal));
             const int64_t l0 = h->launches;
-            for (int i = 0; i < chunk; ++i) launch_iteration(h, P, h->o.profile ? 4 * i : -1);
+            lbfgsb_err e0 = LBFGSB_OK;
+            for (int i = 0; i < chunk && e0 == LBFGSB_OK; ++i) e0 = launch_iteration(g, h->o.profile ? 4 * i : -1);
             h->launches = l0;
-            cudaError_t e = cudaStreamEndCapture(h->st, &g);
+            cudaError_t e = cudaStreamEndCapture(g.st, &gr);
+            if (e0 != LBFGSB_OK) { if (gr) cudaGraphDestroy(gr); return e0; }
             if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
-            e = cudaGraphInstantiate(&h->gexec, g, 0);
-            cudaGraphDestroy(g);
+            e = cudaGraphInstantiate(&h->gexec, gr, 0);
+            cudaGraphDestroy(gr);
             if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-            h->gkey = P;
+            h->gkey = g.Ps[0];
             h->gchunk = chunk;
+            h->gstream = g.st;
         }
-        CK(cudaGraphLaunch(h->gexec, h->st));
-        h->launches += (int64_t)per * chunk;
+        CK(cudaGraphLaunch(h->gexec, g.st));
+        h->launches += (int64_t)per_iteration_launches(g) * chunk;
     } else {
-        for (int i = 0; i < chunk; ++i) launch_iteration(h, P, h->o.profile ? 4 * i : -1);
+        for (int i = 0; i < chunk; ++i) TRY(launch_iteration(g, h->o.profile ? 4 * i : -1));
     }
     CK(cudaGetLastError());
     return LBFGSB_OK;
@@ -509,17 +659,23 @@ static void init_ctrl(lbfgsb_t* h, double tol)
     std::memcpy(c->rhs, rhs, sizeof rhs);
 }
 
-// Alg. 1 on an LSQ objective; x (device) in/out.  AL params already in h->hc.
-static lbfgsb_err solve_lsq(lbfgsb_t* h, const Prob& P, double* x_user, double tol, lbfgsb_result* res)
+// Alg. 1 on an LSQ objective for a group; xs[p] (device) in/out.  AL params
+// already in every handle's host mirror.
+static lbfgsb_err solve_group(Group& g, double* const* xs, double tol, lbfgsb_result* res)
 {
     auto t0 = std::chrono::steady_clock::now();
-    if (x_user != P.x) CK(cudaMemcpyAsync(P.x, x_user, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
-    init_ctrl(h, tol);
-    h->hc->n_fg = 1;
-    TRY(ctrl_to_dev(h));
-    launch_setup(h, P);
+    lbfgsb_t* h = g.h0();
+    FOR_RANKS {
+        lbfgsb_t* hh = g.hs[i_];
+        if (xs[i_] != PR.x)
+            CK(cudaMemcpyAsync(PR.x, xs[i_], sizeof(double) * hh->n, cudaMemcpyDeviceToDevice, g.st));
+        init_ctrl(hh, tol);
+        hh->hc->n_fg = 1;
+    }
+    TRY(ctrl_to_dev(g));
+    TRY(launch_setup(g));
     CK(cudaGetLastError());
-    TRY(ctrl_to_host(h));
+    TRY(ctrl_to_host(g));
     if (h->hc->nonfinite) return fail(LBFGSB_ERR_NONFINITE, "f(x0) is not finite");
     if (h->o.profile) TRY(ensure_events(h));
 
@@ -527,40 +683,41 @@ static lbfgsb_err solve_lsq(lbfgsb_t* h, const Prob& P, double* x_user, double t
     int64_t loops = 0;
     while (!h->hc->done) {
         const long long k0 = h->hc->k;
-        TRY(run_chunk(h, P));
-        TRY(ctrl_to_host(h));
+        TRY(run_chunk(g));
+        TRY(ctrl_to_host(g));
         collect_profile(h, h->hc->k - k0);
         if (++loops > guard) return fail(LBFGSB_ERR_CUDA, "solver loop did not terminate");
         // ---- stall handling (rare): finish the stalled iteration on the host's cue
         while (h->hc->stall && !h->hc->done) {
             const int s = h->hc->stall;
-            h->hc->stall = 0;
-            if (s == ST_FALLBACK) {
-                // R14: clear the history, d[S] = -g[S], redo Alg. 2 + the search
-                h->hc->fallback = 1;
-                h->hc->nh = 0;
-                h->hc->n_fallbacks += 1;
-                h->hc->coef[0] = -1.0;
-                TRY(ctrl_to_dev(h));
-                launch_iteration(h, P, -1);
-            } else {  // ST_LS_CONT: next batch of Armijo trials, then the gradient pass
-                TRY(ctrl_to_dev(h));
-                launch_sep(P, h->st, SEP_NEXT, nullptr);
-                launch_ls(P, h->st, LS_NEXT, nullptr, nullptr, nullptr, 0);
-                launch_bwd(P, h->st, BWD_ITER, nullptr, nullptr);
-                h->launches += 2 + (P.GS > 0);
+            for (auto* hh : g.hs) {
+                Ctrl* c = hh->hc;
+                c->stall = 0;
+                if (s == ST_FALLBACK) {
+                    // R14: clear the history, d[S] = -g[S], redo Alg. 2 + the search
+                    c->fallback = 1;
+                    c->nh = 0;
+                    c->n_fallbacks += 1;
+                    c->coef[0] = -1.0;
+                }
             }
+            TRY(ctrl_to_dev(g));
+            if (s == ST_FALLBACK) TRY(launch_iteration(g, -1));
+            else TRY(launch_ls_cont(g));
             CK(cudaGetLastError());
-            TRY(ctrl_to_host(h));
+            TRY(ctrl_to_host(g));
         }
     }
     const Ctrl fin = *h->hc;
     h->nact_total += fin.nact;
-    launch_refresh(h, P);
+    TRY(launch_refresh(g));
     CK(cudaGetLastError());
-    TRY(ctrl_to_host(h));
-    if (x_user != P.x) CK(cudaMemcpyAsync(x_user, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
-    CK(cudaStreamSynchronize(h->st));
+    TRY(ctrl_to_host(g));
+    FOR_RANKS {
+        if (xs[i_] != PR.x)
+            CK(cudaMemcpyAsync(xs[i_], PR.x, sizeof(double) * g.hs[i_]->n, cudaMemcpyDeviceToDevice, g.st));
+    }
+    CK(cudaStreamSynchronize(g.st));
     auto t1 = std::chrono::steady_clock::now();
     if (res) {
         std::memset(res, 0, sizeof *res);
@@ -579,9 +736,18 @@ static lbfgsb_err solve_lsq(lbfgsb_t* h, const Prob& P, double* x_user, double t
     return LBFGSB_OK;
 }
 
+static lbfgsb_err single_group(lbfgsb_t* h, const lbfgsb_objective* obj, Group& g)
+{
+    g.hs = {h};
+    g.Ps.resize(1);
+    TRY(make_prob(h, obj, g.Ps[0]));
+    g.st = h->st;
+    g.sharded = h->sharded;
+    g.loopback = false;
+    return LBFGSB_OK;
+}
+
 // ------------------------------------------------------------------ callback objective
-// Host-driven Alg. 1 for user objectives: working set, Gram, Alg. 3 and
-// Alg. 2 run in the device kernels; each Armijo trial calls the user's fg.
 static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_user, double tol,
                            lbfgsb_result* res)
 {
@@ -602,17 +768,17 @@ static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_us
     Ctrl* c = h->hc;
     c->f = f;
     c->n_fg = 1;
-    TRY(ctrl_to_dev(h));
+    TRY(ctrl_to_dev(h, st));
     for (;;) {
         launch_gram_recur(P, st, 0);
         launch_dir(P, st, 0);
         h->launches += 2;
         CK(cudaGetLastError());
-        TRY(ctrl_to_host(h));
+        TRY(ctrl_to_host(h, st));
         if (c->done) break;
         if (c->stall == ST_FALLBACK) {
             c->stall = 0; c->fallback = 1; c->nh = 0; c->n_fallbacks += 1;
-            TRY(ctrl_to_dev(h));
+            TRY(ctrl_to_dev(h, st));
             continue;
         }
         double a = c->alpha0, ft = 0.0;
@@ -630,7 +796,7 @@ static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_us
         if (!acc) {
             if (c->fallback) { c->done = 1; c->status = S_LS_FAIL; break; }
             c->fallback = 1; c->nh = 0; c->n_fallbacks += 1;
-            TRY(ctrl_to_dev(h));
+            TRY(ctrl_to_dev(h, st));
             continue;
         }
         const int head = (c->head + 1) % h->mh;
@@ -639,13 +805,13 @@ static lbfgsb_err solve_cb(lbfgsb_t* h, const lbfgsb_objective* ob, double* x_us
         c->head = head; c->slot = head;
         c->nh = c->nh + 1 < h->mh ? c->nh + 1 : h->mh;
         c->k += 1; c->fallback = 0; c->f = ft; c->alpha = a;
-        TRY(ctrl_to_dev(h));
+        TRY(ctrl_to_dev(h, st));
     }
     const Ctrl fin = *c;
     launch_kkt(P, st);
     h->launches += 1;
     CK(cudaGetLastError());
-    TRY(ctrl_to_host(h));
+    TRY(ctrl_to_host(h, st));
     CK(cudaMemcpyAsync(x_user, P.x, nb, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     auto t1 = std::chrono::steady_clock::now();
@@ -667,14 +833,59 @@ extern "C" lbfgsb_err lbfgsb_solve(lbfgsb_t* h, const lbfgsb_objective* obj, dou
 {
     if (!h || !obj || !x) return fail(LBFGSB_ERR_ARG, "NULL handle, objective or x");
     const double t = tol > 0 ? tol : h->o.tol;
-    if (obj->kind == 1) return solve_cb(h, obj, x, t, res);
-    Prob P;
-    TRY(make_prob(h, obj, P));
-    set_sep(P);
+    if (obj->kind == 1) {
+        if (h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "callback objectives are single-GPU");
+        return solve_cb(h, obj, x, t, res);
+    }
+    Group g;
+    TRY(single_group(h, obj, g));
+    set_sep(g.Ps[0]);
     h->hc->rho = 1.0;
     std::memset(h->hc->lam, 0, sizeof h->hc->lam);
     std::memset(h->hc->rhs, 0, sizeof h->hc->rhs);
-    return solve_lsq(h, P, x, t, res);
+    double* xs[1] = {x};
+    return solve_group(g, xs, t, res);
+}
+
+extern "C" lbfgsb_err lbfgsb_solve_loopback(lbfgsb_t* const* hs, const lbfgsb_objective* const* objs,
+                                            double* const* xs, int32_t nranks, double tol, lbfgsb_result* res)
+{
+    if (!hs || !objs || !xs || nranks < 1) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    Group g;
+    g.st = hs[0]->st;
+    g.sharded = nranks > 1;
+    g.loopback = nranks > 1;
+    g.Ps.resize(nranks);
+    int64_t nglob = 0;
+    for (int p = 0; p < nranks; ++p) {
+        if (!hs[p] || !objs[p] || !xs[p] || objs[p]->kind != 0) return fail(LBFGSB_ERR_ARG, "bad rank %d", p);
+        if (hs[p]->comm_owned) return fail(LBFGSB_ERR_ARG, "NCCL handle in loopback");
+        nglob += hs[p]->n;
+    }
+    for (int p = 0; p < nranks; ++p) {
+        hs[p]->nranks = nranks;
+        hs[p]->sharded = nranks > 1;
+        hs[p]->rank = p;
+        hs[p]->n_global = nglob;
+        g.hs.push_back(hs[p]);
+        lbfgsb_err e = make_prob(hs[p], objs[p], g.Ps[p]);
+        if (e == LBFGSB_OK && objs[p]->m != objs[0]->m) e = fail(LBFGSB_ERR_DIM, "ranks disagree on m");
+        if (e != LBFGSB_OK) {
+            for (int q = 0; q < nranks; ++q) { hs[q]->nranks = 1; hs[q]->sharded = false; }
+            return e;
+        }
+        set_sep(g.Ps[p]);
+        hs[p]->hc->rho = 1.0;
+        std::memset(hs[p]->hc->lam, 0, sizeof hs[p]->hc->lam);
+        std::memset(hs[p]->hc->rhs, 0, sizeof hs[p]->hc->rhs);
+    }
+    // separable-part geometry must agree across ranks (it is part of the pack layout)
+    const double t = tol > 0 ? tol : hs[0]->o.tol;
+    lbfgsb_err e = solve_group(g, xs, t, res);
+    for (int p = 0; p < nranks; ++p) {
+        hs[p]->nranks = 1; hs[p]->sharded = false; hs[p]->rank = 0; hs[p]->n_global = hs[p]->n;
+    }
+    return e;
 }
 
 extern "C" lbfgsb_err lbfgsb_solve_lsq_host(lbfgsb_t* h, const double* M_host, int64_t m, int64_t ncols,
@@ -716,8 +927,9 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
         return fail(LBFGSB_ERR_ARG, "constraint data missing");
     if (!(ao.rho0 > 0) || !(ao.rho_factor > 1) || ao.max_outer < 1)
         return fail(LBFGSB_ERR_ARG, "invalid al_opts");
-    Prob P;
-    TRY(make_prob(h, obj, P));
+    Group g;
+    TRY(single_group(h, obj, g));
+    Prob& P = g.Ps[0];
     P.n_eq = neq; P.n_in = nin;
     for (int k = 0; k < neq; ++k) P.Ecol[k] = cons->E + (int64_t)k * h->n;
     for (int k = 0; k < nin; ++k) P.Ecol[neq + k] = cons->G + (int64_t)k * h->n;
@@ -745,16 +957,14 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
         }
         return v;
     };
-    // constraint values at x^0 (one setup pass)
+    // constraint values at x^0 (one f-evaluation pass)
     set_al();
     CK(cudaMemcpyAsync(P.x, x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
     init_ctrl(h, tol);
-    TRY(ctrl_to_dev(h));
-    launch_clip(P, h->st);
-    launch_sep(P, h->st, SEP_SETUP, P.x);
-    launch_fwd(P, h->st, FWD_SETUP, P.x, nullptr);
+    TRY(ctrl_to_dev(g));
+    TRY(launch_fval(g, true));
     CK(cudaGetLastError());
-    TRY(ctrl_to_host(h));
+    TRY(ctrl_to_host(g));
     CK(cudaMemcpyAsync(x, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st));
     double hv[MAXC];
     std::memcpy(hv, h->hc->hval, sizeof hv);
@@ -762,10 +972,11 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
     al_result R{};
     R.status = AL_MAX_OUTER;
     lbfgsb_result ir{};
+    double* xs[1] = {x};
     for (int it = 0; it < ao.max_outer; ++it) {
         const double tin = 0.1 * vprev > tol ? 0.1 * vprev : tol;      // R22
         set_al();
-        TRY(solve_lsq(h, P, x, tin, &ir));                            // Alg. 4 line 5
+        TRY(solve_group(g, xs, tin, &ir));                            // Alg. 4 line 5
         R.inner_iters_total += ir.iters;
         R.outer_iters = it + 1;
         R.pg_inf = ir.pg_inf;
@@ -797,16 +1008,52 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
 }
 
 // ------------------------------------------------------------------ sharded (NCCL)
+extern "C" lbfgsb_err lbfgsb_nccl_unique_id(void* out)
+{
+    if (!out) return fail(LBFGSB_ERR_ARG, "out is NULL");
+#ifdef LBFGSB_WITH_NCCL
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(LBFGSB_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof id);
+    return LBFGSB_OK;
+#else
+    return fail(LBFGSB_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
 extern "C" lbfgsb_err lbfgsb_create_sharded(int64_t n_local, int64_t n_global, int32_t m_hist,
                                             const double* lower_local, const double* upper_local,
                                             const lbfgsb_opts* opts, void* cuda_stream,
                                             const void* nccl_unique_id, int32_t rank, int32_t nranks,
                                             lbfgsb_t** out)
 {
-    (void)n_local; (void)n_global; (void)m_hist; (void)lower_local; (void)upper_local; (void)opts;
-    (void)cuda_stream; (void)nccl_unique_id; (void)rank; (void)nranks;
-    if (out) *out = nullptr;
-    return fail(LBFGSB_ERR_UNSUPPORTED, "sharded handles are not available in this build yet");
+    if (!out || !nccl_unique_id) return fail(LBFGSB_ERR_ARG, "NULL out or unique id");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LBFGSB_ERR_ARG, "bad rank/nranks");
+    if (n_global < n_local) return fail(LBFGSB_ERR_DIM, "n_global < n_local");
+#ifdef LBFGSB_WITH_NCCL
+    lbfgsb_t* h = nullptr;
+    TRY(create_common(n_local, m_hist, lower_local, upper_local, opts, cuda_stream, &h));
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        lbfgsb_destroy(h);
+        return fail(LBFGSB_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    h->comm_owned = true;
+    h->sharded = true;          // sharded protocol even for a 1-rank communicator
+    h->nranks = nranks;
+    h->rank = rank;
+    h->n_global = n_global;
+    *out = h;
+    return LBFGSB_OK;
+#else
+    (void)n_local; (void)m_hist; (void)lower_local; (void)upper_local; (void)opts; (void)cuda_stream;
+    return fail(LBFGSB_ERR_UNSUPPORTED, "built without NCCL");
+#endif
 }
 
 // ------------------------------------------------------------------ ops
@@ -879,11 +1126,11 @@ extern "C" lbfgsb_err lbfgsb_op_direction(lbfgsb_t* h, const double* x, const do
     init_ctrl(h, h->o.tol);
     h->hc->nh = nh;
     h->hc->head = nh > 0 ? nh - 1 : h->mh - 1;
-    TRY(ctrl_to_dev(h));
+    TRY(ctrl_to_dev(h, h->st));
     launch_gram_recur(P, st, 1);
     launch_dir(P, st, 1);
     CK(cudaGetLastError());
-    TRY(ctrl_to_host(h));
+    TRY(ctrl_to_host(h, h->st));
     const int br = h->hc->branch;
     if (free_out) CK(cudaMemcpyAsync(free_out, P.mask, (size_t)h->n, cudaMemcpyDeviceToDevice, st));
     if (d_out) CK(cudaMemcpyAsync(d_out, P.d, nb, cudaMemcpyDeviceToDevice, st));
@@ -909,7 +1156,7 @@ extern "C" lbfgsb_err lbfgsb_op_trials(lbfgsb_t* h, const lbfgsb_objective* obj,
     init_ctrl(h, h->o.tol);
     h->hc->alpha0 = alpha0;
     h->hc->rho = 1.0;
-    TRY(ctrl_to_dev(h));
+    TRY(ctrl_to_dev(h, h->st));
     launch_sep(P, h->st, SEP_OP, p);
     launch_ls(P, h->st, LS_OP, r, q, h->fout.d(), ntrials);
     CK(cudaGetLastError());

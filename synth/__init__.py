@@ -133,6 +133,19 @@ def svm_dual_linear(N: int, d: int, seed: int, C: float = 1.0, sep: float = 2.0)
                    e=np.zeros(1), meta=dict(N=N, d=d, seed=seed, C=C))
 
 
+def weak_shard(m: int, ncols_local: int, rank: int, seed: int):
+    """Rank `rank`'s column block of the weak-scaled NNLS workload: the global
+    A = [A_0 | ... | A_{N-1}] with A_r ~ N(0,1)/sqrt(m) drawn from
+    default_rng([seed, r]) and b ~ N(0,1) from default_rng(seed) (replicated),
+    so the global problem is a C2-distributed NNLS with n = N * ncols_local."""
+    b = np.random.default_rng(seed).standard_normal(m)
+    rng = np.random.default_rng([seed, rank])
+    A = rng.standard_normal((ncols_local, m)).T / np.sqrt(m)
+    return Problem("nnls", f"weak_shard_r{rank}", A, b=b, lower=np.zeros(ncols_local),
+                         meta=dict(m=m, ncols_local=ncols_local, rank=rank, seed=seed))
+
+
+
 # Named configurations of BASELINE.json "configs" (SURVEY.md 8(d) table)
 CONFIGS = {
     "C1": lambda seed=1: nnls_gaussian(200, 100, seed, "C1_nnls_200x100"),

@@ -1,0 +1,93 @@
+"""CPU (-m "not gpu") multi-process tests of the N > 1 host path with the
+gloo backend, world_size 2: column partitioning, the ncclUniqueId broadcast,
+max-over-ranks timing, and the decomposition the sharded library uses
+(rank-local partials of q = M~p, of the Alg. 2 sums and of the Gram pack,
+all-gathered and reduced in rank order) checked against the unsharded
+quantities computed by the oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2203_16340_b200.sharded import column_range
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("ncols,P", [(10, 2), (10000, 8), (7, 3), (1, 1), (200000, 8), (5, 5)])
+def test_column_range_partition(ncols, P):
+    rs = [column_range(ncols, P, r) for r in range(P)]
+    assert rs[0][0] == 0 and rs[-1][1] == ncols
+    for (a0, a1), (b0, b1) in zip(rs, rs[1:]):
+        assert a1 == b0
+    sizes = [b - a for a, b in rs]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2203_16340_b200 import sharded
+    import oracle
+
+    # 1) the unique-id broadcast used by make_sharded_solver
+    nid = bytes(range(128)) if rank == 0 else None
+    got = sharded.broadcast_bytes(nid, src=0)
+    # 2) max-over-ranks timing
+    mx = sharded.max_over_ranks(1.5 + rank)
+    # 3) the sharded decomposition on a small NNLS instance
+    m, n = 60, 37
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((m, n)) / np.sqrt(m)
+    x = np.abs(rng.standard_normal(n)) * (rng.random(n) < 0.6)
+    g = rng.standard_normal(n)
+    d = -g * (rng.random(n) < 0.7)
+    l = np.zeros(n)
+    c0, c1 = sharded.column_range(n, world, rank)
+    # rank-local q partial and Alg. 2 sums (projected candidate)
+    q_loc = oracle.matvec(A[:, c0:c1], d[c0:c1])
+    pp = np.maximum(x[c0:c1] + d[c0:c1], 0.0) - x[c0:c1]
+    dir_loc = np.array([pp @ g[c0:c1], pp @ pp])
+    q_all = [torch.zeros(m, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(q_all, torch.from_numpy(q_loc))
+    dir_all = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(dir_all, torch.from_numpy(dir_loc))
+    q = np.zeros(m)
+    for t in q_all:                      # rank order
+        q = q + t.numpy()
+    sums = np.zeros(2)
+    for t in dir_all:
+        sums = sums + t.numpy()
+    q_ref = oracle.matvec(A, d)
+    pp_ref = np.maximum(x + d, 0.0) - x
+    res = dict(got=got, mx=mx, q_err=float(np.max(np.abs(q - q_ref) / (np.abs(A) @ np.abs(d) + 1e-300))),
+               s_err=float(abs(sums[0] - pp_ref @ g) + abs(sums[1] - pp_ref @ pp_ref)),
+               q_bits=q.tobytes())
+    out[rank] = res
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_host_logic():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    for r in range(world):
+        assert out[r]["got"] == bytes(range(128))
+        assert out[r]["mx"] == 2.5
+        assert out[r]["q_err"] <= 1e-12
+        assert out[r]["s_err"] <= 1e-12
+    # every rank reduced the same gathered partials in the same order: identical bits
+    assert out[0]["q_bits"] == out[1]["q_bits"]
