@@ -360,6 +360,144 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
     gram_tail(P, C, E, gacc, gmax, cnt, red, rs, (int)(mpad < 4096 ? mpad : 4096), stash, Gs);
 }
 
+// ---------------------------------------------------------------- k_bwd_w (short columns)
+// m < 2048 rows (C1, C4): a whole column is only a few KB, so a CTA-wide
+// reduction per column group would dominate.  Each WARP owns WCOL columns
+// at a time (lanes stride the rows, r' from shared memory), reduces with
+// shuffles only, and its lanes run the epilogue; the CTA syncs once per
+// round of 8 warp-groups to accumulate the Gram tile.
+constexpr int WCOL = 4;
+constexpr int WTILE = (NT / 32) * WCOL * 2;     // tile rows per round (split: 2 vars per column)
+
+template <int NC>
+__device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int64_t ld, int64_t m,
+                                              const double* rs, double* acc)
+{
+    const int lane = threadIdx.x & 31;
+    int64_t i = 2 * lane;
+    for (; i + 64 + 1 < m; i += 128) {
+        double2 a0[NC], a1[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            a0[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i));
+            a1[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + 64));
+        }
+        const double2 r0 = *reinterpret_cast<const double2*>(rs + i);
+        const double2 r1 = *reinterpret_cast<const double2*>(rs + i + 64);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            acc[c] = fma(a0[c].x, r0.x, acc[c]);
+            acc[c] = fma(a0[c].y, r0.y, acc[c]);
+            acc[c] = fma(a1[c].x, r1.x, acc[c]);
+            acc[c] = fma(a1[c].y, r1.y, acc[c]);
+        }
+    }
+    for (; i < m; i += 64) {
+        if (i + 1 < m) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const double2 a = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i));
+                acc[c] = fma(a.x, rs[i], acc[c]);
+                acc[c] = fma(a.y, rs[i + 1], acc[c]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(M0 + c * ld + i), rs[i], acc[c]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double* rvec, double* gout, int mpad)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    extern __shared__ __align__(16) double smw[];
+    double* rs = smw;                               // r' [mpad]
+    double* tile = smw + mpad;                      // [WTILE][MAXB]
+    double* mk = tile + WTILE * MAXB;               // [WTILE]
+    __shared__ double red[NT / 32 * BWD_NB];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
+    const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
+    const int64_t i0 = (int64_t)cta * m / G, i1 = (int64_t)(cta + 1) * m / G;
+    const bool iter = mode == BWD_ITER;
+    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
+    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
+    double* rnext = P.rbuf[rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += NT) {
+        double r = rcur[i];
+        if (iter) {
+            r = fma(alpha, P.q[i], r);                          // carried residual (R13)
+            if (i >= i0 && i < i1) rnext[i] = r;
+        }
+        rs[i] = r;
+    }
+    __syncthreads();
+    const bool epi = mode != BWD_PLAIN;
+    EpiCtx E;
+    if (epi) epi_init(P, C, mode, E);
+    const int nb = epi ? E.nb : 1;
+    const int ne = nb * (nb + 1) / 2;
+    GramEnt ent;
+    ent.init(nb, ne, ne + (epi && P.screen_full ? E.nh : 0), epi ? E.nh : 0);
+    double gacc[3] = {0.0, 0.0, 0.0};
+    double gmax = 0.0, cnt = 0.0;
+    const int nvg = P.split ? 2 : 1;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = NT / 32;
+    const int64_t ncl = j1 - j0;
+    const int64_t ngroups = (ncl + WCOL - 1) / WCOL;
+    const int64_t rounds = (ngroups + nw - 1) / nw;
+    const int rows_per_warp = WCOL * nvg;
+    for (int64_t rd = 0; rd < rounds; ++rd) {
+        const int64_t grp = rd * nw + w;
+        const int64_t jg = j0 + grp * WCOL;
+        const int nc = jg < j1 ? (int)(j1 - jg < WCOL ? j1 - jg : WCOL) : 0;
+        double acc[WCOL] = {0.0, 0.0, 0.0, 0.0};
+        const double* M0 = P.M + jg * ld;
+        switch (nc) {
+            case 4: warp_col_dots<4>(M0, ld, m, rs, acc); break;
+            case 3: warp_col_dots<3>(M0, ld, m, rs, acc); break;
+            case 2: warp_col_dots<2>(M0, ld, m, rs, acc); break;
+            case 1: warp_col_dots<1>(M0, ld, m, rs, acc); break;
+            default: break;
+        }
+#pragma unroll
+        for (int c = 0; c < WCOL; ++c)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        // all lanes now hold the column dots (xor butterfly: identical in every lane)
+        const int trow0 = w * rows_per_warp;
+        if (lane < rows_per_warp) {
+            const int t = trow0 + lane;
+            if (lane < nc * nvg) {
+                const int jj = lane % nc, vv = lane / nc;
+                double dot = acc[0];
+                if (jj == 1) dot = acc[1];
+                if (jj == 2) dot = acc[2];
+                if (jj == 3) dot = acc[3];
+                const int64_t j = jg + jj;
+                double dval = vv ? -dot : dot;
+                if (P.colscale) dval = P.colscale[j] * dot;
+                if (!epi) gout[j + vv * ncols] = dval;
+                else epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)t * nb, mk + t, gmax, cnt);
+            } else if (epi) {
+                for (int b = 0; b < nb; ++b) tile[(int64_t)t * nb + b] = 0.0;
+                mk[t] = 0.0;
+            }
+        }
+        if (epi && E.gram) {
+            __syncthreads();
+            ent.accumulate(tile, mk, nw * rows_per_warp, nb, gacc);
+            __syncthreads();
+        }
+    }
+    if (!epi || !E.gram) return;
+    gram_tail(P, C, E, gacc, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
+}
+
 // ---------------------------------------------------------------- k_bwd (generic)
 template <bool VEC>
 __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* rvec, double* gout)
@@ -433,7 +571,9 @@ __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* r
 }
 
 // ---------------------------------------------------------------- launch
-static int g_bwd_occ = 0;
+static int g_bwd_occ = 0, g_bwdw_occ = 0;
+constexpr int BWD_W_MAXM = 2048;
+constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + 64);
 static bool g_bwd_init = false;
 
 static void bwd_init()
@@ -443,6 +583,10 @@ static void bwd_init()
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd<true>, NT, 0);
     g_bwd_occ = o > 0 ? o : 1;
     cudaFuncSetAttribute(k_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_MAX);
+    cudaFuncSetAttribute(k_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_W_SMEM_MAX);
+    o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_w, NT, BWD_W_SMEM_MAX);
+    g_bwdw_occ = o > 0 ? o : 1;
     cudaGetLastError();
     g_bwd_init = true;
 }
@@ -478,6 +622,14 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
     const int sms = sm_count();
     const int Gs_ = (int)(P.ncols < sms ? P.ncols : sms);
     const size_t smem = aligned ? bwd_s_smem(P, Gs_) : 0;
+    if (aligned && P.m < BWD_W_MAXM) {
+        const int G = (int)(P.ncols < (int64_t)sms * g_bwdw_occ ? P.ncols : (int64_t)sms * g_bwdw_occ);
+        int mpad = (int)(P.m + (P.m & 1));
+        if (mpad < 4096 / 2) mpad = 4096 / 2;     // tail reduce buffer reuses r' space
+        const size_t sm = sizeof(double) * ((size_t)mpad + WTILE * (MAXB + 1));
+        k_bwd_w<<<G, NT, sm, st>>>(P, mode, rvec, gout, mpad);
+        return;
+    }
     if (smem && P.m >= 2048) {
         const int64_t cmax = (P.ncols + Gs_ - 1) / Gs_;
         const int64_t mpad = (int64_t)(smem / sizeof(double)) - cmax - 1;

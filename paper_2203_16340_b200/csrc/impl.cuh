@@ -41,6 +41,7 @@ constexpr int FWD_SUB = 1024;                      // columns per compaction sub
 constexpr int BWD_NB = 8;                          // columns per register group in k_bwd
 constexpr int GRP = 32;                            // k_bwd CTAs per level-1 Gram group
 constexpr int NTICKETS = 8192;
+constexpr int SEP_MAXG = 64;                       // max k_sep CTAs
 
 enum Stall : int { ST_NONE = 0, ST_FALLBACK = 1, ST_LS_CONT = 2 };
 enum Status : int { S_CONVERGED = 0, S_MAX_ITERS = 1, S_LS_FAIL = 2 };

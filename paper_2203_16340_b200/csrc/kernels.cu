@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NT) k_sep(Prob P, int mode, const double* pvec
 {
     const Ctrl* C = P.ctrl;
     if ((mode == SEP_ITER || mode == SEP_NEXT) && halted(C)) return;
-    __shared__ double red[NT / 32];
+    __shared__ double wsum[NT / 32][4 * NSEP];
     double al[KT];
     const int ntr = mode == SEP_SETUP ? 1 : KT;
     al[0] = mode == SEP_SETUP ? 0.0 : C->alpha0;
@@ -170,27 +170,35 @@ __global__ void __launch_bounds__(NT) k_sep(Prob P, int mode, const double* pvec
                     if (k < ncons) a[tt][2 + k] += ev[k] * xt;
             }
         }
+        // multi-value block reduction: warp shuffles, one smem stage, one barrier
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-        for (int tt = 0; tt < 4; ++tt) {
-            if (t0 + tt >= ntr) break;
+        for (int tt = 0; tt < 4; ++tt)
 #pragma unroll
             for (int s = 0; s < NSEP; ++s) {
-                if (s >= 2 + ncons) break;
-                const double v = block_reduce<0>(a[tt][s], red);
-                if (threadIdx.x == 0)
-                    P.sep_part[((int64_t)blockIdx.x * KT + t0 + tt) * NSEP + s] = v;
+                const double v = warp_red<0>(a[tt][s]);
+                if (lane == 0) wsum[w][tt * NSEP + s] = v;
+            }
+        __syncthreads();
+        if (threadIdx.x < 4 * NSEP) {
+            const int tt = threadIdx.x / NSEP, s = threadIdx.x % NSEP;
+            if (t0 + tt < ntr && s < 2 + ncons) {
+                double v = wsum[0][threadIdx.x];
+                for (int k = 1; k < NT / 32; ++k) v += wsum[k][threadIdx.x];
+                P.sep_part[((int64_t)blockIdx.x * KT + t0 + tt) * NSEP + s] = v;
             }
         }
+        __syncthreads();
     }
-    if (!P.sharded || mode == SEP_OP) return;
-    // sharded: local reduction of the GS partials into the QS pack (after q)
-    __shared__ double buf[1024];
+    // tail: the last CTA reduces the GS partials into one pack (single GPU:
+    // sep_red after the partials; sharded: this rank's QS pack after q)
+    __shared__ double buf[4096];
     __shared__ double stash[NT];
     if (!last_cta(P.tickets + T_SEP, gridDim.x)) return;
-    for (int i = threadIdx.x; i < KT * NSEP; i += NT) P.pk_loc[P.m + i] = 0.0;
+    double* dst = P.sharded && mode != SEP_OP ? P.pk_loc + P.m : P.sep_part + (int64_t)SEP_MAXG * KT * NSEP;
+    for (int i = threadIdx.x; i < KT * NSEP; i += NT) dst[i] = 0.0;
     __syncthreads();
-    reduce_parts(P.sep_part, gridDim.x, KT * NSEP, ntr * NSEP, [](int) { return 0; }, buf, 1024, stash,
-                 P.pk_loc + P.m);
+    reduce_parts(P.sep_part, gridDim.x, KT * NSEP, ntr * NSEP, [](int) { return 0; }, buf, 4096, stash, dst);
 }
 
 // reduce the separable partials of GS CTAs into sm[KT * NSEP]
@@ -202,7 +210,9 @@ __device__ void reduce_sep(const Prob& P, int ntr, double* buf, int bufn, double
                      bufn, stash, out);
         return;
     }
-    reduce_parts(P.sep_part, P.GS, KT * NSEP, ntr * NSEP, [](int) { return 0; }, buf, bufn, stash, out);
+    const double* red = P.sep_part + (int64_t)SEP_MAXG * KT * NSEP;   // k_sep's reduced pack
+    for (int i = threadIdx.x; i < ntr * NSEP; i += blockDim.x) out[i] = __ldcg(red + i);
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------ a1: forward GEMV + line search

@@ -198,7 +198,7 @@ static lbfgsb_err alloc_n(lbfgsb_t* h)
     TRY(h->gram_grp.ensure(sizeof(double) * cdiv(parts, GRP) * GRAM_STRIDE));
     TRY(h->dir_part.ensure(sizeof(double) * 2LL * sms * 4));
     TRY(h->kkt_part.ensure(sizeof(double) * 2LL * sms * 3));
-    TRY(h->sep_part.ensure(sizeof(double) * 32 * KT * NSEP));
+    TRY(h->sep_part.ensure(sizeof(double) * (SEP_MAXG + 1) * KT * NSEP));
     TRY(h->tickets.ensure(sizeof(unsigned) * (NTICKETS + 8192), true));
     TRY(h->fout.ensure(sizeof(double) * KT));
     CK(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
@@ -397,7 +397,7 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
 static void set_sep(Prob& P)
 {
     const bool has_sep = P.c || P.delta != 0.0 || (P.n_eq + P.n_in) > 0;
-    P.GS = has_sep ? (int)clampi(cdiv(P.n, 2048), 1, 32) : 0;
+    P.GS = has_sep ? (int)clampi(cdiv(P.n, 1024), 1, SEP_MAXG) : 0;
 }
 
 static lbfgsb_err ctrl_to_dev(lbfgsb_t* h, cudaStream_t st)

@@ -152,6 +152,33 @@ int main()
         cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
         rep("bulk 4x16KB 2CTA/SM tpb=256", timeit([&] { bulk_sum<S, B><<<sms * 2, 256, S * B>>>(a, n, out); }, 10));
     }
+    {
+        constexpr int S = 3, B = 16384;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 3x16KB 1CTA/SM tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+        rep("bulk 3x16KB 1CTA/SM tpb=256", timeit([&] { bulk_sum<S, B><<<sms, 256, S * B>>>(a, n, out); }, 10));
+    }
+    {
+        constexpr int S = 4, B = 12288;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 4x12KB 1CTA/SM tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+    }
+    {
+        constexpr int S = 2, B = 24576;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 2x24KB 1CTA/SM tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+    }
+    {
+        constexpr int S = 8, B = 8192;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 8x8KB 1CTA/SM tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+        rep("bulk 8x8KB 1CTA/SM tpb=256", timeit([&] { bulk_sum<S, B><<<sms, 256, S * B>>>(a, n, out); }, 10));
+    }
+    {
+        constexpr int S = 6, B = 8192;
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+        rep("bulk 6x8KB 1CTA/SM tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+    }
     // copy reference (cudaMemcpy D2D, read+write counted)
     double* b; cudaMalloc(&b, bytes / 2);
     float ms = timeit([&] { cudaMemcpyAsync(b, a, bytes / 2, cudaMemcpyDeviceToDevice); }, 10);
