@@ -16,6 +16,7 @@
 // accumulate the masked Gram of the NEXT basis {s_i, y_i, g'}, and end in a
 // deterministic 2-level last-CTA tail: Gram reduce -> convergence test
 // (R15) -> vector-free Alg. 3 -> ctrl->coef.
+#include <cstdlib>
 #include "common.cuh"
 
 namespace lb {
@@ -498,6 +499,253 @@ __global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double*
     gram_tail(P, C, E, gacc, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
 }
 
+// ---------------------------------------------------------------- k_bwd_c (TMA, CTA pairs)
+// The B200 read ceiling for a per-CTA contiguous stream is reached with bulk
+// (TMA) copies and >= 128 KB in flight per SM (profiles/r01_bw_probe.txt:
+// 7.1 TB/s vs 6.0 TB/s for LDG from one 512-thread CTA).  With r' resident
+// in shared memory there is no room for that at m = 20000 (160 KB), so the
+// ROWS are split across a cluster of two CTAs: CTA h of cluster c keeps r'
+// for its half of the rows (80 KB) and streams its half of every column of
+// the cluster's column range through a 4 x 32 KB cp.async.bulk ring
+// (mbarrier full / empty pipeline, one producer warp, 16 consumer warps).
+// Half-row dots are combined over distributed shared memory (rank 0 + rank
+// 1, fixed order), then each CTA runs the epilogue for half of the columns.
+constexpr int TC_STAGES = 4;
+constexpr int TC_CHUNK = 4096;                                // rows per stage (one column segment)
+constexpr int TC_STAGE_BYTES = TC_CHUNK * 8;                  // 32 KB, one cp.async.bulk
+constexpr int TC_CONS = 512;                                  // consumer threads (16 warps)
+constexpr int TC_THREADS = TC_CONS;                           // all threads consume; thread 0 issues
+constexpr int TC_SMEM_MAX = 212 * 1024;   // + ~12.3 KB static <= 227 KB
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity)
+{
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+                 ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ double ld_dsmem(const double* local_ptr, unsigned rank)
+{
+    unsigned a = smem_u32(local_ptr), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+    return v;
+}
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(TC_CONS) : "memory"); }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+k_bwd_c(Prob P, int mode, const double* rvec, double* gout, int hmax, int cmax)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;      // uniform across the cluster (same ctrl)
+    extern __shared__ __align__(1024) unsigned char smc[];
+    double* stage = reinterpret_cast<double*>(smc);                                    // [S][TC_CHUNK]
+    double* rs = reinterpret_cast<double*>(smc + (size_t)TC_STAGES * TC_STAGE_BYTES);   // [hmax]
+    double* dh = rs + hmax;                                                            // [cmax] half dots
+    double* dfull = dh + cmax;                                                         // [cmax] full dots
+    __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES];
+    __shared__ double wsh[2][TC_THREADS / 32][BWD_NB];
+    __shared__ double red[TC_THREADS / 32 * BWD_NB];
+    __shared__ double stash[TC_THREADS];
+    __shared__ double Gs[MAXE + MAXH + 2];
+
+    const unsigned h = cluster_rank();
+    const int ncl = gridDim.x / 2, cl = blockIdx.x / 2;
+    const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
+    const int64_t j0 = (int64_t)cl * ncols / ncl, j1 = (int64_t)(cl + 1) * ncols / ncl;
+    const int64_t mid = ((m / 2) + 1) & ~(int64_t)1;                 // even split row
+    const int64_t rlo = h ? mid : 0, rhi = h ? m : mid, H = rhi - rlo;
+    const bool iter = mode == BWD_ITER;
+    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
+    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
+    double* rnext = P.rbuf[rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TC_CONS / 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t ngroups = (j1 - j0 + BWD_NB - 1) / BWD_NB;
+    // uniform row chunks of <= TC_CHUNK rows (even) per stage
+    const int64_t nchunks = (H + TC_CHUNK - 1) / TC_CHUNK;
+    const int64_t chunk = (((H + nchunks - 1) / nchunks) + 1) & ~(int64_t)1;
+    {
+        // r' for this CTA's rows; rnext slice: rows [rlo + cl*H/ncl, rlo + (cl+1)*H/ncl)
+        const int64_t w0 = rlo + (int64_t)cl * H / ncl, w1 = rlo + (int64_t)(cl + 1) * H / ncl;
+        for (int64_t i = rlo + tid; i < rhi; i += TC_THREADS) {
+            double r = rcur[i];
+            if (iter) {
+                r = fma(alpha, P.q[i], r);                      // carried residual (R13)
+                if (i >= w0 && i < w1) rnext[i] = r;
+            }
+            rs[i - rlo] = r;
+        }
+    }
+    // stage it <-> (group g, column c, row chunk ch), issued in this order by thread 0
+    int64_t total = 0;
+    for (int64_t g = 0; g < ngroups; ++g) {
+        const int64_t jg = j0 + g * BWD_NB;
+        total += (j1 - jg < BWD_NB ? j1 - jg : BWD_NB) * nchunks;
+    }
+    auto issue = [&](int64_t it) {
+        const int64_t per_col = nchunks;
+        const int64_t col = it / per_col, ch = it % per_col;      // column index within the range
+        const int s = (int)(it % TC_STAGES);
+        const int64_t r0 = rlo + ch * chunk;
+        const int rows = (int)(rhi - r0 < chunk ? rhi - r0 : chunk);
+        const unsigned bytes = (unsigned)rows * 8u;
+        mbar_arrive_tx(&full[s], bytes);
+        bulk_g2s(stage + (size_t)s * TC_CHUNK, P.M + (j0 + col) * ld + r0, bytes, &full[s]);
+    };
+    if (tid == 0)
+        for (int64_t it = 0; it < TC_STAGES && it < total; ++it) issue(it);
+    __syncthreads();                                            // r' complete
+    double acc[BWD_NB];
+#pragma unroll
+    for (int k = 0; k < BWD_NB; ++k) acc[k] = 0.0;
+    int64_t it = 0;
+    for (int64_t g = 0; g < ngroups; ++g) {
+        const int64_t jg = j0 + g * BWD_NB;
+        const int nc = (int)(j1 - jg < BWD_NB ? j1 - jg : BWD_NB);
+        for (int c = 0; c < nc; ++c) {
+            double sacc = 0.0;
+            for (int64_t ch = 0; ch < nchunks; ++ch, ++it) {
+                const int s = (int)(it % TC_STAGES);
+                const int64_t r0 = ch * chunk;                  // relative to rlo
+                const int rows = (int)(H - r0 < chunk ? H - r0 : chunk);
+                mbar_wait(&full[s], (unsigned)((it / TC_STAGES) & 1));
+                const double* src = stage + (size_t)s * TC_CHUNK;
+                for (int i = 2 * tid; i < rows; i += 2 * TC_THREADS) {   // consecutive 16 B per thread
+                    if (i + 1 < rows) {
+                        const double2 av = *reinterpret_cast<const double2*>(src + i);
+                        const double2 rv = *reinterpret_cast<const double2*>(rs + r0 + i);
+                        sacc = fma(av.x, rv.x, sacc);
+                        sacc = fma(av.y, rv.y, sacc);
+                    } else {
+                        sacc = fma(src[i], rs[r0 + i], sacc);
+                    }
+                }
+                __syncthreads();                                // stage s consumed
+                if (tid == 0 && it + TC_STAGES < total) issue(it + TC_STAGES);
+            }
+#pragma unroll
+            for (int k = 0; k < BWD_NB; ++k)
+                if (k == c) acc[k] = sacc;
+        }
+        // group complete: reduce the nc column dots
+        const int par = (int)(g & 1);
+#pragma unroll
+        for (int k = 0; k < BWD_NB; ++k) {
+            const double v = warp_red<0>(acc[k]);
+            if (lane == 0) wsh[par][warp][k] = v;
+            acc[k] = 0.0;
+        }
+        __syncthreads();
+        if (tid < nc) {
+            double v = wsh[par][0][tid];
+            for (int w = 1; w < TC_THREADS / 32; ++w) v += wsh[par][w][tid];
+            dh[g * BWD_NB + tid] = v;
+        }
+    }
+    __syncthreads();
+    // ---- combine the two half-row dots over DSMEM: rank 0 part + rank 1 part
+    const int64_t ccount = j1 - j0;
+    cluster_sync_all();
+    for (int64_t t = tid; t < ccount; t += TC_THREADS) {
+        const double a0 = h == 0 ? dh[t] : ld_dsmem(dh + t, 0);
+        const double a1 = h == 1 ? dh[t] : ld_dsmem(dh + t, 1);
+        dfull[t] = a0 + a1;
+    }
+    cluster_sync_all();                                         // partner done reading our dh
+    // ---- epilogue: CTA h owns columns [e0, e1) of the cluster range
+    const int64_t e0 = h ? ccount / 2 : 0, e1 = h ? ccount : ccount / 2;
+    const int nvg = P.split ? 2 : 1;
+    const int64_t ecols = e1 - e0, nvar = ecols * nvg;
+    if (mode == BWD_PLAIN) {
+        for (int64_t t = tid; t < nvar; t += TC_THREADS) {
+            const int64_t jj = e0 + t % ecols, vv = t / ecols;
+            const int64_t j = j0 + jj;
+            const double dot = dfull[jj];
+            double dval = vv ? -dot : dot;
+            if (P.colscale) dval = P.colscale[j] * dot;
+            gout[j + vv * ncols] = dval;
+        }
+        return;
+    }
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    GramEnt ent;
+    const int ne = E.nb * (E.nb + 1) / 2;
+    ent.init(E.nb, ne, ne + (P.screen_full ? E.nh : 0), E.nh);
+    double gacc[3] = {0.0, 0.0, 0.0};
+    double gmax = 0.0, cnt = 0.0;
+    constexpr int EPI_ROWS = 256;                               // tile fits the 128 KB stage ring
+    double* tile = stage;                                       // stages are free now
+    double* mk = stage + (size_t)EPI_ROWS * E.nb;
+    for (int64_t vb = 0; vb < nvar; vb += EPI_ROWS) {
+        const int rows = (int)(nvar - vb < EPI_ROWS ? nvar - vb : EPI_ROWS);
+        if (tid < rows) {
+            const int64_t idx = vb + tid;
+            const int64_t jj = e0 + idx % ecols, vv = idx / ecols;
+            const int64_t j = j0 + jj;
+            const double dot = dfull[jj];
+            double dval = vv ? -dot : dot;
+            if (P.colscale) dval = P.colscale[j] * dot;
+            epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)tid * E.nb, mk + tid, gmax, cnt);
+        }
+        if (E.gram) {
+            __syncthreads();
+            ent.accumulate(tile, mk, rows, E.nb, gacc);
+        }
+        __syncthreads();
+    }
+    if (!E.gram) return;
+    gram_tail(P, C, E, gacc, gmax, cnt, red, stage, 4096, stash, Gs);
+}
+
+// smem k_bwd_c needs (0 = does not fit / not applicable)
+static size_t bwd_c_smem(const Prob& P, int ncl, int* hmax, int* cmax)
+{
+    if (P.m % 2 != 0 || P.m < 4096) return 0;
+    const int64_t mid = ((P.m / 2) + 1) & ~(int64_t)1;
+    const int64_t H = P.m - mid > mid ? P.m - mid : mid;
+    const int64_t cm = (P.ncols + ncl - 1) / ncl + 1;
+    const size_t bytes = (size_t)TC_STAGES * TC_STAGE_BYTES + sizeof(double) * (size_t)(H + 2 * cm + 8);
+    if (bytes > (size_t)TC_SMEM_MAX) return 0;
+    *hmax = (int)H;
+    *cmax = (int)cm;
+    return bytes;
+}
+
 // ---------------------------------------------------------------- k_bwd (generic)
 template <bool VEC>
 __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* rvec, double* gout)
@@ -572,6 +820,9 @@ __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* r
 
 // ---------------------------------------------------------------- launch
 static int g_bwd_occ = 0, g_bwdw_occ = 0;
+// k_bwd_c (TMA, CTA pairs) is opt-in: on C2 it measured 275-335 us vs 268 us for k_bwd_s
+// (DESIGN.md section 5); enable with LBFGSB_TMA=1 for experiments.
+static bool g_no_tma = getenv("LBFGSB_TMA") == nullptr;
 constexpr int BWD_W_MAXM = 2048;
 constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + 64);
 static bool g_bwd_init = false;
@@ -583,6 +834,7 @@ static void bwd_init()
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd<true>, NT, 0);
     g_bwd_occ = o > 0 ? o : 1;
     cudaFuncSetAttribute(k_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_MAX);
+    cudaFuncSetAttribute(k_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
     cudaFuncSetAttribute(k_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_W_SMEM_MAX);
     o = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_w, NT, BWD_W_SMEM_MAX);
@@ -629,6 +881,15 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         const size_t sm = sizeof(double) * ((size_t)mpad + WTILE * (MAXB + 1));
         k_bwd_w<<<G, NT, sm, st>>>(P, mode, rvec, gout, mpad);
         return;
+    }
+    if (aligned && !g_no_tma) {
+        const int ncl = (int)(P.ncols < sms / 2 ? P.ncols : sms / 2);
+        int hmax = 0, cmax = 0;
+        const size_t csm = bwd_c_smem(P, ncl, &hmax, &cmax);
+        if (csm && ncl >= 1) {
+            k_bwd_c<<<2 * ncl, TC_THREADS, csm, st>>>(P, mode, rvec, gout, hmax, cmax);
+            return;
+        }
     }
     if (smem && P.m >= 2048) {
         const int64_t cmax = (P.ncols + Gs_ - 1) / Gs_;

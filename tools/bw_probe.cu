@@ -100,6 +100,44 @@ __global__ void bulk_sum(const double* __restrict__ a, size_t n, double* out)
     if (acc == 123.456) out[0] = acc;
 }
 
+
+template <int STAGES, int BYTES>
+__global__ void __cluster_dims__(2, 1, 1) bulk_sum_cl(const double* __restrict__ a, size_t n, double* out)
+{
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t full[STAGES];
+    const size_t per = (n + gridDim.x - 1) / gridDim.x;
+    const size_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+    const size_t elems = BYTES / 8;
+    const size_t nchunks = (b1 - b0 + elems - 1) / elems;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    auto issue = [&](size_t c) {
+        const int s = c % STAGES;
+        const size_t e0 = b0 + c * elems;
+        const size_t cnt = e0 + elems < b1 ? elems : b1 - e0;
+        mbar_expect_tx(&full[s], (unsigned)(cnt * 8));
+        bulk_g2s(sm + (size_t)s * BYTES, a + e0, (unsigned)(cnt * 8), &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (size_t c = 0; c < (size_t)STAGES && c < nchunks; ++c) issue(c);
+    double acc = 0.0;
+    for (size_t c = 0; c < nchunks; ++c) {
+        const int s = c % STAGES;
+        mbar_wait(&full[s], (unsigned)((c / STAGES) & 1));
+        const size_t e0 = b0 + c * elems;
+        const size_t cnt = e0 + elems < b1 ? elems : b1 - e0;
+        const double* buf = reinterpret_cast<const double*>(sm + (size_t)s * BYTES);
+        for (size_t k = threadIdx.x; k < cnt; k += blockDim.x) acc += buf[k];
+        __syncthreads();
+        if (threadIdx.x == 0 && c + STAGES < nchunks) issue(c + STAGES);
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
 template <typename F>
 float timeit(F f, int reps)
 {
@@ -178,6 +216,15 @@ int main()
         constexpr int S = 6, B = 8192;
         cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
         rep("bulk 6x8KB 1CTA/SM tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+    }
+    {
+        constexpr int S = 4, B = 32768;
+        cudaFuncSetAttribute(bulk_sum_cl<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        rep("bulk 4x32KB cluster2 smem128K tpb=512", timeit([&] { bulk_sum_cl<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
+        rep("bulk 4x32KB cluster2 smem200K tpb=512", timeit([&] { bulk_sum_cl<S, B><<<sms, 512, 200 * 1024>>>(a, n, out); }, 10));
+        cudaFuncSetAttribute(bulk_sum<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        rep("bulk 4x32KB nocluster smem200K tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, 200 * 1024>>>(a, n, out); }, 10));
+        rep("bulk 4x32KB nocluster smem128K tpb=512", timeit([&] { bulk_sum<S, B><<<sms, 512, S * B>>>(a, n, out); }, 10));
     }
     // copy reference (cudaMemcpy D2D, read+write counted)
     double* b; cudaMalloc(&b, bytes / 2);
