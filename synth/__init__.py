@@ -146,6 +146,61 @@ def weak_shard(m: int, ncols_local: int, rank: int, seed: int):
 
 
 
+# --------------------------------------------------------------------------- C5 (device-generated)
+def _gen_lib():
+    """synth/libsynth.so (nvcc, sm_100a): the device twin of synth/philox.py."""
+    import ctypes, os, subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    src, lib = os.path.join(here, "csrc", "gen.cu"), os.path.join(here, "libsynth.so")
+    if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-Xcompiler", "-fPIC", "-shared", src, "-o", lib + ".tmp"])
+        os.replace(lib + ".tmp", lib)
+    L = ctypes.CDLL(lib)
+    L.synth_fill_centered.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_double,
+                                      ctypes.c_void_p]
+    L.synth_fill_centered.restype = ctypes.c_int
+    return L
+
+
+def c5_device(m: int = 100000, n: int = 200000, seed: int = 5, col0: int = 0, ncols: int | None = None,
+              device="cuda", b_chunk: int = 2048):
+    """C5: NNLS with A_ij = (u_ij - 1/2) sqrt(12/m) generated ON the
+    device (Philox, bit-identical to synth.philox on the host); planted x (10%
+    nonzeros |N(0,1)|, numpy seed) and b = A x_plant + 0.1 z with the product
+    formed by torch GEMVs over column chunks (library routine, input synthesis).
+    Returns (A (m, ncols) column-major torch tensor for columns [col0, col0+ncols), b (m,) numpy,
+    x_plant (n,) numpy).  b always covers ALL n columns (replicated across shards)."""
+    import torch
+    L = _gen_lib()
+    ncols = n - col0 if ncols is None else ncols
+    scale = float(np.sqrt(12.0 / m))
+    rng = np.random.default_rng(seed)
+    xp = np.zeros(n)
+    nz = rng.random(n) < 0.1
+    xp[nz] = np.abs(rng.standard_normal(int(nz.sum())))
+    z = rng.standard_normal(m)
+    st = torch.cuda.current_stream().cuda_stream
+    At = torch.empty((ncols, m), dtype=torch.float64, device=device)   # column-major (m, ncols)
+    rc = L.synth_fill_centered(At.data_ptr(), m, ncols, m, col0, seed, 0, scale, st)
+    if rc != 0:
+        raise RuntimeError(f"synth_fill_centered failed: {rc}")
+    # b = A x_plant + 0.1 z over ALL columns (chunks of the full matrix regenerated on the fly)
+    bt = torch.zeros(m, dtype=torch.float64, device=device)
+    tmp = torch.empty((b_chunk, m), dtype=torch.float64, device=device)
+    for c0 in range(0, n, b_chunk):
+        k = min(b_chunk, n - c0)
+        xs = xp[c0:c0 + k]
+        if not np.any(xs):
+            continue
+        L.synth_fill_centered(tmp.data_ptr(), m, k, m, c0, seed, 0, scale, st)
+        bt += tmp[:k].T @ torch.from_numpy(xs).to(device)
+    del tmp
+    b = bt.cpu().numpy() + 0.1 * z
+    return At.T, b, xp
+
+
 # Named configurations of BASELINE.json "configs" (SURVEY.md 8(d) table)
 CONFIGS = {
     "C1": lambda seed=1: nnls_gaussian(200, 100, seed, "C1_nnls_200x100"),
