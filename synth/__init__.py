@@ -136,10 +136,12 @@ def svm_dual_linear(N: int, d: int, seed: int, C: float = 1.0, sep: float = 2.0)
 def weak_shard(m: int, ncols_local: int, rank: int, seed: int):
     """Rank `rank`'s column block of the weak-scaled NNLS workload: the global
     A = [A_0 | ... | A_{N-1}] with A_r ~ N(0,1)/sqrt(m) drawn from
-    default_rng([seed, r]) and b ~ N(0,1) from default_rng(seed) (replicated),
+    default_rng([seed, 0xA11, r+1]) and b ~ N(0,1) from default_rng([seed, 0xB0B]) (replicated),
     so the global problem is a C2-distributed NNLS with n = N * ncols_local."""
-    b = np.random.default_rng(seed).standard_normal(m)
-    rng = np.random.default_rng([seed, rank])
+    # distinct SeedSequence entropies for b and every block (note: numpy treats
+    # [seed, 0] like [seed], so the rank is offset to keep the streams apart)
+    b = np.random.default_rng([seed, 0xB0B]).standard_normal(m)
+    rng = np.random.default_rng([seed, 0xA11, rank + 1])
     A = rng.standard_normal((ncols_local, m)).T / np.sqrt(m)
     return Problem("nnls", f"weak_shard_r{rank}", A, b=b, lower=np.zeros(ncols_local),
                          meta=dict(m=m, ncols_local=ncols_local, rank=rank, seed=seed))

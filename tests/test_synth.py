@@ -30,3 +30,14 @@ def test_generators_deterministic():
     b = synth.nnls_gaussian(30, 20, 7)
     assert np.array_equal(a.M, b.M) and np.array_equal(a.b, b.b)
     assert a.M.flags.f_contiguous
+
+
+def test_weak_shards_independent_of_b():
+    """Regression: the weak-scaling shards must not share a random stream with b
+    (numpy SeedSequence([s, 0]) == SeedSequence(s) once made column 0 of A = b/sqrt(m))."""
+    p0, p1 = synth.weak_shard(300, 50, 0, 2), synth.weak_shard(300, 50, 1, 2)
+    assert np.array_equal(p0.b, p1.b)
+    for p in (p0, p1):
+        c = np.abs(p.M.T @ p.b) / (np.linalg.norm(p.M, axis=0) * np.linalg.norm(p.b))
+        assert c.max() < 0.5
+    assert not np.allclose(p0.M, p1.M)
