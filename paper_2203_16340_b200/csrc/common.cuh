@@ -59,6 +59,27 @@ __device__ __forceinline__ double block_reduce(double v, double* sh)
     return r;
 }
 
+// N block-wide sums with a single barrier: warp shuffles, one smem stage
+// (sh >= N * warps doubles), threads k < N sum the warp partials in warp
+// order.  out[k] valid for all threads after the call (trailing barrier).
+template <int N>
+__device__ __forceinline__ void block_sum_multi(const double* v, double* sh, double* out)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const double s = warp_red<0>(v[k]);
+        if (lane == 0) sh[w * N + k] = s;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < N) {
+        double s = sh[threadIdx.x];
+        for (int i = 1; i < nw; ++i) s += sh[i * N + threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ bool halted(const Ctrl* C) { return (C->done | C->stall) != 0; }
 
 // Last-CTA ticket: true in every thread of the last of `total` CTAs to arrive.

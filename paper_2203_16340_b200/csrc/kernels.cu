@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
     __shared__ double buf[1024];
     __shared__ double stash[NT];
     __shared__ double res[4];
+    __shared__ double msh[NT / 32 * 3];
     if (threadIdx.x < 2 * nh + 1) cf[threadIdx.x] = C->coef[threadIdx.x];
     if (threadIdx.x < nh) {
         const int s = ring_slot(head, nh, threadIdx.x, mh);
@@ -101,13 +102,12 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
         else if (pt > 0.0) t = (uj - xj) / pt;
         amin = t < amin ? t : amin;
     }
-    const double a0 = block_reduce<0>(spg, red);
-    const double a1 = block_reduce<0>(spp, red);
-    const double a2 = block_reduce<0>(stg, red);
+    const double v3[3] = {spg, spp, stg};
+    block_sum_multi<3>(v3, msh, res);
     const double a3 = block_reduce<2>(amin, red);
     if (threadIdx.x == 0) {
         double* o = P.dir_part + (int64_t)blockIdx.x * 4;
-        o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+        o[0] = res[0]; o[1] = res[1]; o[2] = res[2]; o[3] = a3;
     }
     if (!last_cta(P.tickets + T_DIR, gridDim.x)) return;
     reduce_parts(P.dir_part, gridDim.x, 4, 4, [](int e) { return e == 3 ? 2 : 0; }, buf, 1024,
@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
     __shared__ double stash[NT];
     __shared__ double Ssum[KT];
     __shared__ double sepv[KT * NSEP];
+    __shared__ double msh[NT / 32 * KT];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool r0ok = row < m, r1ok = row + 1 < m;
     double acc0 = 0.0, acc1 = 0.0;
@@ -364,9 +365,12 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
             acc[t] = s;
         }
     }
-    for (int t = 0; t < ntr; ++t) {
-        const double s = block_reduce<0>(acc[t], red);
-        if (threadIdx.x == 0) P.lsp[(int64_t)blockIdx.x * KT + t] = s;
+    if (ntr == 1) {
+        const double s = block_reduce<0>(acc[0], red);
+        if (threadIdx.x == 0) P.lsp[(int64_t)blockIdx.x * KT] = s;
+    } else {
+        block_sum_multi<KT>(acc, msh, Ssum);
+        if (threadIdx.x < KT) P.lsp[(int64_t)blockIdx.x * KT + threadIdx.x] = Ssum[threadIdx.x];
     }
     // ---- global tail: the Armijo decision (ITER) or f(x) (SETUP)
     if (!last_cta(P.tickets + T_FWD_ALL, gridDim.x)) return;
@@ -399,6 +403,7 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
     __shared__ double stash[NT];
     __shared__ double Ssum[KT];
     __shared__ double sepv[KT * NSEP];
+    __shared__ double msh[NT / 32 * KT];
     const bool op = mode == LS_OP, setup = mode == LS_SH_SETUP, gather = mode == LS_SH_ITER || setup;
     double* rcur = op ? nullptr : P.rbuf[C->rsel];
     const double* r = op ? rv : rcur;
@@ -432,10 +437,8 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
             acc[t] += v * v;
         }
     }
-    for (int t = 0; t < ntr; ++t) {
-        const double s = block_reduce<0>(acc[t], red);
-        if (threadIdx.x == 0) P.lsp[(int64_t)blockIdx.x * KT + t] = s;
-    }
+    block_sum_multi<KT>(acc, msh, Ssum);
+    if ((int)threadIdx.x < ntr) P.lsp[(int64_t)blockIdx.x * KT + threadIdx.x] = Ssum[threadIdx.x];
     if (!last_cta(P.tickets + T_LS, gridDim.x)) return;
     reduce_parts(P.lsp, gridDim.x, KT, ntr, [](int) { return 0; }, buf, 1024, stash, Ssum);
     reduce_sep(P, ntr, buf, 1024, stash, sepv);
