@@ -21,19 +21,20 @@
 
 namespace lb {
 
-constexpr int NTB = 512;                // threads of k_bwd_s
+constexpr int NTB = 512;                // threads of k_bwd_s (one CTA per SM)
+constexpr int EPI_TILE = 256;           // epilogue tile rows
 constexpr int BWD_SMEM_MAX = 210 * 1024;   // dynamic; + ~10 KB static <= 227 KB per CTA
 
 // ---------------------------------------------------------------- column dots
 // acc[c] += sum over this thread's rows of M[i, jg + c] * r'_i, rows
 // i = 2 tid + 2 blockDim k (row pairs), two row pairs per loop trip.
-template <int NC>
+template <int NC, bool TWO = true>
 __device__ __forceinline__ void col_dots_smem(const double* __restrict__ M0, int64_t ld, int64_t m,
                                               const double* rs, double* acc)
 {
     const int64_t step = 2 * (int64_t)blockDim.x;
     int64_t i = 2 * (int64_t)threadIdx.x;
-    for (; i + step + 1 < m; i += 2 * step) {
+    for (; TWO && i + step + 1 < m; i += 2 * step) {
         double2 a0[NC], a1[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
@@ -338,9 +339,9 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
     double gacc[3] = {0.0, 0.0, 0.0};
     double gmax = 0.0, cnt = 0.0;
     double* tile = rs;                                          // r' no longer needed
-    double* mk = rs + (int64_t)NTB * E.nb;
-    for (int vb = 0; vb < nvar; vb += NTB) {
-        const int rows = nvar - vb < NTB ? nvar - vb : NTB;
+    double* mk = rs + (int64_t)EPI_TILE * E.nb;
+    for (int vb = 0; vb < nvar; vb += EPI_TILE) {
+        const int rows = nvar - vb < EPI_TILE ? nvar - vb : EPI_TILE;
         const int t = threadIdx.x;
         if (t < rows) {
             const int idx = vb + t;
@@ -856,7 +857,7 @@ static size_t bwd_s_smem(const Prob& P, int G)
     const int64_t cmax = (P.ncols + G - 1) / G;
     const int nbmax = 2 * P.mh + 1;
     int64_t mpad = P.m + (P.m & 1);
-    const int64_t need_tile = (int64_t)NTB * (nbmax + 1);
+    const int64_t need_tile = (int64_t)EPI_TILE * (nbmax + 1);
     if (mpad < need_tile) mpad = need_tile;
     if (mpad < 4096) mpad = 4096;
     const size_t bytes = sizeof(double) * (size_t)(mpad + cmax + 1);
