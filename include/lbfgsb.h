@@ -86,7 +86,8 @@ typedef struct {
     int32_t check_every;        /* iterations launched between host checks; default 8   */
     int32_t use_graph;          /* 1: replay a CUDA graph of check_every iterations; 1  */
     int32_t profile;            /* 1: CUDA events around the two GEMV launches (ops.h)  */
-    int32_t pad_;
+    int32_t no_projection;      /* 1: skip Alg. 2's projected branch, always truncate
+                                   (the proof-only variant of PAPER.md:201); default 0 */
     int64_t max_iters;          /* default 10000                                        */
 } lbfgsb_opts;
 

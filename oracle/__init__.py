@@ -62,7 +62,8 @@ class _Lsq(C.Structure):
 class _Opts(C.Structure):
     _fields_ = [("eps", C.c_double), ("c1", C.c_double), ("shrink", C.c_double),
                 ("tol", C.c_double), ("max_backtracks", C.c_int32),
-                ("screen_full_norm", C.c_int32), ("max_iters", C.c_int64)]
+                ("screen_full_norm", C.c_int32), ("no_projection", C.c_int32),
+                ("max_iters", C.c_int64)]
 
 
 class _Res(C.Structure):
@@ -221,6 +222,7 @@ class Options:
     max_backtracks: int = 50   # R11
     screen_full_norm: bool = False  # R3
     max_iters: int = 10000
+    no_projection: bool = False     # PAPER.md:201 variant
 
 
 @dataclass
@@ -305,7 +307,7 @@ def minimize_lsq(P: LSQ, l=None, u=None, x0=None, m_hist=5, opts: Options | None
     l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
     u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               o.max_iters)
+               int(o.no_projection), o.max_iters)
     res = _Res()
     s = P._struct()
     _L().orc_minimize_lsq(C.byref(s), _ptr(l), _ptr(u), m_hist, C.byref(so), _ptr(x),
@@ -336,7 +338,7 @@ def al_solve(P: LSQ, l=None, u=None, m_hist=5, opts: Options | None = None,
     u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
     lam = np.zeros(max(P.n_eq, 1)); mu = np.zeros(max(P.n_in, 1))
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               o.max_iters)
+               int(o.no_projection), o.max_iters)
     sa = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer)
     s = P._struct()
     res = _AlRes()

@@ -171,6 +171,21 @@ int32_t orc_project_direction(int64_t n, const double* x, const double* g, const
     return 0;
 }
 
+/* Alg. 2 lines 6-8 alone: the variant of PAPER.md:201 ("one can skip the
+ * projection branch ... and still obtain convergence guarantees").  Returns 0
+ * (truncated). */
+int32_t orc_truncate_direction(int64_t n, const double* x, const double* d, const double* l,
+                               const double* u, double eps, double* p_out)
+{
+    for (int64_t j = 0; j < n; ++j) {
+        double pj = d[j];
+        if (d[j] < 0.0 && x[j] <= lo_of(l, j) + eps) pj = 0.0;
+        if (d[j] > 0.0 && x[j] >= up_of(u, j) - eps) pj = 0.0;
+        p_out[j] = pj;
+    }
+    return 0;
+}
+
 /* Largest alpha >= 0 with l <= x + alpha p <= u, as the minimum blocking
  * ratio; +inf if nothing blocks (Alg. 1 line 7 "appropriate upper bound on
  * alpha^k"; R10). */
@@ -318,6 +333,7 @@ static double half_sq(int64_t m, const double* r)
 typedef struct {
     double eps, c1, shrink, tol;
     int32_t max_backtracks, screen_full_norm;
+    int32_t no_projection;       /* 1: Alg. 2 without the projected branch */
     int64_t max_iters;
 } orc_opts;
 
@@ -396,7 +412,8 @@ void orc_minimize_lsq(const orc_lsq* P, const double* l, const double* u, int32_
         for (int attempt = 0; attempt < 2 && !accepted; ++attempt) {
             if (attempt == 1) { nh = 0; res->n_fallbacks += 1; }      /* R14 fallback */
             orc_two_loop(nv, g, fr, nh, Sr, Yr, o->eps, o->screen_full_norm, d);  /* line 4 */
-            const int32_t br = orc_project_direction(nv, x, g, d, l, u, o->eps, p); /* line 6 */
+            const int32_t br = o->no_projection ? orc_truncate_direction(nv, x, d, l, u, o->eps, p)
+                                                : orc_project_direction(nv, x, g, d, l, u, o->eps, p); /* line 6 */
             res->last_branch = br;
             double gp = 0.0;
             for (int64_t j = 0; j < nv; ++j) gp += g[j] * p[j];

@@ -90,6 +90,7 @@ struct Prob {
     // options
     double eps, c1, shrink;
     int max_bt, screen_full, mh;
+    int no_projection;      // Alg. 2 without the projected branch
     long long max_iters;
     // workspace
     double* x; double* g; double* d; double* pp; double* pt;

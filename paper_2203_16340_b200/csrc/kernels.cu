@@ -30,7 +30,7 @@ __device__ __forceinline__ void dir_decide(const Prob& P, Ctrl* C, const double*
 {
     const double eps = P.eps;
     const double Spg = res[0], Spp = res[1], Stg = res[2], amin_all = res[3];
-    const int projected = (Spg <= -eps * Spp && Spp >= eps) ? 1 : 0;    // Alg. 2 line 3
+    const int projected = (!P.no_projection && Spg <= -eps * Spp && Spp >= eps) ? 1 : 0;  // Alg. 2 line 3
     double amax = projected ? 1.0 : amin_all;
     if (amax < 0.0) amax = 0.0;
     const double gp = projected ? Spg : Stg;

@@ -357,6 +357,7 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
     P.l = h->l.d(); P.u = h->u.d();
     P.eps = h->o.eps; P.c1 = h->o.c1; P.shrink = h->o.shrink;
     P.max_bt = h->o.max_backtracks; P.screen_full = h->o.screen_full_norm; P.mh = h->mh;
+    P.no_projection = h->o.no_projection ? 1 : 0;
     P.max_iters = h->o.max_iters;
     P.x = h->x.d(); P.g = h->g.d(); P.d = h->d.d(); P.pp = h->pp.d(); P.pt = h->pt.d();
     P.S = h->S.d(); P.Y = h->Y.d(); P.mask = static_cast<uint8_t*>(h->mask.p);

@@ -459,3 +459,18 @@ def test_ds2_iteration_count_loose(orc):
         if r.f - fstar <= 1e-10:
             break
     assert 15 <= k <= 60, k
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_no_projection_variant_same_optimum(orc, seed):
+    """skipping Alg. 2's projection branch keeps the convergence
+    guarantee -- the variant reaches the brute-force NNLS optimum too."""
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.integers(3, 10)); m = n + 4
+    A = rng.standard_normal((m, n)) / np.sqrt(m)
+    b = rng.standard_normal(m)
+    x_bf, f_bf = _nnls_bruteforce(A, b)
+    r = orc.minimize_lsq(orc.LSQ(A, b=b), l=np.zeros(n),
+                         opts=orc.Options(tol=1e-11, max_iters=20000, no_projection=True))
+    assert r.status == orc.CONVERGED and r.last_branch == 0
+    assert abs(r.f - f_bf) <= 1e-10 * max(1.0, abs(f_bf))
