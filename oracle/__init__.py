@@ -56,7 +56,7 @@ class _Lsq(C.Structure):
                 ("b", _dp), ("c", _dp), ("delta", C.c_double),
                 ("n_eq", C.c_int32), ("E", _dp), ("e", _dp), ("lam", _dp),
                 ("n_in", C.c_int32), ("G", _dp), ("hv", _dp), ("mu", _dp),
-                ("rho", C.c_double)]
+                ("rho", C.c_double), ("qp", C.c_int32)]
 
 
 class _Opts(C.Structure):
@@ -243,9 +243,12 @@ class LSQ:
     """
 
     def __init__(self, M, b=None, c=None, delta=0.0, colscale=None, split=False,
-                 E=None, e=None, G=None, hv=None):
+                 E=None, e=None, G=None, hv=None, qp=False):
         self.M = np.asfortranarray(M, dtype=np.float64)
         self.m, self.ncols = self.M.shape
+        self.qp = bool(qp)           # 1/2 x^T D M D x (+ c, delta, AL); M square symmetric
+        if self.qp:
+            assert self.m == self.ncols and not split and b is None
         self.split = bool(split)
         self.nvars = 2 * self.ncols if split else self.ncols
         self.b = None if b is None else _f64(b)
@@ -273,6 +276,7 @@ class LSQ:
         s.n_eq = self.n_eq; s.E = _ptr(self.E); s.e = _ptr(self.e); s.lam = _ptr(self.lam)
         s.n_in = self.n_in; s.G = _ptr(self.G); s.hv = _ptr(self.hv); s.mu = _ptr(self.mu)
         s.rho = self.rho
+        s.qp = int(self.qp)
         return s
 
     def value(self, x):

@@ -225,6 +225,8 @@ typedef struct {
     int32_t n_in;                /* G nvars x n_in column-major, hv n_in */
     const double* G; const double* hv; const double* mu;
     double rho;
+    int32_t qp;                  /* 1: quadratic objective 1/2 x^T Q~ x, Q~ = D M D (M n x n
+                                    symmetric, D = diag(colscale)); "r" holds w = Q~ x */
 } orc_lsq;
 
 static int64_t lsq_nvars(const orc_lsq* P) { return P->split ? 2 * P->ncols : P->ncols; }
@@ -240,14 +242,16 @@ static void lsq_apply(const orc_lsq* P, const double* p, double* q)
         pe[j] = v;
     }
     orc_matvec(P->m, nc, P->M, P->lda, pe, q);
+    if (P->qp && P->colscale)                       /* Q~ = D M D: scale the rows too */
+        for (int64_t i = 0; i < P->m; ++i) q[i] = P->colscale[i] * q[i];
     free(pe);
 }
 
-/* r = M~ x - b */
+/* r = M~ x - b   (QP: w = Q~ x) */
 static void lsq_residual(const orc_lsq* P, const double* x, double* r)
 {
     lsq_apply(P, x, r);
-    if (P->b)
+    if (P->b && !P->qp)
         for (int64_t i = 0; i < P->m; ++i) r[i] = r[i] - P->b[i];
 }
 
@@ -296,18 +300,23 @@ static double lsq_phi(const orc_lsq* P, const double* x, double* coef_eq, double
     return phi;
 }
 
-/* g = M~^T r + c + delta x + E (rho h + lam) + G (rho g + mu)_+ */
+/* g = M~^T r + c + delta x + E (rho h + lam) + G (rho g + mu)_+
+ * (QP: g = w + c + delta x + ..., the gradient of 1/2 x^T Q~ x being w = Q~ x) */
 static void lsq_grad(const orc_lsq* P, const double* x, const double* r, double* g)
 {
     const int64_t nc = P->ncols, nv = lsq_nvars(P);
-    double* t = (double*)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
-    orc_matvec_t(P->m, nc, P->M, P->lda, r, t);
-    for (int64_t j = 0; j < nc; ++j) {
-        const double v = P->colscale ? P->colscale[j] * t[j] : t[j];
-        g[j] = v;
-        if (P->split) g[nc + j] = -v;
+    if (P->qp) {
+        for (int64_t j = 0; j < nv; ++j) g[j] = r[j];
+    } else {
+        double* t = (double*)malloc(sizeof(double) * (size_t)(nc > 0 ? nc : 1));
+        orc_matvec_t(P->m, nc, P->M, P->lda, r, t);
+        for (int64_t j = 0; j < nc; ++j) {
+            const double v = P->colscale ? P->colscale[j] * t[j] : t[j];
+            g[j] = v;
+            if (P->split) g[nc + j] = -v;
+        }
+        free(t);
     }
-    free(t);
     double ce[64], ci[64];
     lsq_phi(P, x, ce, ci);
     for (int64_t j = 0; j < nv; ++j) {
@@ -325,6 +334,19 @@ static double half_sq(int64_t m, const double* r)
     double s = 0.0;
     for (int64_t i = 0; i < m; ++i) s += r[i] * r[i];
     return 0.5 * s;
+}
+
+static double dotv(int64_t n, const double* a, const double* b)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+
+/* quadratic part of f at x with carried r:  LSQ 1/2 ||r||^2,  QP 1/2 x^T w */
+static double quad_value(const orc_lsq* P, const double* x, const double* r)
+{
+    return P->qp ? 0.5 * dotv(P->m, x, r) : half_sq(P->m, r);
 }
 
 /* ------------------------------------------------------------------ */
@@ -360,11 +382,15 @@ static int armijo_lsq(const orc_lsq* P, const orc_opts* o, int64_t nv, const dou
                       int64_t* n_fg, int64_t* n_bt)
 {
     double alpha = amax < 1.0 ? amax : 1.0;
+    double xw = 0.0, pw = 0.0, pq = 0.0;
+    if (P->qp) { xw = dotv(nv, x, r); pw = dotv(nv, p, r); pq = dotv(nv, p, q); }
     for (int32_t t = 0; t <= o->max_backtracks; ++t) {
         if (t > 0) alpha = o->shrink * alpha;
         for (int64_t j = 0; j < nv; ++j) x_t[j] = clip1(fma(alpha, p[j], x[j]), l, u, j);
         for (int64_t i = 0; i < P->m; ++i) r_t[i] = fma(alpha, q[i], r[i]);
-        const double ft = half_sq(P->m, r_t) + lsq_phi(P, x_t, NULL, NULL);
+        const double quad = P->qp ? 0.5 * xw + alpha * pw + 0.5 * alpha * alpha * pq
+                                  : half_sq(P->m, r_t);
+        const double ft = quad + lsq_phi(P, x_t, NULL, NULL);
         *n_fg += 1;
         if (ft <= f + o->c1 * alpha * gp) {
             *f_out = ft; *alpha_out = alpha;
@@ -393,7 +419,7 @@ void orc_minimize_lsq(const orc_lsq* P, const double* l, const double* u, int32_
     memset(res, 0, sizeof(*res));
     orc_clip(nv, x, l, u, x);                                   /* feasible x^0 */
     lsq_residual(P, x, r);
-    double f = half_sq(m, r) + lsq_phi(P, x, NULL, NULL);
+    double f = quad_value(P, x, r) + lsq_phi(P, x, NULL, NULL);
     lsq_grad(P, x, r, g);
     res->n_fg = 1;
 
@@ -448,7 +474,7 @@ void orc_minimize_lsq(const orc_lsq* P, const double* l, const double* u, int32_
 
     /* final refresh: r = M~x - b, g, f; pg = ||clip(x - g) - x||_inf */
     lsq_residual(P, x, r);
-    f = half_sq(m, r) + lsq_phi(P, x, NULL, NULL);
+    f = quad_value(P, x, r) + lsq_phi(P, x, NULL, NULL);
     lsq_grad(P, x, r, g);
     orc_working_set(nv, x, g, l, u, o->eps, fr);
     double pg = 0.0, gfree = 0.0; int64_t nfree = 0;
@@ -548,7 +574,7 @@ void orc_al_solve(orc_lsq* P, double* lam_io, double* mu_io, const double* l, co
         orc_lsq Q = *P; Q.n_eq = 0; Q.n_in = 0;
         double* r = malloc(sizeof(double) * (size_t)(P->m > 0 ? P->m : 1));
         lsq_residual(&Q, x, r);
-        res->f = half_sq(P->m, r) + lsq_phi(&Q, x, NULL, NULL);
+        res->f = quad_value(&Q, x, r) + lsq_phi(&Q, x, NULL, NULL);
         free(r);
     }
     res->violation_inf = viol_inf(P, x, mu_io, rho);
@@ -567,7 +593,7 @@ double orc_lsq_value(const orc_lsq* P, const double* x)
 {
     double* r = malloc(sizeof(double) * (size_t)(P->m > 0 ? P->m : 1));
     lsq_residual(P, x, r);
-    const double f = half_sq(P->m, r) + lsq_phi(P, x, NULL, NULL);
+    const double f = quad_value(P, x, r) + lsq_phi(P, x, NULL, NULL);
     free(r);
     return f;
 }

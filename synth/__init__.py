@@ -203,6 +203,40 @@ def c5_device(m: int = 100000, n: int = 200000, seed: int = 5, col0: int = 0, nc
     return At.T, b, xp
 
 
+def blobs(N: int, d: int, seed: int, sep: float = 2.0):
+    """Two Gaussian blobs, labels +-1 balanced: x_i ~ N(y_i sep/sqrt(d) 1, I_d).
+    Returns (X (N, d) row-major, y (N,))."""
+    rng = np.random.default_rng(seed)
+    y = np.where(np.arange(N) % 2 == 0, 1.0, -1.0)
+    rng.shuffle(y)
+    X = rng.standard_normal((N, d)) + (y * (sep / np.sqrt(d)))[:, None]
+    return X, y
+
+
+def gaussian_kernel(X, gamma: float):
+    """K_ij = exp(-gamma ||x_i - x_j||^2) (PAPER.md:355 "standard Gaussian kernel"), numpy, by
+    direct differences (no ||x||^2 expansion)."""
+    X = np.asarray(X, dtype=np.float64)
+    N = X.shape[0]
+    K = np.empty((N, N))
+    for i in range(N):
+        d = X - X[i]
+        K[:, i] = np.exp(-gamma * np.einsum("ij,ij->i", d, d))
+    return np.asfortranarray(K)
+
+
+def svm_dual_kernel(N: int, d: int, seed: int, gamma: float = 1.0, C: float = 1.0, sep: float = 2.0):
+    """N1: Gaussian-kernel dual SVM on synthetic blobs (PAPER.md:349-355,
+    gamma = 1, c = 1): min 1/2 (a*y)^T K (a*y) - 1^T a s.t. y^T a = 0, 0 <= a <= C.
+    Returns the Problem with M = K (QP objective, colscale = y) and the raw X."""
+    X, y = blobs(N, d, seed, sep)
+    K = gaussian_kernel(X, gamma)
+    p = Problem("svm_kernel", f"svmk_{N}x{d}", K, b=None, c=-np.ones(N), colscale=y,
+                lower=np.zeros(N), upper=np.full(N, C), E=y.reshape(N, 1), e=np.zeros(1),
+                meta=dict(N=N, d=d, seed=seed, gamma=gamma, C=C, X=X, qp=True))
+    return p
+
+
 # Named configurations of BASELINE.json "configs" (SURVEY.md 8(d) table)
 CONFIGS = {
     "C1": lambda seed=1: nnls_gaussian(200, 100, seed, "C1_nnls_200x100"),
