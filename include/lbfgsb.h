@@ -159,6 +159,17 @@ lbfgsb_err lbfgsb_objective_lsq(const double* M, int64_t m, int64_t ncols, int64
                                 const double* colscale, int32_t split, const double* b,
                                 const double* c, double delta, lbfgsb_objective** out);
 
+/* Built-in dense QP (the Gaussian-kernel dual SVM of
+ * PAPER.md:349-355):  f(x) = 1/2 x^T D Q D x + c^T x + delta/2 ||x||^2, with Q
+ * n x n symmetric column-major (ld >= n, DEVICE, borrowed) and D =
+ * diag(colscale) (NULL = identity; the SVM labels y).  The gradient is
+ * carried as w = D Q D x (w' = w + alpha D Q D p, reading R13 for QPs), so an
+ * iteration needs ONE pass over the active columns of Q; trial values are
+ * 1/2 x^T w + alpha p^T w + 1/2 alpha^2 p^T (DQDp) + c^T x_t + ....
+ * Single-GPU handles only (sharded: UNSUPPORTED).  Errors: ARG, DIM. */
+lbfgsb_err lbfgsb_objective_qp(const double* Q, int64_t n, int64_t ld, const double* colscale,
+                               const double* c, double delta, lbfgsb_objective** out);
+
 /* User objective: fg(user, x, g, f_host, stream) must write grad f(x) into
  * the DEVICE vector g (length n), *f_host = f(x) (host), enqueue its device
  * work on `stream` (or synchronise it), and return 0 (nonzero -> the solve

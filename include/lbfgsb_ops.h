@@ -28,6 +28,14 @@ lbfgsb_err lbfgsb_op_gemv(const lbfgsb_objective* obj, const double* p, double* 
 lbfgsb_err lbfgsb_op_gemvt(const lbfgsb_objective* obj, const double* r, double* g,
                            void* cuda_stream);
 
+/* Gaussian kernel matrix of SURVEY.md 8(f) N1 ("standard
+ * Gaussian kernel with bandwidth parameter gamma"): K(i, j) =
+ * exp(-gamma ||x_i - x_j||^2) by direct differences.  X: N x d row-major
+ * (sample i at X + i*d, DEVICE); K: N x N column-major, ld ldk >= N (DEVICE,
+ * caller-allocated, N*ldk*8 bytes).  Errors: ARG, CUDA. */
+lbfgsb_err lbfgsb_op_gaussian_kernel(const double* X, int64_t N, int64_t d, double gamma, double* K,
+                                     int64_t ldk, void* cuda_stream);
+
 /* Direction pipeline of one iteration (rows a4, a5, a6): working set Eq. (1)
  * (PAPER.md:104-110), masked Gram + vector-free Alg. 3,
  * d[S-bar] = 0, Alg. 2.

@@ -19,7 +19,7 @@ from . import _build
 
 __all__ = ["Options", "ALOptions", "Result", "ALResult", "Solver", "LSQObjective",
            "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor",
-           "solve_loopback", "nccl_unique_id"]
+           "solve_loopback", "nccl_unique_id", "QPObjective", "op_gaussian_kernel"]
 
 _c_d, _c_i32, _c_i64, _c_vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
 
@@ -103,10 +103,13 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_solve_loopback.argtypes = [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), _c_i32, _c_d,
                                         C.POINTER(_Res)]
     L.lbfgsb_nccl_unique_id.argtypes = [vp]
+    L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
+    L.lbfgsb_op_gaussian_kernel.argtypes = [vp, _c_i64, _c_i64, _c_d, vp, _c_i64, vp]
     for name in ("lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
                  "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
-                 "lbfgsb_profile_get", "lbfgsb_solve_loopback", "lbfgsb_nccl_unique_id"):
+                 "lbfgsb_profile_get", "lbfgsb_solve_loopback", "lbfgsb_nccl_unique_id",
+                 "lbfgsb_objective_qp", "lbfgsb_op_gaussian_kernel"):
         getattr(L, name).restype = _c_i32
     _lib = L
     return L
@@ -229,6 +232,24 @@ class LSQObjective:
         if getattr(self, "_h", None) and _lib is not None:
             _lib.lbfgsb_objective_free(self._h)
             self._h = None
+
+
+class QPObjective(LSQObjective):
+    """f(x) = 1/2 x^T D Q D x + c^T x + delta/2||x||^2 (lbfgsb_objective_qp): Q CUDA fp64
+    (n, n) symmetric column-major, D = diag(colscale) (e.g. the SVM labels)."""
+
+    def __init__(self, Q, c=None, delta=0.0, colscale=None):   # noqa: D107 -- no super().__init__
+        L = load()
+        if Q.dim() != 2 or Q.shape[0] != Q.shape[1] or (Q.stride(0) != 1 and Q.shape[0] > 1):
+            raise LbfgsbError("Q must be square (n, n) column-major")
+        self.m = self.ncols = self.nvars = Q.shape[0]
+        self.ld = max(Q.stride(1), self.m) if self.ncols > 1 else self.m
+        self.split = False
+        self._keep = (Q, c, colscale)
+        h = C.c_void_p()
+        _check(L.lbfgsb_objective_qp(_ptr(Q), self.m, self.ld, _ptr(colscale), _ptr(c), float(delta),
+                                     C.byref(h)))
+        self._h = h
 
 
 class CallbackObjective:
@@ -404,6 +425,18 @@ def solve_loopback(solvers, objs, xs, tol=0.0) -> Result:
     _check(load().lbfgsb_solve_loopback(hs, os_, xp, R, float(tol), C.byref(r)))
     return Result(r.f, r.pg_inf, r.gfree_inf, r.seconds, r.iters, r.n_fg, r.n_backtracks,
                   r.n_free, r.n_fallbacks, r.status, r.last_branch)
+
+
+def op_gaussian_kernel(X, gamma, stream=None):
+    """K = exp(-gamma ||x_i - x_j||^2) for X (N, d) row-major CUDA fp64; returns K (N, N)
+    column-major (lbfgsb_op_gaussian_kernel)."""
+    import torch
+    N, d = X.shape
+    Xc = X.contiguous()
+    Kt = torch.empty((N, N), dtype=torch.float64, device=X.device)   # column-major K = Kt^T
+    _check(load().lbfgsb_op_gaussian_kernel(_ptr(Xc), N, d, float(gamma), _ptr(Kt), N,
+                                            _stream_ptr(stream)))
+    return Kt.T
 
 
 def op_gemv(obj: LSQObjective, p, q, stream=None):

@@ -747,6 +747,58 @@ static size_t bwd_c_smem(const Prob& P, int ncl, int* hmax, int* cmax)
     return bytes;
 }
 
+// ---------------------------------------------------------------- k_qpu (QP objective)
+// QP objective (the kernel dual SVM): f = 1/2 x^T Q~ x + ..., the
+// gradient is carried as w = Q~ x (like the LSQ residual, R13): w' =
+// fma(alpha, q, w) with q = Q~ p from k_fwd, so an iteration needs ONE pass
+// over Q.  This elementwise kernel is the "a3" step of the QP: w', then the
+// same per-variable epilogue, Gram and Alg. 3 tail as k_bwd.
+__global__ void __launch_bounds__(NT) k_qpu(Prob P, int mode, int bufn)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    extern __shared__ __align__(16) double smq[];
+    __shared__ double red[NT / 32 * BWD_NB];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    const bool iter = mode == BWD_ITER;
+    const int rsel = C->rsel;
+    const double* wcur = P.rbuf[rsel];
+    double* wnext = P.rbuf[rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    double* tile = smq;
+    double* mk = smq + (size_t)NT * E.nb;
+    GramEnt ent;
+    const int ne = E.nb * (E.nb + 1) / 2;
+    ent.init(E.nb, ne, ne + (P.screen_full ? E.nh : 0), E.nh);
+    double gacc[3] = {0.0, 0.0, 0.0};
+    double gmax = 0.0, cnt = 0.0;
+    const int64_t n = P.n;
+    for (int64_t base = (int64_t)blockIdx.x * NT; base < n; base += (int64_t)gridDim.x * NT) {
+        const int64_t v = base + threadIdx.x;
+        if (v < n) {
+            double w = wcur[v];
+            if (iter) {
+                w = fma(alpha, P.q[v], w);                      // carried w' = Q~ x'
+                wnext[v] = w;
+            }
+            epilogue_var(P, C, E, v, w, tile + (int64_t)threadIdx.x * E.nb, mk + threadIdx.x, gmax, cnt);
+        } else if (E.gram) {
+            for (int b = 0; b < E.nb; ++b) tile[(int64_t)threadIdx.x * E.nb + b] = 0.0;
+            mk[threadIdx.x] = 0.0;
+        }
+        if (E.gram) {
+            __syncthreads();
+            ent.accumulate(tile, mk, NT, E.nb, gacc);
+            __syncthreads();
+        }
+    }
+    if (!E.gram) return;
+    gram_tail(P, C, E, gacc, gmax, cnt, red, smq, bufn, stash, Gs);
+}
+
 // ---------------------------------------------------------------- k_bwd (generic)
 template <bool VEC>
 __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* rvec, double* gout)
@@ -835,6 +887,8 @@ static void bwd_init()
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd<true>, NT, 0);
     g_bwd_occ = o > 0 ? o : 1;
     cudaFuncSetAttribute(k_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_MAX);
+    cudaFuncSetAttribute(k_qpu, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (NT * (MAXB + 1) > 4096 ? NT * (MAXB + 1) : 4096)));
     cudaFuncSetAttribute(k_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
     cudaFuncSetAttribute(k_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_W_SMEM_MAX);
     o = 0;
@@ -867,6 +921,16 @@ static size_t bwd_s_smem(const Prob& P, int G)
 void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, double* gout)
 {
     bwd_init();
+    if (P.qp && mode != BWD_PLAIN) {
+        const int sms = sm_count();
+        int64_t g = (P.n + NT - 1) / NT;
+        if (g > 2LL * sms) g = 2LL * sms;
+        const int nbmax = 2 * P.mh + 1;
+        int bufn = NT * (nbmax + 1);
+        if (bufn < 4096) bufn = 4096;
+        k_qpu<<<(int)g, NT, sizeof(double) * (size_t)bufn, st>>>(P, mode, bufn);
+        return;
+    }
     const double* r = mode == BWD_PLAIN ? rvec : P.rbuf[0];
     const bool aligned = (P.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(P.M) & 15u) == 0) &&
                          (reinterpret_cast<uintptr_t>(r) & 15u) == 0 &&

@@ -253,13 +253,13 @@ __device__ __forceinline__ void recur_decide(const Prob& P, Ctrl* C, const doubl
 
 // Trial objective from reduced sums (oracle order: 1/2 S + phi,
 // phi = c^T x + delta/2 ||x||^2, then the AL terms of Eq. (3)).
-__device__ __forceinline__ double trial_value(const Prob& P, const Ctrl* C, double S, const double* sep,
+__device__ __forceinline__ double trial_value(const Prob& P, const Ctrl* C, double quad, const double* sep,
                               double* ccoef, double* hval, double* fbase)
 {
     const int ncons = P.n_eq + P.n_in;
     const double cx = sep ? sep[0] : 0.0, xx = sep ? sep[1] : 0.0;
     double phi = cx + 0.5 * P.delta * xx;
-    if (fbase) *fbase = 0.5 * S + phi;
+    if (fbase) *fbase = quad + phi;
     for (int k = 0; k < ncons; ++k) {
         const double hv = sep[2 + k] - C->rhs[k];
         hval[k] = hv;
@@ -274,12 +274,25 @@ __device__ __forceinline__ double trial_value(const Prob& P, const Ctrl* C, doub
             ccoef[k] = C->rho * tt;
         }
     }
-    return 0.5 * S + phi;
+    return quad + phi;
+}
+
+// Quadratic part of the KT trial values of the current batch:
+//   LSQ: 1/2 ||fma(alpha_t, q, r)||^2 = 1/2 S[t]          (R13, carried residual)
+//   QP : 1/2 x^T w + alpha_t p^T w + 1/2 alpha_t^2 p^T q   (exact expansion of
+//        1/2 (x + alpha p)^T Q~ (x + alpha p) with the carried w = Q~ x)
+__device__ __forceinline__ void quad_values(const Prob& P, const Ctrl* C, const double* S, double* quad)
+{
+    double a = C->alpha0;
+    for (int t = 0; t < KT; ++t) {
+        if (t > 0) a = a * P.shrink;
+        quad[t] = P.qp ? 0.5 * C->qp_xw + a * C->qp_pw + 0.5 * a * a * C->qp_pq : 0.5 * S[t];
+    }
 }
 
 // Armijo decision over one batch of KT trials (R10, R11, R13); single thread.
 // S[t] = sum (r + alpha_t q)^2, sep[t*NSEP + s] the separable sums.
-__device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const double* S, const double* sep)
+__device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const double* quad, const double* sep)
 {
     double cc[MAXC], hv[MAXC];
     const int ncons = P.n_eq + P.n_in;
@@ -289,7 +302,7 @@ __device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const doub
         if (t > 0) a = a * P.shrink;
         if (C->ls_batch * KT + t > P.max_bt) break;
         ++tried;
-        const double ft = trial_value(P, C, S[t], sep ? sep + t * NSEP : nullptr, cc, hv, nullptr);
+        const double ft = trial_value(P, C, quad[t], sep ? sep + t * NSEP : nullptr, cc, hv, nullptr);
         if (ft <= C->f + P.c1 * a * C->gp) {                    // Armijo condition
             C->alpha = a;
             C->f_new = ft;

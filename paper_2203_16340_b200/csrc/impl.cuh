@@ -61,6 +61,7 @@ struct Ctrl {
     double f_new;
     double f_base;          // setup/refresh: f without the AL terms
     double gp, amax, alpha0, alpha, gfree, pg;
+    double qp_xw, qp_pw, qp_pq;   // QP objective: x^T w, p^T w, p^T q of the current step
     double tol;
     double coef[MAXB];      // d = sum_b coef[b] B_b on S (basis s_0..s_{nh-1}, y_0.., g)
     double ccoef[MAXC];     // AL gradient coefficients at the point whose gradient k_bwd forms
@@ -91,6 +92,7 @@ struct Prob {
     double eps, c1, shrink;
     int max_bt, screen_full, mh;
     int no_projection;      // Alg. 2 without the projected branch
+    int qp;                 // 1: f = 1/2 x^T D M D x + ... (M n x n symmetric); rbuf holds w = Q~ x
     long long max_iters;
     // workspace
     double* x; double* g; double* d; double* pp; double* pt;
@@ -155,6 +157,8 @@ void launch_kkt(const Prob& P, cudaStream_t st);
 void launch_dir_decide(const Prob& P, cudaStream_t st);
 void launch_gram_decide(const Prob& P, cudaStream_t st, int bwd_mode);
 void launch_kkt_decide(const Prob& P, cudaStream_t st);
+void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K, int64_t ldk,
+                  cudaStream_t st);
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);
 void launch_cb_trial(const Prob& P, cudaStream_t st, double alpha, double* xt);
 void launch_cb_commit(const Prob& P, cudaStream_t st, const double* xt, const double* gt, int slot);

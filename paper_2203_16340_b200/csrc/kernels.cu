@@ -331,6 +331,10 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
         if (r0ok) q0 += __ldcg(src + row);
         if (r1ok) q1 += __ldcg(src + row + 1);
     }
+    if (P.qp && P.colscale) {                                   // Q~ = D M D: row scaling
+        if (r0ok) q0 = P.colscale[row] * q0;
+        if (r1ok) q1 = P.colscale[row + 1] * q1;
+    }
     if (mode == FWD_P) {
         if (r0ok) qout[row] = q0;
         if (r1ok) qout[row + 1] = q1;
@@ -345,7 +349,30 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
     double* rcur = P.rbuf[rsel];
     double acc[KT];
     const int ntr = mode == FWD_SETUP ? 1 : KT;
-    if (mode == FWD_SETUP) {
+    if (P.qp) {
+        // QP: rows are variables; w = Q~x (setup) or the step sums x^T w, p^T w, p^T q
+        if (mode == FWD_SETUP) {
+            double s = 0.0;
+            if (r0ok) { rcur[row] = q0; s += P.x[row] * q0; }
+            if (r1ok) { rcur[row + 1] = q1; s += P.x[row + 1] * q1; }
+            acc[0] = s;
+        } else {
+            double xw = 0.0, pw = 0.0, pq = 0.0;
+            if (r0ok) {
+                P.q[row] = q0;
+                const double w = rcur[row], xi = P.x[row], pi = pv[row];
+                xw += xi * w; pw += pi * w; pq += pi * q0;
+            }
+            if (r1ok) {
+                P.q[row + 1] = q1;
+                const double w = rcur[row + 1], xi = P.x[row + 1], pi = pv[row + 1];
+                xw += xi * w; pw += pi * w; pq += pi * q1;
+            }
+            acc[0] = xw; acc[1] = pw; acc[2] = pq;
+#pragma unroll
+            for (int t = 3; t < KT; ++t) acc[t] = 0.0;
+        }
+    } else if (mode == FWD_SETUP) {
         // r = M~x - b (sum, then subtract), partial of ||r||^2
         double s = 0.0;
         if (r0ok) { const double r0 = P.b ? q0 - P.b[row] : q0; rcur[row] = r0; s += r0 * r0; }
@@ -380,14 +407,17 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
     const double* sp = P.GS ? sepv : nullptr;
     if (mode == FWD_SETUP) {
         double cc[MAXC], hv[MAXC], fb = 0.0;
-        const double f = trial_value(P, C, Ssum[0], sp, cc, hv, &fb);
+        const double f = trial_value(P, C, 0.5 * Ssum[0], sp, cc, hv, &fb);
         const int ncons = P.n_eq + P.n_in;
         C->f = f;
         C->f_base = fb;
         for (int k = 0; k < ncons; ++k) { C->ccoef[k] = cc[k]; C->hval[k] = hv[k]; }
         C->nonfinite = isfinite(f) ? 0 : 1;
     } else {
-        armijo_decide(P, C, Ssum, sp);
+        if (P.qp) { C->qp_xw = Ssum[0]; C->qp_pw = Ssum[1]; C->qp_pq = Ssum[2]; }
+        double quad[KT];
+        quad_values(P, C, Ssum, quad);
+        armijo_decide(P, C, quad, sp);
     }
 }
 
@@ -413,7 +443,7 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
     double acc[KT];
 #pragma unroll
     for (int t = 0; t < KT; ++t) acc[t] = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * NT) {
+    for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; !P.qp && i < P.m; i += (int64_t)gridDim.x * NT) {
         double qi;
         if (gather) {                                           // q = sum over ranks, rank order
             qi = 0.0;
@@ -446,7 +476,7 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
     const double* sp = P.GS ? sepv : nullptr;
     if (setup) {
         double cc[MAXC], hv[MAXC], fb = 0.0;
-        const double f = trial_value(P, C, Ssum[0], sp, cc, hv, &fb);
+        const double f = trial_value(P, C, 0.5 * Ssum[0], sp, cc, hv, &fb);
         const int ncons = P.n_eq + P.n_in;
         C->f = f;
         C->f_base = fb;
@@ -454,13 +484,15 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
         C->nonfinite = isfinite(f) ? 0 : 1;
         return;
     }
+    double quad[KT];
+    quad_values(P, C, Ssum, quad);
     if (mode == LS_OP) {
         double cc[MAXC], hv[MAXC];
         for (int t = 0; t < ntr_op; ++t)
-            f_out[t] = trial_value(P, C, Ssum[t], sp ? sp + t * NSEP : nullptr, cc, hv, nullptr);
+            f_out[t] = trial_value(P, C, quad[t], sp ? sp + t * NSEP : nullptr, cc, hv, nullptr);
         return;
     }
-    armijo_decide(P, C, Ssum, sp);
+    armijo_decide(P, C, quad, sp);
 }
 
 // ------------------------------------------------------------------ standalone Gram + Alg. 3
@@ -613,6 +645,47 @@ __global__ void k_cb_commit(Prob P, const double* xt, const double* gt, int slot
         P.x[j] = xt[j];
         P.g[j] = gt[j];
     }
+}
+
+// ------------------------------------------------------------------ Gaussian kernel build (N1)
+// K(i, j) = exp(-gamma ||x_i - x_j||^2) by direct differences (no ||x||^2
+// expansion, no cancellation), X row-major N x d.  32 x 32 output tile per
+// CTA (32 x 8 threads, 4 entries each), features staged in 32-wide chunks.
+__global__ void __launch_bounds__(256) k_gauss(const double* __restrict__ X, int64_t N, int64_t d,
+                                               double gamma, double* __restrict__ K, int64_t ldk)
+{
+    __shared__ double xi[32][33], xj[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t k0 = 0; k0 < d; k0 += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            const int64_t a = i0 + r, b = j0 + r, k = k0 + tx;
+            xi[r][tx] = (a < N && k < d) ? X[a * d + k] : 0.0;
+            xj[r][tx] = (b < N && k < d) ? X[b * d + k] : 0.0;
+        }
+        __syncthreads();
+        const int kk = (int)(d - k0 < 32 ? d - k0 : 32);
+        for (int k = 0; k < kk; ++k) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double t = xi[tx][k] - xj[ty + 8 * r][k];
+                s[r] += t * t;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i = i0 + tx, j = j0 + ty + 8 * r;
+        if (i < N && j < N) K[i + j * ldk] = exp(-gamma * s[r]);
+    }
+}
+
+void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K, int64_t ldk, cudaStream_t st)
+{
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((N + 31) / 32));
+    k_gauss<<<grid, dim3(32, 8), 0, st>>>(X, N, d, gamma, K, ldk);
 }
 
 // ------------------------------------------------------------------ launchers

@@ -66,6 +66,7 @@ struct lbfgsb_objective {
     double delta;
     lbfgsb_fg_cb fg;
     void* user;
+    int qp;                         // 1: 1/2 x^T D M D x (+ c, delta); M n x n symmetric
 };
 
 namespace {
@@ -315,6 +316,14 @@ extern "C" lbfgsb_err lbfgsb_objective_lsq(const double* M, int64_t m, int64_t n
     return LBFGSB_OK;
 }
 
+extern "C" lbfgsb_err lbfgsb_objective_qp(const double* Q, int64_t n, int64_t ld, const double* colscale,
+                                          const double* c, double delta, lbfgsb_objective** out)
+{
+    TRY(lbfgsb_objective_lsq(Q, n, n, ld, colscale, 0, nullptr, c, delta, out));
+    (*out)->qp = 1;
+    return LBFGSB_OK;
+}
+
 extern "C" lbfgsb_err lbfgsb_objective_callback(lbfgsb_fg_cb fg, void* user, lbfgsb_objective** out)
 {
     if (!out) return fail(LBFGSB_ERR_ARG, "out is NULL");
@@ -375,6 +384,8 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
                         (long long)h->n);
         P.m = ob->m; P.ncols = ob->ncols; P.ld = ob->ld; P.M = ob->M;
         P.colscale = ob->colscale; P.split = ob->split; P.b = ob->b; P.c = ob->c; P.delta = ob->delta;
+        P.qp = ob->qp;
+        if (P.qp && h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "QP objectives are single-GPU");
         gemv_geometry(P);
         const size_t mb = sizeof(double) * (size_t)P.m;
         TRY(h->r0.ensure(mb)); TRY(h->r1.ensure(mb)); TRY(h->q.ensure(mb));
@@ -1070,7 +1081,7 @@ extern "C" lbfgsb_err lbfgsb_op_gemv(const lbfgsb_objective* obj, const double* 
     Prob P;
     std::memset(&P, 0, sizeof P);
     P.m = obj->m; P.ncols = obj->ncols; P.ld = obj->ld; P.M = obj->M;
-    P.colscale = obj->colscale; P.split = obj->split;
+    P.colscale = obj->colscale; P.split = obj->split; P.qp = obj->qp;
     P.n = obj->split ? 2 * obj->ncols : obj->ncols;
     gemv_geometry(P);
     double* qpart = nullptr;
@@ -1089,10 +1100,24 @@ extern "C" lbfgsb_err lbfgsb_op_gemv(const lbfgsb_objective* obj, const double* 
     return LBFGSB_OK;
 }
 
+extern "C" lbfgsb_err lbfgsb_op_gaussian_kernel(const double* X, int64_t N, int64_t d, double gamma,
+                                                double* K, int64_t ldk, void* cuda_stream)
+{
+    if (!X || !K || N <= 0 || d <= 0 || ldk < N || !(gamma > 0)) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LBFGSB_ERR_CUDA, "no device");
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    launch_gauss(X, N, d, gamma, K, ldk, st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return LBFGSB_OK;
+}
+
 extern "C" lbfgsb_err lbfgsb_op_gemvt(const lbfgsb_objective* obj, const double* r, double* g,
                                       void* cuda_stream)
 {
     if (!obj || obj->kind != 0 || !r || !g) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    if (obj->qp) return lbfgsb_op_gemv(obj, r, g, cuda_stream);   // Q~ is symmetric
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LBFGSB_ERR_CUDA, "no device");
     init_kernels();
@@ -1151,6 +1176,7 @@ extern "C" lbfgsb_err lbfgsb_op_trials(lbfgsb_t* h, const lbfgsb_objective* obj,
     if (!h || !obj || obj->kind != 0 || !r || !q || !x || !p || !f_out)
         return fail(LBFGSB_ERR_ARG, "bad arguments");
     if (ntrials < 1 || ntrials > KT) return fail(LBFGSB_ERR_ARG, "ntrials in [1, %d]", KT);
+    if (obj->qp) return fail(LBFGSB_ERR_UNSUPPORTED, "op_trials is for LSQ objectives");
     Prob P;
     TRY(make_prob(h, obj, P));
     set_sep(P);
