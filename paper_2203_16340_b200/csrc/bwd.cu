@@ -207,18 +207,15 @@ __device__ __forceinline__ void epi_init(const Prob& P, const Ctrl* C, int mode,
 }
 
 // Per-CTA Gram partial -> 2-level deterministic tail -> Alg. 3 (thread 0).
-__device__ void gram_tail(const Prob& P, Ctrl* C, const EpiCtx& E, const double* gacc, double gmax,
-                          double cnt, double* red, double* buf, int bufn, double* stash, double* Gs)
+__device__ void gram_tail(const Prob& P, Ctrl* C, const EpiCtx& E, const GramEnt& ent, const double* gacc,
+                          double gmax, double cnt, double* red, double* buf, int bufn, double* stash,
+                          double* Gs)
 {
     const int G = gridDim.x, cta = blockIdx.x;
     const int nh = E.nh, nb = E.nb, ne = nb * (nb + 1) / 2;
     const int ntot = ne + (P.screen_full ? nh : 0);
     double* out = P.gram_part + (int64_t)cta * GRAM_STRIDE;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int e = threadIdx.x + k * (int)blockDim.x;
-        if (e < ntot) out[e] = gacc[k];
-    }
+    ent.finalize(gacc, stash, out, ntot);
     const double bm = block_reduce<1>(gmax, red);
     const double bc = block_reduce<0>(cnt, red);
     if (threadIdx.x == 0) { out[ntot] = bm; out[ntot + 1] = bc; }
@@ -359,7 +356,7 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
         __syncthreads();
     }
     if (!E.gram) return;
-    gram_tail(P, C, E, gacc, gmax, cnt, red, rs, (int)(mpad < 4096 ? mpad : 4096), stash, Gs);
+    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, rs, (int)(mpad < 4096 ? mpad : 4096), stash, Gs);
 }
 
 // ---------------------------------------------------------------- k_bwd_w (short columns)
@@ -497,7 +494,7 @@ __global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double*
         }
     }
     if (!epi || !E.gram) return;
-    gram_tail(P, C, E, gacc, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
+    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
 }
 
 // ---------------------------------------------------------------- k_bwd_c (TMA, CTA pairs)
@@ -730,7 +727,7 @@ k_bwd_c(Prob P, int mode, const double* rvec, double* gout, int hmax, int cmax)
         __syncthreads();
     }
     if (!E.gram) return;
-    gram_tail(P, C, E, gacc, gmax, cnt, red, stage, 4096, stash, Gs);
+    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, stage, 4096, stash, Gs);
 }
 
 // smem k_bwd_c needs (0 = does not fit / not applicable)
@@ -796,7 +793,7 @@ __global__ void __launch_bounds__(NT) k_qpu(Prob P, int mode, int bufn)
         }
     }
     if (!E.gram) return;
-    gram_tail(P, C, E, gacc, gmax, cnt, red, smq, bufn, stash, Gs);
+    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, smq, bufn, stash, Gs);
 }
 
 // ---------------------------------------------------------------- k_bwd (generic)
@@ -868,7 +865,7 @@ __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* r
         __syncthreads();
     }
     if (mode == BWD_PLAIN || !E.gram) return;
-    gram_tail(P, C, E, gacc, gmax, cnt, red, buf, BWD_BUF, stash, Gs);
+    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, buf, BWD_BUF, stash, Gs);
 }
 
 // ---------------------------------------------------------------- launch

@@ -163,27 +163,42 @@ __device__ __forceinline__ int ring_slot(int head, int nh, int i, int mh)
     return ((head - (nh - 1) + i) % mh + mh) % mh;
 }
 
-// Entries of the per-CTA Gram partial a thread accumulates (<= 3 per thread,
-// entry e = threadIdx.x + k * blockDim.x).
+// Entries of the per-CTA Gram partial.  When the entries are few (m_h small)
+// R = 2..8 threads share an entry and each sums every R-th tile row (fixed
+// assignment); otherwise a thread owns up to 3 entries (e = tid + k blockDim).
+// finalize() combines the R partials of an entry in ascending j and writes
+// the CTA's partial: deterministic either way.
 struct GramEnt {
     int a[3], b[3];
     bool full[3];
-    __device__ void init(int nb, int ne, int ntot, int nh)
+    int R, j;
+    __device__ void set_entry(int k, int e, int nb, int ne, int ntot, int nh)
     {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const int e = threadIdx.x + k * (int)blockDim.x;
-            a[k] = -1; b[k] = -1; full[k] = false;
-            if (e < ne) {
-                int aa = 0, rem = e;
-                while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
-                a[k] = aa; b[k] = aa + rem;
-            } else if (e < ntot) {
-                a[k] = b[k] = nh + (e - ne); full[k] = true;
-            }
+        a[k] = -1; b[k] = -1; full[k] = false;
+        if (e < ne) {
+            int aa = 0, rem = e;
+            while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
+            a[k] = aa; b[k] = aa + rem;
+        } else if (e < ntot) {
+            a[k] = b[k] = nh + (e - ne); full[k] = true;
         }
     }
-    // acc[k] += sum over tile rows (in row order) of mask * B_a * B_b
+    __device__ void init(int nb, int ne, int ntot, int nh)
+    {
+        R = 1;
+        while (R < 8 && R * 2 * ntot <= (int)blockDim.x) R *= 2;
+        if (R > 1) {
+            j = threadIdx.x % R;
+            set_entry(0, threadIdx.x / R, nb, ne, ntot, nh);
+            a[1] = a[2] = b[1] = b[2] = -1;
+            full[1] = full[2] = false;
+        } else {
+            j = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) set_entry(k, threadIdx.x + k * (int)blockDim.x, nb, ne, ntot, nh);
+        }
+    }
+    // acc[k] += sum over this thread's tile rows (in row order) of mask * B_a * B_b
     __device__ void accumulate(const double* tile, const double* mk, int rows, int nb, double* acc) const
     {
 #pragma unroll
@@ -192,13 +207,35 @@ struct GramEnt {
             const int aa = a[k], bb = b[k];
             double s = 0.0;
             if (!full[k]) {
-                for (int r = 0; r < rows; ++r)
+                for (int r = j; r < rows; r += R)
                     if (mk[r] != 0.0) s = fma(tile[r * nb + aa], tile[r * nb + bb], s);
             } else {
-                for (int r = 0; r < rows; ++r) s = fma(tile[r * nb + aa], tile[r * nb + aa], s);
+                for (int r = j; r < rows; r += R) s = fma(tile[r * nb + aa], tile[r * nb + aa], s);
             }
             acc[k] += s;
         }
+    }
+    // write this CTA's partial entries out[0 .. ntot); sh: >= blockDim doubles (smem)
+    __device__ void finalize(const double* acc, double* sh, double* out, int ntot) const
+    {
+        if (R == 1) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int e = threadIdx.x + k * (int)blockDim.x;
+                if (e < ntot) out[e] = acc[k];
+            }
+            return;
+        }
+        __syncthreads();
+        sh[threadIdx.x] = a[0] >= 0 ? acc[0] : 0.0;
+        __syncthreads();
+        const int e = threadIdx.x / R;
+        if (j == 0 && e < ntot) {
+            double s = sh[threadIdx.x];
+            for (int jj = 1; jj < R; ++jj) s += sh[threadIdx.x + jj];
+            out[e] = s;
+        }
+        __syncthreads();
     }
 };
 

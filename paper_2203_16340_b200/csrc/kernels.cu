@@ -551,11 +551,7 @@ __global__ void __launch_bounds__(NT) k_gram_recur(Prob P, int op_mode)
         __syncthreads();
     }
     double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int e = threadIdx.x + k * NT;
-        if (e < ntot) out[e] = acc[k];
-    }
+    ent.finalize(acc, stash, out, ntot);
     const double bm = block_reduce<1>(gmax, red);
     const double bc = block_reduce<0>(cnt, red);
     if (threadIdx.x == 0) { out[ntot] = bm; out[ntot + 1] = bc; }

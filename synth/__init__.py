@@ -203,13 +203,16 @@ def c5_device(m: int = 100000, n: int = 200000, seed: int = 5, col0: int = 0, nc
     return At.T, b, xp
 
 
-def blobs(N: int, d: int, seed: int, sep: float = 2.0):
-    """Two Gaussian blobs, labels +-1 balanced: x_i ~ N(y_i sep/sqrt(d) 1, I_d).
-    Returns (X (N, d) row-major, y (N,))."""
+def blobs(N: int, d: int, seed: int, sep: float = 2.0, scale: float = 1.0):
+    """Two Gaussian blobs, labels +-1 balanced: x_i ~ scale * N(y_i sep/sqrt(d) 1, I_d).
+    scale = 1/sqrt(d) gives ||x_i - x_j||^2 ~ 2 (LibSVM-like feature scaling, so a
+    gamma = 1 Gaussian kernel is far from the identity).  Returns (X (N, d), y (N,))."""
     rng = np.random.default_rng(seed)
     y = np.where(np.arange(N) % 2 == 0, 1.0, -1.0)
     rng.shuffle(y)
     X = rng.standard_normal((N, d)) + (y * (sep / np.sqrt(d)))[:, None]
+    if scale != 1.0:
+        X *= scale
     return X, y
 
 
