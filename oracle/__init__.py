@@ -63,7 +63,7 @@ class _Opts(C.Structure):
     _fields_ = [("eps", C.c_double), ("c1", C.c_double), ("shrink", C.c_double),
                 ("tol", C.c_double), ("max_backtracks", C.c_int32),
                 ("screen_full_norm", C.c_int32), ("no_projection", C.c_int32),
-                ("max_iters", C.c_int64)]
+                ("armijo_diff", C.c_int32), ("max_iters", C.c_int64)]
 
 
 class _Res(C.Structure):
@@ -106,6 +106,8 @@ def _setup(L):
     L.orc_lsq_value.argtypes = [C.POINTER(_Lsq), _dp]
     L.orc_lsq_value.restype = d
     L.orc_lsq_grad.argtypes = [C.POINTER(_Lsq), _dp, _dp]
+    L.orc_armijo_delta.argtypes = [C.POINTER(_Lsq), i64, _dp, _dp, _dp, _dp, d]
+    L.orc_armijo_delta.restype = d
     L.orc_armijo_scalar_quadratic.argtypes = [d, d, d, d, d, i32]
     L.orc_armijo_scalar_quadratic.restype = d
 
@@ -223,6 +225,7 @@ class Options:
     screen_full_norm: bool = False  # R3
     max_iters: int = 10000
     no_projection: bool = False     # PAPER.md:201 variant
+    armijo_diff: bool = False       # R29: Armijo on the expanded difference (N4)
 
 
 @dataclass
@@ -288,6 +291,31 @@ class LSQ:
         _L().orc_lsq_grad(C.byref(s), _ptr(x), _ptr(g))
         return g
 
+    def apply(self, v):
+        """M~ v (QP: Q~ v = D M D v), plain numpy."""
+        v = _f64(v)
+        if self.split:
+            v = v[:self.ncols] - v[self.ncols:]
+        if self.colscale is not None:
+            v = self.colscale * v
+        out = self.M @ v
+        if self.qp and self.colscale is not None:
+            out = self.colscale * out
+        return out
+
+    def armijo_delta(self, x, p, alpha):
+        """f(x + alpha p) - f(x) by the expanded form of reading R29
+        (orc_armijo_delta), with the carried r (LSQ: M~x - b, QP: w = Q~x) and
+        q = M~p formed here."""
+        x = _f64(x); p = _f64(p)
+        r = self.apply(x)
+        if not self.qp and self.b is not None:
+            r = r - self.b
+        q = self.apply(p)
+        s = self._struct()
+        return _L().orc_armijo_delta(C.byref(s), self.nvars, _ptr(x), _ptr(_f64(r)), _ptr(_f64(q)),
+                                     _ptr(p), float(alpha))
+
 
 @dataclass
 class Result:
@@ -311,7 +339,7 @@ def minimize_lsq(P: LSQ, l=None, u=None, x0=None, m_hist=5, opts: Options | None
     l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
     u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               int(o.no_projection), o.max_iters)
+               int(o.no_projection), int(o.armijo_diff), o.max_iters)
     res = _Res()
     s = P._struct()
     _L().orc_minimize_lsq(C.byref(s), _ptr(l), _ptr(u), m_hist, C.byref(so), _ptr(x),
@@ -342,7 +370,7 @@ def al_solve(P: LSQ, l=None, u=None, m_hist=5, opts: Options | None = None,
     u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
     lam = np.zeros(max(P.n_eq, 1)); mu = np.zeros(max(P.n_in, 1))
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               int(o.no_projection), o.max_iters)
+               int(o.no_projection), int(o.armijo_diff), o.max_iters)
     sa = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer)
     s = P._struct()
     res = _AlRes()

@@ -356,6 +356,7 @@ typedef struct {
     double eps, c1, shrink, tol;
     int32_t max_backtracks, screen_full_norm;
     int32_t no_projection;       /* 1: Alg. 2 without the projected branch */
+    int32_t armijo_diff;         /* 1: Armijo test on the expanded difference f_t - f (R29) */
     int64_t max_iters;
 } orc_opts;
 
@@ -368,6 +369,43 @@ typedef struct {
 
 enum { ORC_CONVERGED = 0, ORC_MAX_ITERS = 1, ORC_LINESEARCH_FAILURE = 2,
        ORC_AL_MAX_OUTER = 3, ORC_AL_INNER_FAILURE = 4 };
+
+/* Difference form of the Armijo test (reading R29): for the
+ * quadratic-plus-separable objective the change along the segment x + alpha p
+ * is, exactly,
+ *   f(x + alpha p) - f(x) = alpha (r^T q + c^T p + delta x^T p)
+ *                         + alpha^2/2 (q^T q + delta p^T p) + sum_k dphi_k
+ * (QP: r^T q -> p^T w, q^T q -> p^T q), with the AL term of constraint k,
+ * t0 = h_k(x) + lam_k/rho, a = E_k^T p, t1 = t0 + alpha a,
+ *   dphi_k = rho/2 (t1^2 - t0^2) = rho alpha a (t0 + alpha a / 2)
+ * (inequalities: rho/2 ((t1)_+^2 - (t0)_+^2), the same product when both
+ * are positive).  Evaluated directly, without forming f(x + alpha p). */
+double orc_armijo_delta(const orc_lsq* P, int64_t nv, const double* x, const double* r,
+                        const double* q, const double* p, double alpha)
+{
+    const double rq = P->qp ? dotv(nv, p, r) : dotv(P->m, r, q);
+    const double qq = P->qp ? dotv(nv, p, q) : dotv(P->m, q, q);
+    const double cp = P->c ? dotv(nv, P->c, p) : 0.0;
+    const double xp = dotv(nv, x, p), pp = dotv(nv, p, p);
+    double dl = alpha * (rq + cp + P->delta * xp) + 0.5 * alpha * alpha * (qq + P->delta * pp);
+    double hval[64], gval[64];
+    lsq_cons(P, x, hval, gval);
+    for (int32_t k = 0; k < P->n_eq + P->n_in; ++k) {
+        const int eq = k < P->n_eq;
+        const int32_t kk = eq ? k : k - P->n_eq;
+        const double* col = eq ? P->E + (int64_t)kk * nv : P->G + (int64_t)kk * nv;
+        const double a = dotv(nv, col, p);
+        const double t0 = eq ? hval[kk] + P->lam[kk] / P->rho : gval[kk] + P->mu[kk] / P->rho;
+        const double t1 = t0 + alpha * a;
+        if (eq || (t0 > 0.0 && t1 > 0.0)) {
+            dl += P->rho * alpha * a * (t0 + 0.5 * alpha * a);
+        } else {
+            const double p0 = t0 > 0.0 ? t0 : 0.0, p1 = t1 > 0.0 ? t1 : 0.0;
+            dl += 0.5 * P->rho * (p1 * p1 - p0 * p0);
+        }
+    }
+    return dl;
+}
 
 /* Armijo backtracking on the incremental residual (R10, R11, R13):
  * alpha_0 = min(1, amax), alpha_t = shrink * alpha_{t-1};
@@ -388,10 +426,19 @@ static int armijo_lsq(const orc_lsq* P, const orc_opts* o, int64_t nv, const dou
         if (t > 0) alpha = o->shrink * alpha;
         for (int64_t j = 0; j < nv; ++j) x_t[j] = clip1(fma(alpha, p[j], x[j]), l, u, j);
         for (int64_t i = 0; i < P->m; ++i) r_t[i] = fma(alpha, q[i], r[i]);
+        *n_fg += 1;
+        if (o->armijo_diff) {                                     /* R29 */
+            const double dl = orc_armijo_delta(P, nv, x, r, q, p, alpha);
+            if (dl <= o->c1 * alpha * gp) {
+                *f_out = f + dl; *alpha_out = alpha;
+                return 1;
+            }
+            *n_bt += 1;
+            continue;
+        }
         const double quad = P->qp ? 0.5 * xw + alpha * pw + 0.5 * alpha * alpha * pq
                                   : half_sq(P->m, r_t);
         const double ft = quad + lsq_phi(P, x_t, NULL, NULL);
-        *n_fg += 1;
         if (ft <= f + o->c1 * alpha * gp) {
             *f_out = ft; *alpha_out = alpha;
             return 1;
