@@ -88,6 +88,9 @@ typedef struct {
     int32_t profile;            /* 1: CUDA events around the two GEMV launches (ops.h)  */
     int32_t no_projection;      /* 1: skip Alg. 2's projected branch, always truncate
                                    (the proof-only variant of PAPER.md:201); default 0 */
+    int32_t armijo_diff;        /* 1: Armijo test on the exact expansion of f(x+a p) - f(x)
+                                   (LSQ / QP objectives; reading R29, avoids the
+                                   cancellation floor of f_t <= f + c1 a g^T p); default 0 */
     int64_t max_iters;          /* default 10000                                        */
 } lbfgsb_opts;
 

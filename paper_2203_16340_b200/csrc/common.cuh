@@ -320,6 +320,11 @@ __device__ __forceinline__ double trial_value(const Prob& P, const Ctrl* C, doub
 //        1/2 (x + alpha p)^T Q~ (x + alpha p) with the carried w = Q~ x)
 __device__ __forceinline__ void quad_values(const Prob& P, const Ctrl* C, const double* S, double* quad)
 {
+    if (P.diff) {                                               // R29: linear / quadratic coefficients
+        quad[0] = P.qp ? C->qp_pw : S[0];
+        quad[1] = P.qp ? C->qp_pq : S[1];
+        return;
+    }
     double a = C->alpha0;
     for (int t = 0; t < KT; ++t) {
         if (t > 0) a = a * P.shrink;
@@ -329,8 +334,71 @@ __device__ __forceinline__ void quad_values(const Prob& P, const Ctrl* C, const 
 
 // Armijo decision over one batch of KT trials (R10, R11, R13); single thread.
 // S[t] = sum (r + alpha_t q)^2, sep[t*NSEP + s] the separable sums.
+__device__ __forceinline__ void accept_step(const Prob& P, Ctrl* C, int t)
+{
+    C->n_fg += t + 1;
+    C->n_bt += t;
+    const int head = (C->head + 1) % P.mh;                      // store pair
+    C->head = head;
+    C->slot = head;
+    C->nh = C->nh + 1 < P.mh ? C->nh + 1 : P.mh;
+    C->k += 1;
+    C->fallback = 0;
+}
+
+// Difference form of the Armijo test (reading R29): with L, Q the linear and
+// quadratic coefficients of the smooth part along p (quad[0], quad[1]) and the
+// separable sums sep = (c^T p, x^T p, E_k^T p | -, p^T p),
+//   Delta(a) = a (L + c^T p + delta x^T p) + a^2/2 (Q + delta p^T p) + sum_k dphi_k(a),
+// accepted when Delta(a) <= c1 a g^T p; all max_bt + 1 trials in one pass.
+__device__ __forceinline__ void armijo_decide_diff(const Prob& P, Ctrl* C, const double* quad,
+                                                   const double* sep)
+{
+    const int ncons = P.n_eq + P.n_in;
+    const double cp = sep ? sep[0] : 0.0, xp = sep ? sep[1] : 0.0, pp = sep ? sep[NSEP + 1] : 0.0;
+    const double lin = quad[0] + cp + P.delta * xp;
+    const double qua = quad[1] + P.delta * pp;
+    double a = C->alpha0;
+    for (int t = 0; t <= P.max_bt; ++t) {
+        if (t > 0) a = a * P.shrink;
+        double dl = a * lin + 0.5 * a * a * qua;
+        for (int k = 0; k < ncons; ++k) {
+            const double ak = sep[2 + k];
+            const double t0 = C->hval[k] + C->lam[k] / C->rho, t1 = t0 + a * ak;
+            if (k < P.n_eq || (t0 > 0.0 && t1 > 0.0)) {
+                dl += C->rho * a * ak * (t0 + 0.5 * a * ak);
+            } else {
+                const double p0 = t0 > 0.0 ? t0 : 0.0, p1 = t1 > 0.0 ? t1 : 0.0;
+                dl += 0.5 * C->rho * (p1 * p1 - p0 * p0);
+            }
+        }
+        if (dl <= P.c1 * a * C->gp) {
+            C->alpha = a;
+            C->f = C->f + dl;
+            C->f_new = C->f;
+            for (int k = 0; k < ncons; ++k) {
+                const double hv = C->hval[k] + a * sep[2 + k];
+                C->hval[k] = hv;
+                if (k < P.n_eq) {
+                    C->ccoef[k] = C->rho * hv + C->lam[k];
+                } else {
+                    double tt = hv + C->lam[k] / C->rho;
+                    C->ccoef[k] = C->rho * (tt > 0.0 ? tt : 0.0);
+                }
+            }
+            accept_step(P, C, t);
+            return;
+        }
+    }
+    C->n_fg += P.max_bt + 1;
+    C->n_bt += P.max_bt + 1;
+    if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }
+    else C->stall = ST_FALLBACK;
+}
+
 __device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const double* quad, const double* sep)
 {
+    if (P.diff) { armijo_decide_diff(P, C, quad, sep); return; }
     double cc[MAXC], hv[MAXC];
     const int ncons = P.n_eq + P.n_in;
     double a = C->alpha0;
@@ -345,14 +413,7 @@ __device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const doub
             C->f_new = ft;
             C->f = ft;
             for (int k = 0; k < ncons; ++k) { C->ccoef[k] = cc[k]; C->hval[k] = hv[k]; }
-            C->n_fg += t + 1;
-            C->n_bt += t;
-            const int head = (C->head + 1) % P.mh;              // store pair
-            C->head = head;
-            C->slot = head;
-            C->nh = C->nh + 1 < P.mh ? C->nh + 1 : P.mh;
-            C->k += 1;
-            C->fallback = 0;
+            accept_step(P, C, t);
             return;
         }
     }

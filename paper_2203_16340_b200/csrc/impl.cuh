@@ -92,6 +92,7 @@ struct Prob {
     double eps, c1, shrink;
     int max_bt, screen_full, mh;
     int no_projection;      // Alg. 2 without the projected branch
+    int diff;               // Armijo on the expanded difference (R29): trial sums -> r^T q, q^T q, c^T p ...
     int qp;                 // 1: f = 1/2 x^T D M D x + ... (M n x n symmetric); rbuf holds w = Q~ x
     long long max_iters;
     // workspace

@@ -142,12 +142,15 @@ __global__ void __launch_bounds__(NT) k_sep(Prob P, int mode, const double* pvec
     if ((mode == SEP_ITER || mode == SEP_NEXT) && halted(C)) return;
     __shared__ double wsum[NT / 32][4 * NSEP];
     double al[KT];
-    const int ntr = mode == SEP_SETUP ? 1 : KT;
+    const int ntr_std = mode == SEP_SETUP ? 1 : KT;
     al[0] = mode == SEP_SETUP ? 0.0 : C->alpha0;
 #pragma unroll
     for (int t = 1; t < KT; ++t) al[t] = al[t - 1] * P.shrink;
     const double* pv = (mode == SEP_ITER || mode == SEP_NEXT) ? (C->branch ? P.pp : P.pt) : pvec;
     const int ncons = P.n_eq + P.n_in;
+    // R29 difference form: slot 0 = (c^T p, x^T p, E_k^T p), slot 1 = (-, p^T p, -)
+    const bool dsum = P.diff && mode == SEP_ITER;
+    const int ntr = dsum ? 2 : ntr_std;
     for (int t0 = 0; t0 < ntr; t0 += 4) {
         double a[4][NSEP];
 #pragma unroll
@@ -160,6 +163,15 @@ __global__ void __launch_bounds__(NT) k_sep(Prob P, int mode, const double* pvec
             double ev[MAXC];
 #pragma unroll
             for (int k = 0; k < MAXC; ++k) ev[k] = k < ncons ? P.Ecol[k][j] : 0.0;
+            if (dsum) {
+                if (P.c) a[0][0] += cj * pj;
+                a[0][1] += xj * pj;
+                a[1][1] += pj * pj;
+#pragma unroll
+                for (int k = 0; k < MAXC; ++k)
+                    if (k < ncons) a[0][2 + k] += ev[k] * pj;
+                continue;
+            }
 #pragma unroll
             for (int tt = 0; tt < 4; ++tt) {
                 const double xt = clipd(fma(al[t0 + tt], pj, xj), lj, uj);
@@ -378,6 +390,15 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
         if (r0ok) { const double r0 = P.b ? q0 - P.b[row] : q0; rcur[row] = r0; s += r0 * r0; }
         if (r1ok) { const double r1 = P.b ? q1 - P.b[row + 1] : q1; rcur[row + 1] = r1; s += r1 * r1; }
         acc[0] = s;
+    } else if (P.diff) {
+        // R29: S[0] = r^T q, S[1] = q^T q
+        if (r0ok) P.q[row] = q0;
+        if (r1ok) P.q[row + 1] = q1;
+        const double ri0 = r0ok ? rcur[row] : 0.0, ri1 = r1ok ? rcur[row + 1] : 0.0;
+        acc[0] = (r0ok ? ri0 * q0 : 0.0) + (r1ok ? ri1 * q1 : 0.0);
+        acc[1] = (r0ok ? q0 * q0 : 0.0) + (r1ok ? q1 * q1 : 0.0);
+#pragma unroll
+        for (int t = 2; t < KT; ++t) acc[t] = 0.0;
     } else {
         if (r0ok) P.q[row] = q0;
         if (r1ok) P.q[row + 1] = q1;
@@ -428,7 +449,6 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
 {
     Ctrl* C = P.ctrl;
     if (mode != LS_OP && halted(C)) return;
-    __shared__ double red[NT / 32];
     __shared__ double buf[1024];
     __shared__ double stash[NT];
     __shared__ double Ssum[KT];
@@ -459,6 +479,11 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
         }
         if (mode == LS_SH_ITER) P.q[i] = qi;
         const double ri = r[i];
+        if (P.diff && mode == LS_SH_ITER) {                     // R29: r^T q, q^T q
+            acc[0] += ri * qi;
+            acc[1] += qi * qi;
+            continue;
+        }
         double al = C->alpha0;
 #pragma unroll
         for (int t = 0; t < KT; ++t) {

@@ -385,6 +385,7 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
         P.m = ob->m; P.ncols = ob->ncols; P.ld = ob->ld; P.M = ob->M;
         P.colscale = ob->colscale; P.split = ob->split; P.b = ob->b; P.c = ob->c; P.delta = ob->delta;
         P.qp = ob->qp;
+        P.diff = h->o.armijo_diff ? 1 : 0;                  // R29 (LSQ / QP objectives only)
         if (P.qp && h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "QP objectives are single-GPU");
         gemv_geometry(P);
         const size_t mb = sizeof(double) * (size_t)P.m;
