@@ -56,7 +56,8 @@ class _Lsq(C.Structure):
                 ("b", _dp), ("c", _dp), ("delta", C.c_double),
                 ("n_eq", C.c_int32), ("E", _dp), ("e", _dp), ("lam", _dp),
                 ("n_in", C.c_int32), ("G", _dp), ("hv", _dp), ("mu", _dp),
-                ("rho", C.c_double), ("qp", C.c_int32)]
+                ("rho", C.c_double), ("qp", C.c_int32), ("ent", C.c_double),
+                ("tm", C.c_int64)]
 
 
 class _Opts(C.Structure):
@@ -106,7 +107,7 @@ def _setup(L):
     L.orc_lsq_value.argtypes = [C.POINTER(_Lsq), _dp]
     L.orc_lsq_value.restype = d
     L.orc_lsq_grad.argtypes = [C.POINTER(_Lsq), _dp, _dp]
-    L.orc_armijo_delta.argtypes = [C.POINTER(_Lsq), i64, _dp, _dp, _dp, _dp, d]
+    L.orc_armijo_delta.argtypes = [C.POINTER(_Lsq), i64, _dp, _dp, _dp, _dp, _dp, _dp, d]
     L.orc_armijo_delta.restype = d
     L.orc_armijo_scalar_quadratic.argtypes = [d, d, d, d, d, i32]
     L.orc_armijo_scalar_quadratic.restype = d
@@ -246,7 +247,7 @@ class LSQ:
     """
 
     def __init__(self, M, b=None, c=None, delta=0.0, colscale=None, split=False,
-                 E=None, e=None, G=None, hv=None, qp=False):
+                 E=None, e=None, G=None, hv=None, qp=False, ent=0.0, tm=0):
         self.M = np.asfortranarray(M, dtype=np.float64)
         self.m, self.ncols = self.M.shape
         self.qp = bool(qp)           # 1/2 x^T D M D x (+ c, delta, AL); M square symmetric
@@ -262,12 +263,34 @@ class LSQ:
         self.e = None if e is None else _f64(np.atleast_1d(e))
         self.G = None if G is None else np.asfortranarray(np.reshape(G, (self.nvars, -1)), dtype=np.float64)
         self.hv = None if hv is None else _f64(np.atleast_1d(hv))
-        self.n_eq = 0 if self.E is None else self.E.shape[1]
+        self.ent = float(ent)         # + ent * sum x log x (SURVEY N2 entropy regulariser)
+        self.tm = int(tm)             # > 0: equality constraints = marginals of P (tm x nvars/tm)
+        if self.tm > 0:
+            assert self.E is None and self.nvars % self.tm == 0 and self.e is not None
+            self.n_eq = self.tm + self.nvars // self.tm
+            assert len(self.e) == self.n_eq
+        else:
+            self.n_eq = 0 if self.E is None else self.E.shape[1]
         self.n_in = 0 if self.G is None else self.G.shape[1]
         self.lam = np.zeros(max(self.n_eq, 1))
         self.mu = np.zeros(max(self.n_in, 1))
         self.rho = 1.0
-        assert self.n_eq <= 64 and self.n_in <= 64
+
+    @classmethod
+    def transport(cls, cost, u, v, reg="entropy", lam=0.5):
+        """Joint probability / regularised OT:
+        min <cost, P> + lam r(P)  s.t. P 1 = u, P^T 1 = v, P >= 0, with
+        r = sum P log P (reg="entropy") or 1/2 ||P||_F^2 (reg="gaussian").
+        Variables x = vec(P) column-major (m*n); no quadratic data term."""
+        cost = np.asarray(cost, dtype=np.float64)
+        m, n = cost.shape
+        c = cost.reshape(-1, order="F")
+        e = np.concatenate([_f64(u), _f64(v)])
+        if reg == "entropy":
+            return cls(np.zeros((0, m * n)), c=c, ent=lam, tm=m, e=e)
+        if reg == "gaussian":
+            return cls(np.zeros((0, m * n)), c=c, delta=lam, tm=m, e=e)
+        raise ValueError(reg)
 
     def _struct(self):
         s = _Lsq()
@@ -280,6 +303,8 @@ class LSQ:
         s.n_in = self.n_in; s.G = _ptr(self.G); s.hv = _ptr(self.hv); s.mu = _ptr(self.mu)
         s.rho = self.rho
         s.qp = int(self.qp)
+        s.ent = self.ent
+        s.tm = self.tm
         return s
 
     def value(self, x):
@@ -303,7 +328,7 @@ class LSQ:
             out = self.colscale * out
         return out
 
-    def armijo_delta(self, x, p, alpha):
+    def armijo_delta(self, x, p, alpha, l=None, u=None):
         """f(x + alpha p) - f(x) by the expanded form of reading R29
         (orc_armijo_delta), with the carried r (LSQ: M~x - b, QP: w = Q~x) and
         q = M~p formed here."""
@@ -313,8 +338,10 @@ class LSQ:
             r = r - self.b
         q = self.apply(p)
         s = self._struct()
+        lb = None if l is None else _f64(np.broadcast_to(l, (self.nvars,)))
+        ub = None if u is None else _f64(np.broadcast_to(u, (self.nvars,)))
         return _L().orc_armijo_delta(C.byref(s), self.nvars, _ptr(x), _ptr(_f64(r)), _ptr(_f64(q)),
-                                     _ptr(p), float(alpha))
+                                     _ptr(p), _ptr(lb), _ptr(ub), float(alpha))
 
 
 @dataclass

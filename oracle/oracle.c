@@ -227,6 +227,12 @@ typedef struct {
     double rho;
     int32_t qp;                  /* 1: quadratic objective 1/2 x^T Q~ x, Q~ = D M D (M n x n
                                     symmetric, D = diag(colscale)); "r" holds w = Q~ x */
+    double ent;                  /* entropy weight: + ent * sum_j x_j log x_j (0 log 0 = 0;
+                                    the joint-probability regulariser) */
+    int64_t tm;                  /* > 0: the n_eq equality constraints are the marginals of
+                                    x = vec(P), P tm x (nvars/tm) column-major:
+                                    h_i = sum_j P_ij - e_i (i < tm), h_{tm+j} = sum_i P_ij -
+                                    e_{tm+j}; E unused */
 } orc_lsq;
 
 static int64_t lsq_nvars(const orc_lsq* P) { return P->split ? 2 * P->ncols : P->ncols; }
@@ -255,11 +261,30 @@ static void lsq_residual(const orc_lsq* P, const double* x, double* r)
         for (int64_t i = 0; i < P->m; ++i) r[i] = r[i] - P->b[i];
 }
 
+/* scratch for per-constraint values (n_eq or n_in doubles, at least one) */
+static double* cons_buf(int32_t k) { return (double*)calloc((size_t)(k > 0 ? k : 1), sizeof(double)); }
+
+/* x log x with 0 log 0 = 0 */
+static double xlogx(double x) { return x > 0.0 ? x * log(x) : 0.0; }
+
 /* constraint values at x */
 static void lsq_cons(const orc_lsq* P, const double* x, double* hval, double* gval)
 {
     const int64_t nv = lsq_nvars(P);
-    for (int32_t k = 0; k < P->n_eq; ++k) {
+    if (P->tm > 0 && P->n_eq > 0) {                    /* marginals P 1 = u, P^T 1 = v */
+        const int64_t tm = P->tm, tn = nv / tm;
+        for (int64_t i = 0; i < tm; ++i) {
+            double s = 0.0;
+            for (int64_t j = 0; j < tn; ++j) s += x[i + j * tm];
+            hval[i] = s - P->e[i];
+        }
+        for (int64_t j = 0; j < tn; ++j) {
+            double s = 0.0;
+            for (int64_t i = 0; i < tm; ++i) s += x[i + j * tm];
+            hval[tm + j] = s - P->e[tm + j];
+        }
+    }
+    for (int32_t k = 0; k < (P->tm > 0 ? 0 : P->n_eq); ++k) {
         double s = 0.0;
         const double* Ek = P->E + (int64_t)k * nv;
         for (int64_t j = 0; j < nv; ++j) s += Ek[j] * x[j];
@@ -278,13 +303,15 @@ static void lsq_cons(const orc_lsq* P, const double* x, double* hval, double* gv
 static double lsq_phi(const orc_lsq* P, const double* x, double* coef_eq, double* coef_in)
 {
     const int64_t nv = lsq_nvars(P);
-    double cx = 0.0, xx = 0.0;
+    double cx = 0.0, xx = 0.0, xl = 0.0;
     for (int64_t j = 0; j < nv; ++j) {
         if (P->c) cx += P->c[j] * x[j];
         xx += x[j] * x[j];
+        if (P->ent != 0.0) xl += xlogx(x[j]);
     }
-    double phi = cx + 0.5 * P->delta * xx;
-    double hval[64], gval[64];
+    double phi = cx + 0.5 * P->delta * xx + P->ent * xl;
+    double* hval = cons_buf(P->n_eq);
+    double* gval = cons_buf(P->n_in);
     lsq_cons(P, x, hval, gval);
     for (int32_t k = 0; k < P->n_eq; ++k) {
         const double t = hval[k] + P->lam[k] / P->rho;               /* Eq. (3) */
@@ -297,6 +324,7 @@ static double lsq_phi(const orc_lsq* P, const double* x, double* coef_eq, double
         phi += 0.5 * P->rho * t * t;
         if (coef_in) coef_in[k] = P->rho * t;                          /* (rho g + mu)_+ */
     }
+    free(hval); free(gval);
     return phi;
 }
 
@@ -317,16 +345,23 @@ static void lsq_grad(const orc_lsq* P, const double* x, const double* r, double*
         }
         free(t);
     }
-    double ce[64], ci[64];
+    double* ce = cons_buf(P->n_eq);
+    double* ci = cons_buf(P->n_in);
     lsq_phi(P, x, ce, ci);
     for (int64_t j = 0; j < nv; ++j) {
         double v = g[j];
         if (P->c) v = v + P->c[j];
         v = v + P->delta * x[j];
-        for (int32_t k = 0; k < P->n_eq; ++k) v = v + ce[k] * P->E[(int64_t)k * nv + j];
+        if (P->ent != 0.0) v = v + P->ent * (log(x[j]) + 1.0);       /* d/dx x log x */
+        if (P->tm > 0) {                                               /* row i, column jj */
+            if (P->n_eq > 0) v = v + ce[j % P->tm] + ce[P->tm + j / P->tm];
+        } else {
+            for (int32_t k = 0; k < P->n_eq; ++k) v = v + ce[k] * P->E[(int64_t)k * nv + j];
+        }
         for (int32_t k = 0; k < P->n_in; ++k) v = v + ci[k] * P->G[(int64_t)k * nv + j];
         g[j] = v;
     }
+    free(ce); free(ci);
 }
 
 static double half_sq(int64_t m, const double* r)
@@ -381,20 +416,53 @@ enum { ORC_CONVERGED = 0, ORC_MAX_ITERS = 1, ORC_LINESEARCH_FAILURE = 2,
  * (inequalities: rho/2 ((t1)_+^2 - (t0)_+^2), the same product when both
  * are positive).  Evaluated directly, without forming f(x + alpha p). */
 double orc_armijo_delta(const orc_lsq* P, int64_t nv, const double* x, const double* r,
-                        const double* q, const double* p, double alpha)
+                        const double* q, const double* p, const double* l, const double* u,
+                        double alpha)
 {
     const double rq = P->qp ? dotv(nv, p, r) : dotv(P->m, r, q);
     const double qq = P->qp ? dotv(nv, p, q) : dotv(P->m, q, q);
     const double cp = P->c ? dotv(nv, P->c, p) : 0.0;
     const double xp = dotv(nv, x, p), pp = dotv(nv, p, p);
     double dl = alpha * (rq + cp + P->delta * xp) + 0.5 * alpha * alpha * (qq + P->delta * pp);
-    double hval[64], gval[64];
+    if (P->ent != 0.0) {
+        /* entropy at the clipped trial point y = clip(x + alpha p), per element:
+         * y log y - x log x = d log x + y log(y / x),  d = y - x, with
+         * log(y / x) = log1p(d / x) when |d| < x / 2 (no rounding of y / x near 1) */
+        double se = 0.0;
+        for (int64_t j = 0; j < nv; ++j) {
+            const double y = clip1(fma(alpha, p[j], x[j]), l, u, j), d = y - x[j];
+            if (x[j] > 0.0 && y > 0.0) {
+                const double lr = fabs(d) < 0.5 * x[j] ? log1p(d / x[j]) : log(y / x[j]);
+                se += d * log(x[j]) + y * lr;
+            } else {
+                se += xlogx(y) - xlogx(x[j]);
+            }
+        }
+        dl += P->ent * se;
+    }
+    double* hval = cons_buf(P->n_eq);
+    double* gval = cons_buf(P->n_in);
+    double* ap = cons_buf(P->n_eq + P->n_in);
     lsq_cons(P, x, hval, gval);
+    if (P->tm > 0) {                                    /* a = marginals of p */
+        double* z = cons_buf(P->n_eq);
+        orc_lsq T = *P;
+        double* e0 = cons_buf(P->n_eq);
+        T.e = e0; T.n_in = 0;
+        lsq_cons(&T, p, z, NULL);
+        for (int32_t k = 0; k < P->n_eq; ++k) ap[k] = z[k];
+        free(z); free(e0);
+    }
     for (int32_t k = 0; k < P->n_eq + P->n_in; ++k) {
         const int eq = k < P->n_eq;
         const int32_t kk = eq ? k : k - P->n_eq;
-        const double* col = eq ? P->E + (int64_t)kk * nv : P->G + (int64_t)kk * nv;
-        const double a = dotv(nv, col, p);
+        double a;
+        if (eq && P->tm > 0) {
+            a = ap[k];
+        } else {
+            const double* col = eq ? P->E + (int64_t)kk * nv : P->G + (int64_t)kk * nv;
+            a = dotv(nv, col, p);
+        }
         const double t0 = eq ? hval[kk] + P->lam[kk] / P->rho : gval[kk] + P->mu[kk] / P->rho;
         const double t1 = t0 + alpha * a;
         if (eq || (t0 > 0.0 && t1 > 0.0)) {
@@ -404,6 +472,7 @@ double orc_armijo_delta(const orc_lsq* P, int64_t nv, const double* x, const dou
             dl += 0.5 * P->rho * (p1 * p1 - p0 * p0);
         }
     }
+    free(hval); free(gval); free(ap);
     return dl;
 }
 
@@ -428,7 +497,7 @@ static int armijo_lsq(const orc_lsq* P, const orc_opts* o, int64_t nv, const dou
         for (int64_t i = 0; i < P->m; ++i) r_t[i] = fma(alpha, q[i], r[i]);
         *n_fg += 1;
         if (o->armijo_diff) {                                     /* R29 */
-            const double dl = orc_armijo_delta(P, nv, x, r, q, p, alpha);
+            const double dl = orc_armijo_delta(P, nv, x, r, q, p, l, u, alpha);
             if (dl <= o->c1 * alpha * gp) {
                 *f_out = f + dl; *alpha_out = alpha;
                 return 1;
@@ -560,7 +629,9 @@ typedef struct {
  * when g > 0 and otherwise how far mu is from complementary slackness. */
 static double viol_inf(const orc_lsq* P, const double* x, const double* mu, double rho)
 {
-    double hval[64], gval[64], v = 0.0;
+    double* hval = cons_buf(P->n_eq);
+    double* gval = cons_buf(P->n_in);
+    double v = 0.0;
     lsq_cons(P, x, hval, gval);
     for (int32_t k = 0; k < P->n_eq; ++k) if (fabs(hval[k]) > v) v = fabs(hval[k]);
     for (int32_t k = 0; k < P->n_in; ++k) {
@@ -569,6 +640,7 @@ static double viol_inf(const orc_lsq* P, const double* x, const double* mu, doub
         if (mr < t) t = mr;
         if (fabs(t) > v) v = fabs(t);
     }
+    free(hval); free(gval);
     return v;
 }
 
@@ -598,13 +670,15 @@ void orc_al_solve(orc_lsq* P, double* lam_io, double* mu_io, const double* l, co
         res->inner_iters_total += ir.iters;
         res->outer_iters = it + 1;
         if (ir.status == ORC_LINESEARCH_FAILURE) { res->status = ORC_AL_INNER_FAILURE; break; }
-        double hval[64], gval[64];
+        double* hval = cons_buf(P->n_eq);
+        double* gval = cons_buf(P->n_in);
         lsq_cons(P, x, hval, gval);
         for (int32_t k = 0; k < P->n_eq; ++k) lam_io[k] = lam_io[k] + rho * hval[k];  /* line 6 */
         for (int32_t k = 0; k < P->n_in; ++k) {                                        /* line 7 */
             const double t = mu_io[k] + rho * gval[k];
             mu_io[k] = t > 0.0 ? t : 0.0;
         }
+        free(hval); free(gval);
         const double v = viol_inf(P, x, mu_io, rho);
         if (v > 0.5 * vprev) {                                      /* line 8, R20 */
             rho = rho * ao->rho_factor;

@@ -240,6 +240,56 @@ def svm_dual_kernel(N: int, d: int, seed: int, gamma: float = 1.0, C: float = 1.
     return p
 
 
+@dataclass
+class Transport:
+    """Joint-probability / regularised OT instance:
+    min <cost, P> + lam r(P) s.t. P 1 = u, P^T 1 = v, P >= 0."""
+    name: str
+    cost: np.ndarray                   # (m, n), column-major
+    u: np.ndarray                      # (m,), sums to 1
+    v: np.ndarray                      # (n,), sums to 1
+    lam: float = 0.5                   # PAPER.md:402, 768 ("lambda = 1/2")
+
+    @property
+    def m(self):
+        return self.cost.shape[0]
+
+    @property
+    def n(self):
+        return self.cost.shape[1]
+
+
+def _discrete_gauss(t, mu, sigma):
+    w = np.exp(-0.5 * ((t - mu) / sigma) ** 2)
+    return w / w.sum()
+
+
+def transport_ds1(n: int) -> Transport:
+    """Data set 1: m = n; u a discretised Gaussian, v a
+    discretised mixture of two Gaussians, cost = u u^T (the discretised
+    isotropic two-dimensional Gaussian).  The paper gives no means or
+    widths; reading R31: grid t_i = i / (n - 1), u = N(0.5, 0.15),
+    v = 1/2 N(0.3, 0.08) + 1/2 N(0.7, 0.08), each normalised to sum 1.
+    Deterministic (no seed)."""
+    t = np.linspace(0.0, 1.0, n)
+    u = _discrete_gauss(t, 0.5, 0.15)
+    v = 0.5 * _discrete_gauss(t, 0.3, 0.08) + 0.5 * _discrete_gauss(t, 0.7, 0.08)
+    v = v / v.sum()
+    cost = np.asfortranarray(np.outer(u, u))
+    return Transport(f"jp_ds1_{n}", cost, u, v)
+
+
+def transport_ds2(n: int, seed: int) -> Transport:
+    """Data set 2 (after Frogner & Poggio): m = 2n; u, v ~ U(0,1)
+    scaled to sum 1; cost entries ~ U(0,1); lam = 1/2."""
+    rng = np.random.default_rng([seed, 0xD52])
+    m = 2 * n
+    u = rng.uniform(size=m); u = u / u.sum()
+    v = rng.uniform(size=n); v = v / v.sum()
+    cost = np.asfortranarray(rng.uniform(size=(m, n)))
+    return Transport(f"jp_ds2_{m}x{n}", cost, u, v)
+
+
 # Named configurations of BASELINE.json "configs" (SURVEY.md 8(d) table)
 CONFIGS = {
     "C1": lambda seed=1: nnls_gaussian(200, 100, seed, "C1_nnls_200x100"),
