@@ -173,6 +173,18 @@ lbfgsb_err lbfgsb_objective_lsq(const double* M, int64_t m, int64_t ncols, int64
 lbfgsb_err lbfgsb_objective_qp(const double* Q, int64_t n, int64_t ld, const double* colscale,
                                const double* c, double delta, lbfgsb_objective** out);
 
+/* Joint probability / regularised optimal transport (SURVEY.md 8(f) N2,
+ * PAPER.md:393-402): variables x = vec(P), P m x n column-major (n_vars = m n),
+ *   f(P) = <M, P> + lam r(P),   r = sum_ij P_ij log P_ij   (reg = 0, entropy)
+ *                               r = 1/2 ||P||_F^2          (reg = 1, Gaussian),
+ * M: m x n column-major cost (ld = m, DEVICE, borrowed); lam > 0 (the paper
+ * uses 1/2).  The marginal equalities P 1 = u, P^T 1 = v are
+ * attached by al_solve_transport (lbfgsb_solve returns UNSUPPORTED).  The
+ * entropy needs a positive lower bound on the handle (reading R30: 1e-300).
+ * Single-GPU handles only.  Errors: ARG, DIM. */
+lbfgsb_err lbfgsb_objective_transport(const double* M, int64_t m, int64_t n, int32_t reg, double lam,
+                                      lbfgsb_objective** out);
+
 /* User objective: fg(user, x, g, f_host, stream) must write grad f(x) into
  * the DEVICE vector g (length n), *f_host = f(x) (host), enqueue its device
  * work on `stream` (or synchronise it), and return 0 (nonzero -> the solve
@@ -247,6 +259,19 @@ typedef struct {
 lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const al_constraints* cons,
                     const al_opts* opts, double* x, double* lambda, double* mu,
                     al_result* res);
+
+/* Alg. 4 for a transport objective with its m + n marginal equalities
+ * h(P) = [P 1 - u; P^T 1 - v]: x^0 = clip(0) (R19), lambda^0 =
+ * 0, rho = rho0; each outer iteration minimises Eq. (3) over the box with
+ * Alg. 1 (inner tol max(tol, 0.1 v), R22), then lambda += rho h(x)
+ * and rho *= rho_factor if v = ||h||_inf was not halved
+ * (R20).  The Armijo test is always the difference form of
+ * reading R29.  u (m), v (n): DEVICE; x (DEVICE, m n) out = vec(P*);
+ * lambda (DEVICE, m + n, may be NULL) out; res (host).  res->f is <M, P> +
+ * lam r(P) at P*.  Errors: ARG, DIM, UNSUPPORTED (sharded handle), CUDA. */
+lbfgsb_err al_solve_transport(lbfgsb_t* h, const lbfgsb_objective* obj, const double* u,
+                              const double* v, const al_opts* opts, double* x, double* lambda,
+                              al_result* res);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,8 @@ from . import _build
 
 __all__ = ["Options", "ALOptions", "Result", "ALResult", "Solver", "LSQObjective",
            "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor",
-           "solve_loopback", "nccl_unique_id", "QPObjective", "op_gaussian_kernel"]
+           "solve_loopback", "nccl_unique_id", "QPObjective", "op_gaussian_kernel",
+           "TransportObjective"]
 
 _c_d, _c_i32, _c_i64, _c_vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
 
@@ -105,7 +106,10 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_nccl_unique_id.argtypes = [vp]
     L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
     L.lbfgsb_op_gaussian_kernel.argtypes = [vp, _c_i64, _c_i64, _c_d, vp, _c_i64, vp]
-    for name in ("lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
+    L.lbfgsb_objective_transport.argtypes = [vp, _c_i64, _c_i64, _c_i32, _c_d, C.POINTER(vp)]
+    L.al_solve_transport.argtypes = [vp, vp, vp, vp, C.POINTER(_AlOpts), vp, vp, C.POINTER(_AlRes)]
+    for name in ("lbfgsb_objective_transport", "al_solve_transport",
+                 "lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
                  "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
                  "lbfgsb_profile_get", "lbfgsb_solve_loopback", "lbfgsb_nccl_unique_id",
@@ -254,6 +258,28 @@ class QPObjective(LSQObjective):
         self._h = h
 
 
+class TransportObjective(LSQObjective):
+    """Joint probability / regularised OT (lbfgsb_objective_transport):
+    f(P) = <M, P> + lam r(P), r = sum P log P ("entropy") or 1/2||P||^2
+    ("gaussian"); M CUDA fp64 (m, n) column-major; variables vec(P) (m*n)."""
+
+    def __init__(self, M, reg="entropy", lam=0.5):   # noqa: D107 -- no super().__init__
+        L = load()
+        if M.dim() != 2 or (M.stride(0) != 1 and M.shape[0] > 1) or \
+                (M.shape[1] > 1 and M.stride(1) != M.shape[0]):
+            raise LbfgsbError("M must be (m, n) column-major with ld = m")
+        if reg not in ("entropy", "gaussian"):
+            raise LbfgsbError("reg must be 'entropy' or 'gaussian'")
+        self.m, self.n = M.shape
+        self.nvars = self.m * self.n
+        self.reg = reg
+        self._keep = (M,)
+        h = C.c_void_p()
+        _check(L.lbfgsb_objective_transport(_ptr(M), self.m, self.n, 0 if reg == "entropy" else 1,
+                                            float(lam), C.byref(h)))
+        self._h = h
+
+
 class CallbackObjective:
     """User objective: ``fg(x, g) -> f`` with x, g CUDA fp64 tensors (g written
     in place).  Runs on the current torch stream."""
@@ -376,6 +402,18 @@ class Solver:
                              C.byref(r)))
         return ALResult(r.violation_inf, r.f, r.rho, r.pg_inf, r.outer_iters, r.inner_iters_total,
                         r.status, list(lam)[:m_eq], list(mu)[:p_in])
+
+    def al_solve_transport(self, obj, x, u, v, lam_out=None,
+                           al_opts: ALOptions | None = None) -> ALResult:
+        """Alg. 4 with the marginal equalities P 1 = u, P^T 1 = v (u, v CUDA fp64);
+        x (m*n) out = vec(P*) column-major; lam_out (m+n, CUDA) receives the multipliers."""
+        ao = al_opts or ALOptions()
+        c_ao = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer, 0)
+        r = _AlRes()
+        _check(_lib.al_solve_transport(self._h, obj._h, _ptr(u), _ptr(v), C.byref(c_ao), _ptr(x),
+                                       _ptr(lam_out), C.byref(r)))
+        return ALResult(r.violation_inf, r.f, r.rho, r.pg_inf, r.outer_iters, r.inner_iters_total,
+                        r.status, [], [])
 
     # ---- op-level entry points (lbfgsb_ops.h) ----
     def op_direction(self, x, g, S=None, Y=None):

@@ -145,10 +145,11 @@ struct EpiCtx {
     const double* bptr[2 * MAXH];
 };
 
-// Per-variable epilogue; writes the variable's row of the Gram tile.
-__device__ __forceinline__ void epilogue_var(const Prob& P, const Ctrl* C, const EpiCtx& E, int64_t v,
-                                             double dval, double* trow, double* mkv, double& gmax,
-                                             double& cnt)
+// Per-variable epilogue core (Alg. 1 lines 7-9, Eq. (1)): x', g', s, y, mask.
+// Returns 1 when the variable is fixed (not in S^{k+1}).
+__device__ __forceinline__ bool epi_core(const Prob& P, const Ctrl* C, const EpiCtx& E, int64_t v,
+                                         double dval, double& xn_o, double& gn_o, double& sv_o,
+                                         double& yv_o, double& gmax, double& cnt)
 {
     const double xo = P.x[v], lv = P.l[v], uv = P.u[v];
     double xn = xo;
@@ -159,6 +160,7 @@ __device__ __forceinline__ void epilogue_var(const Prob& P, const Ctrl* C, const
     double gn = dval;
     if (P.c) gn = gn + P.c[v];
     gn = gn + P.delta * xn;
+    if (P.ent != 0.0) gn = gn + P.ent * (log(xn) + 1.0);       // d/dx x log x (N2 entropy)
     for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * P.Ecol[k][v];
     double sv = 0.0, yv = 0.0;
     if (E.iter) {
@@ -177,6 +179,17 @@ __device__ __forceinline__ void epilogue_var(const Prob& P, const Ctrl* C, const
         gmax = ag > gmax ? ag : gmax;
         cnt += 1.0;
     }
+    xn_o = xn; gn_o = gn; sv_o = sv; yv_o = yv;
+    return fixed;
+}
+
+// Per-variable epilogue; writes the variable's row of the Gram tile.
+__device__ __forceinline__ void epilogue_var(const Prob& P, const Ctrl* C, const EpiCtx& E, int64_t v,
+                                             double dval, double* trow, double* mkv, double& gmax,
+                                             double& cnt)
+{
+    double xn, gn, sv, yv;
+    const bool fixed = epi_core(P, C, E, v, dval, xn, gn, sv, yv, gmax, cnt);
     if (!E.gram) return;
     for (int b = 0; b < E.nh; ++b) {
         const int sl = ring_slot(E.head, E.nh, b, E.mh);
@@ -206,6 +219,9 @@ __device__ __forceinline__ void epi_init(const Prob& P, const Ctrl* C, int mode,
     }
 }
 
+__device__ void gram_tail_after(const Prob& P, Ctrl* C, const EpiCtx& E, double gmax, double cnt,
+                                double* red, double* buf, int bufn, double* stash, double* Gs);
+
 // Per-CTA Gram partial -> 2-level deterministic tail -> Alg. 3 (thread 0).
 __device__ void gram_tail(const Prob& P, Ctrl* C, const EpiCtx& E, const GramEnt& ent, const double* gacc,
                           double gmax, double cnt, double* red, double* buf, int bufn, double* stash,
@@ -216,6 +232,18 @@ __device__ void gram_tail(const Prob& P, Ctrl* C, const EpiCtx& E, const GramEnt
     const int ntot = ne + (P.screen_full ? nh : 0);
     double* out = P.gram_part + (int64_t)cta * GRAM_STRIDE;
     ent.finalize(gacc, stash, out, ntot);
+    gram_tail_after(P, C, E, gmax, cnt, red, buf, bufn, stash, Gs);
+}
+
+// After the CTA's Gram partial is in gram_part[cta]: the norms, then the
+// 2-level deterministic tail and Alg. 3 (thread 0 of the last CTA).
+__device__ void gram_tail_after(const Prob& P, Ctrl* C, const EpiCtx& E, double gmax, double cnt,
+                                double* red, double* buf, int bufn, double* stash, double* Gs)
+{
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int nh = E.nh, nb = E.nb, ne = nb * (nb + 1) / 2;
+    const int ntot = ne + (P.screen_full ? nh : 0);
+    double* out = P.gram_part + (int64_t)cta * GRAM_STRIDE;
     const double bm = block_reduce<1>(gmax, red);
     const double bc = block_reduce<0>(cnt, red);
     if (threadIdx.x == 0) { out[ntot] = bm; out[ntot + 1] = bc; }
@@ -773,13 +801,36 @@ __global__ void __launch_bounds__(NT) k_qpu(Prob P, int mode, int bufn)
     double gacc[3] = {0.0, 0.0, 0.0};
     double gmax = 0.0, cnt = 0.0;
     const int64_t n = P.n;
+    const double rho = C->rho;
+    if (P.tp && iter) {                                         // carried h' = h + alpha A p (N2)
+        const int64_t K = P.tm + P.tn;
+        for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < K; k += (int64_t)gridDim.x * NT)
+            wnext[k] = fma(alpha, P.tap[k], wcur[k]);
+    }
+    const bool small = n < (1LL << 31);
     for (int64_t base = (int64_t)blockIdx.x * NT; base < n; base += (int64_t)gridDim.x * NT) {
         const int64_t v = base + threadIdx.x;
         if (v < n) {
-            double w = wcur[v];
-            if (iter) {
-                w = fma(alpha, P.q[v], w);                      // carried w' = Q~ x'
-                wnext[v] = w;
+            double w;
+            if (P.tp) {
+                // marginal multipliers of row i and column j: (rho h + lam)_i + (rho h + lam)_{tm+j}
+                int64_t i, j;
+                if (small) {
+                    const unsigned vv = (unsigned)v, tmu = (unsigned)P.tm;
+                    j = vv / tmu; i = vv - (unsigned)j * tmu;
+                } else {
+                    j = v / P.tm; i = v - j * P.tm;
+                }
+                const int64_t kj = P.tm + j;
+                double hi = wcur[i], hj = wcur[kj];
+                if (iter) { hi = fma(alpha, P.tap[i], hi); hj = fma(alpha, P.tap[kj], hj); }
+                w = (rho * hi + P.tlam[i]) + (rho * hj + P.tlam[kj]);
+            } else {
+                w = wcur[v];
+                if (iter) {
+                    w = fma(alpha, P.q[v], w);                  // carried w' = Q~ x'
+                    wnext[v] = w;
+                }
             }
             epilogue_var(P, C, E, v, w, tile + (int64_t)threadIdx.x * E.nb, mk + threadIdx.x, gmax, cnt);
         } else if (E.gram) {
@@ -794,6 +845,129 @@ __global__ void __launch_bounds__(NT) k_qpu(Prob P, int mode, int bufn)
     }
     if (!E.gram) return;
     gram_tail(P, C, E, ent, gacc, gmax, cnt, red, smq, bufn, stash, Gs);
+}
+
+// ---------------------------------------------------------------- k_qepi (register Gram)
+// QP / transport epilogue for m_hist <= (NBX - 1) / 2: each thread keeps the
+// variable's Gram row (S, Y, g) in registers and accumulates the upper
+// triangle of B^T diag(mask) B and the unmasked ||B_b||^2 in NBX (NBX + 1) / 2
+// + NBX register accumulators over a grid-stride loop (fixed order per
+// thread), reduced once per CTA (warp shuffles, then warps in order).  No
+// shared-memory tile, no per-tile barriers: for n in the millions (N2) the
+// Gram costs ~66 DFMA per variable, well under the epilogue's HBM time.
+template <int NBX>
+__global__ void __launch_bounds__(NT, 1) k_qepi(Prob P, int mode)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    constexpr int NE = NBX * (NBX + 1) / 2, NA = NE + NBX;
+    __shared__ double red[NT / 32];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    __shared__ double buf[NT / 32 * NA > 4096 ? NT / 32 * NA : 4096];
+    const bool iter = mode == BWD_ITER;
+    const double* wcur = P.rbuf[C->rsel];
+    double* wnext = P.rbuf[C->rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    const double rho = C->rho;
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    const int64_t n = P.n;
+    if (P.tp && iter) {                                         // carried h' = h + alpha A p (N2)
+        const int64_t K = P.tm + P.tn;
+        for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < K; k += (int64_t)gridDim.x * NT)
+            wnext[k] = fma(alpha, P.tap[k], wcur[k]);
+    }
+    double acc[NA];
+#pragma unroll
+    for (int k = 0; k < NA; ++k) acc[k] = 0.0;
+    double gmax = 0.0, cnt = 0.0;
+    const bool small = n < (1LL << 31);
+    const int nh = E.nh;
+    for (int64_t v = (int64_t)blockIdx.x * NT + threadIdx.x; v < n; v += (int64_t)gridDim.x * NT) {
+        double w;
+        if (P.tp) {
+            int64_t i, j;
+            if (small) {
+                const unsigned vv = (unsigned)v, tmu = (unsigned)P.tm;
+                j = vv / tmu; i = vv - (unsigned)j * tmu;
+            } else {
+                j = v / P.tm; i = v - j * P.tm;
+            }
+            const int64_t kj = P.tm + j;
+            double hi = wcur[i], hj = wcur[kj];
+            if (iter) { hi = fma(alpha, P.tap[i], hi); hj = fma(alpha, P.tap[kj], hj); }
+            w = (rho * hi + P.tlam[i]) + (rho * hj + P.tlam[kj]);
+        } else {
+            w = wcur[v];
+            if (iter) {
+                w = fma(alpha, P.q[v], w);                      // carried w' = Q~ x'
+                wnext[v] = w;
+            }
+        }
+        double xn, gn, sv, yv;
+        const bool fixed = epi_core(P, C, E, v, w, xn, gn, sv, yv, gmax, cnt);
+        if (!E.gram) continue;
+        double bv[NBX];
+#pragma unroll
+        for (int b = 0; b < NBX; ++b) {
+            double val = 0.0;
+            if (b < 2 * nh) {
+                const int bb = b < nh ? b : b - nh;
+                const bool cur = E.iter && ring_slot(E.head, nh, bb, E.mh) == E.slot;
+                val = cur ? (b < nh ? sv : yv) : E.bptr[b][v];
+            } else if (b == 2 * nh) {
+                val = gn;
+            }
+            bv[b] = val;
+        }
+        int idx = 0;
+#pragma unroll
+        for (int a = 0; a < NBX; ++a) {
+            const double ma = fixed ? 0.0 : bv[a];
+#pragma unroll
+            for (int b = a; b < NBX; ++b) {
+                acc[idx] = fma(ma, bv[b], acc[idx]);
+                ++idx;
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < NBX; ++b) acc[NE + b] = fma(bv[b], bv[b], acc[NE + b]);
+    }
+    if (!E.gram) return;
+    // CTA reduction of the NA accumulators (warps in order)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+        const double s = warp_red<0>(acc[k]);
+        if (lane == 0) buf[wid * NA + k] = s;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < NA; k += NT) {
+        double s = buf[k];
+        for (int w = 1; w < NT / 32; ++w) s += buf[w * NA + k];
+        stash[k] = s;                                           // NA <= NT
+    }
+    __syncthreads();
+    // this CTA's partial in the runtime enumeration of gram_tail (a <= b < nb, then
+    // the unmasked ||y_k||^2 when screen_full)
+    const int nb = E.nb, ne = nb * (nb + 1) / 2;
+    const int ntot = ne + (P.screen_full ? nh : 0);
+    double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
+    for (int e = threadIdx.x; e < ntot; e += NT) {
+        int k;
+        if (e < ne) {
+            int aa = 0, rem = e;
+            while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
+            const int bb = aa + rem;
+            k = aa * NBX - aa * (aa - 1) / 2 + (bb - aa);
+        } else {
+            k = NE + nh + (e - ne);
+        }
+        out[e] = stash[k];
+    }
+    __syncthreads();
+    gram_tail_after(P, C, E, gmax, cnt, red, buf, 4096, stash, Gs);
 }
 
 // ---------------------------------------------------------------- k_bwd (generic)
@@ -873,6 +1047,9 @@ static int g_bwd_occ = 0, g_bwdw_occ = 0;
 // k_bwd_c (TMA, CTA pairs) is opt-in: on C2 it measured 275-335 us vs 268 us for k_bwd_s
 // (DESIGN.md section 5); enable with LBFGSB_TMA=1 for experiments.
 static bool g_no_tma = getenv("LBFGSB_TMA") == nullptr;
+// k_qepi (register Gram) is the QP / transport epilogue for m_hist <= 5; LBFGSB_NO_QEPI=1
+// selects the shared-memory tile kernel k_qpu instead (A/B experiments)
+static bool g_no_qepi = getenv("LBFGSB_NO_QEPI") != nullptr;
 constexpr int BWD_W_MAXM = 2048;
 constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + 64);
 static bool g_bwd_init = false;
@@ -918,7 +1095,19 @@ static size_t bwd_s_smem(const Prob& P, int G)
 void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, double* gout)
 {
     bwd_init();
-    if (P.qp && mode != BWD_PLAIN) {
+    if ((P.qp || P.tp) && mode != BWD_PLAIN && P.mh <= 5 && !g_no_qepi) {
+        static int occ = 0;
+        if (!occ) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qepi<11>, NT, 0);
+            if (occ < 1) occ = 1;
+        }
+        int64_t g = (P.n + NT - 1) / NT;
+        const int64_t cap = (int64_t)sm_count() * occ;
+        if (g > cap) g = cap;
+        k_qepi<11><<<(int)g, NT, 0, st>>>(P, mode);
+        return;
+    }
+    if ((P.qp || P.tp) && mode != BWD_PLAIN) {
         const int sms = sm_count();
         int64_t g = (P.n + NT - 1) / NT;
         if (g > 2LL * sms) g = 2LL * sms;

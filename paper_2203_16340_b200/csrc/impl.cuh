@@ -126,6 +126,23 @@ struct Prob {
     double* dir_all;        // [nranks][4]
     double* gram_all;       // [nranks][GRAM_STRIDE]
     double* kkt_all;        // [nranks][4]
+    // joint-probability / regularised OT objective (transport.cu):
+    // x = vec(P), P tm x tn column-major; c = cost; delta (Gaussian) or ent
+    // (entropy) weight; rbuf[rsel] holds the carried marginal residual
+    // h = [P1 - u; P^T 1 - v] (tm + tn), tap = [p 1; p^T 1] of the direction
+    int tp;
+    int64_t tm, tn;
+    double ent;
+    double* tlam;           // [tm + tn] AL multipliers (device)
+    const double* te;       // [tm + tn] right-hand sides (u; v)
+    double* tap;            // [tm + tn]
+    double* trow;           // [TCB][tm] row partials
+    double* tcol;           // [TRB][tn] column partials
+    double* tsp;            // [TRB * TCB][TNS] per-CTA sums
+    double* tspr;           // [TRB][2] row-block finisher sums
+    double* tspc;           // [TCB][2] column-chunk finisher sums
+    unsigned* tticket;      // [TRB + TCB + 1]
+    int TRB, TCB;           // k_tsum grid: row blocks of NT rows x chunks of TCOLS columns
 };
 
 __host__ __device__ inline int64_t qs_len(const Prob& P) { return P.m + (int64_t)KT * NSEP; }
@@ -139,6 +156,10 @@ enum FwdMode : int { FWD_ITER = 0, FWD_SETUP = 1, FWD_P = 2 };
 enum BwdMode : int { BWD_ITER = 0, BWD_SETUP = 1, BWD_PLAIN = 2, BWD_REFRESH = 3 };
 enum SepMode : int { SEP_ITER = 0, SEP_NEXT = 1, SEP_SETUP = 2, SEP_OP = 3 };
 enum LsMode : int { LS_NEXT = 0, LS_OP = 1, LS_SH_ITER = 2, LS_SH_SETUP = 3 };
+enum TsMode : int { TS_ITER = 0, TS_NEXT = 1, TS_SETUP = 2 };
+constexpr int TCOLS = 16;                  // k_tsum columns per CTA
+constexpr int TT = 4;                      // entropy Armijo trials per batch
+constexpr int TNS = 3 + TT;                // k_tsum per-CTA sums
 
 // ---- launchers (kernels.cu)
 void init_kernels();
@@ -163,5 +184,8 @@ void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);
 void launch_cb_trial(const Prob& P, cudaStream_t st, double alpha, double* xt);
 void launch_cb_commit(const Prob& P, cudaStream_t st, const double* xt, const double* gt, int slot);
+// transport.cu
+void launch_tsum(const Prob& P, cudaStream_t st, int mode);
+void launch_tviol(const Prob& P, cudaStream_t st, double rho, int update, double* out_dev);
 
 }  // namespace lb

@@ -56,7 +56,10 @@ extern "C" const char* lbfgsb_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------ objects
 struct lbfgsb_objective {
-    int kind;                       // 0 LSQ, 1 callback
+    int kind;                       // 0 LSQ (and QP), 1 callback, 2 transport
+    int64_t tm = 0, tn = 0;         // transport: P is tm x tn
+    int reg = 0;                    // transport: 0 entropy, 1 Gaussian
+    double lam = 0.0;               // transport: regularisation weight
     const double* M;
     int64_t m, ncols, ld;
     const double* colscale;
@@ -115,6 +118,8 @@ struct lbfgsb_t {
     DevBuf pk_loc, qs_all, dir_all, gram_all, kkt_all;
     // host-buffer solve staging
     DevBuf Mh, bh, xh;
+    // transport objective
+    DevBuf tlam, te, tap, trow, tcol, tsp, tspr, tspc, tticket, tvout;
     Ctrl* ctrl = nullptr;           // device
     Ctrl* hc = nullptr;             // pinned host mirror
     // graph cache
@@ -282,7 +287,8 @@ extern "C" void lbfgsb_destroy(lbfgsb_t* h)
                       &h->xt, &h->gt, &h->gram_part, &h->gram_grp, &h->dir_part, &h->kkt_part,
                       &h->tickets, &h->sep_part, &h->r0, &h->r1, &h->q, &h->qpart, &h->lsp,
                       &h->fout, &h->Mh, &h->bh, &h->xh, &h->pk_loc, &h->qs_all, &h->dir_all,
-                      &h->gram_all, &h->kkt_all};
+                      &h->gram_all, &h->kkt_all, &h->tlam, &h->te, &h->tap, &h->trow,
+                      &h->tcol, &h->tsp, &h->tspr, &h->tspc, &h->tticket, &h->tvout};
     for (DevBuf* b : bufs) b->release();
     if (h->ctrl) cudaFree(h->ctrl);
     if (h->hc) cudaFreeHost(h->hc);
@@ -321,6 +327,24 @@ extern "C" lbfgsb_err lbfgsb_objective_qp(const double* Q, int64_t n, int64_t ld
 {
     TRY(lbfgsb_objective_lsq(Q, n, n, ld, colscale, 0, nullptr, c, delta, out));
     (*out)->qp = 1;
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_objective_transport(const double* M, int64_t m, int64_t n, int32_t reg,
+                                                 double lam, lbfgsb_objective** out)
+{
+    if (!out) return fail(LBFGSB_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (!M) return fail(LBFGSB_ERR_ARG, "M is NULL");
+    if (m <= 0 || n <= 0 || m > (1LL << 40) / n) return fail(LBFGSB_ERR_DIM, "bad shape m=%lld n=%lld",
+                                                             (long long)m, (long long)n);
+    if (reg != 0 && reg != 1) return fail(LBFGSB_ERR_ARG, "reg must be 0 (entropy) or 1 (Gaussian)");
+    if (!(lam > 0) || !std::isfinite(lam)) return fail(LBFGSB_ERR_ARG, "lam must be positive");
+    auto* o = new lbfgsb_objective();
+    o->kind = 2;
+    o->M = M; o->m = m; o->ncols = n; o->ld = m;
+    o->tm = m; o->tn = n; o->reg = reg; o->lam = lam;
+    *out = o;
     return LBFGSB_OK;
 }
 
@@ -404,6 +428,35 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
             P.pk_loc = h->pk_loc.d(); P.qs_all = h->qs_all.d(); P.dir_all = h->dir_all.d();
             P.gram_all = h->gram_all.d(); P.kkt_all = h->kkt_all.d();
         }
+    }
+    if (ob && ob->kind == 2) {                                 // transport
+        if (ob->tm * ob->tn != h->n)
+            return fail(LBFGSB_ERR_DIM, "transport objective has %lld variables, handle %lld",
+                        (long long)(ob->tm * ob->tn), (long long)h->n);
+        if (h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "transport objectives are single-GPU");
+        P.tp = 1;
+        P.tm = ob->tm; P.tn = ob->tn;
+        P.c = ob->M;
+        if (ob->reg == 1) P.delta = ob->lam; else P.ent = ob->lam;
+        P.diff = 1;                                            // R29 (always, see transport.cu)
+        P.TRB = (int)cdiv(P.tm, NT);
+        P.TCB = (int)cdiv(P.tn, TCOLS);
+        const int64_t K = P.tm + P.tn;
+        const size_t kb = sizeof(double) * (size_t)K;
+        TRY(h->r0.ensure(kb)); TRY(h->r1.ensure(kb));
+        TRY(h->tlam.ensure(kb)); TRY(h->te.ensure(kb)); TRY(h->tap.ensure(kb));
+        TRY(h->trow.ensure(sizeof(double) * (size_t)P.TCB * P.tm));
+        TRY(h->tcol.ensure(sizeof(double) * (size_t)P.TRB * P.tn));
+        TRY(h->tsp.ensure(sizeof(double) * (size_t)P.TRB * P.TCB * TNS));
+        TRY(h->tspr.ensure(sizeof(double) * (size_t)P.TRB * 2));
+        TRY(h->tspc.ensure(sizeof(double) * (size_t)P.TCB * 2));
+        TRY(h->tticket.ensure(sizeof(unsigned) * (size_t)(P.TRB + P.TCB + 2), true));
+        TRY(h->tvout.ensure(sizeof(double)));
+        P.rbuf[0] = h->r0.d(); P.rbuf[1] = h->r1.d();
+        P.tlam = h->tlam.d(); P.te = h->te.d(); P.tap = h->tap.d();
+        P.trow = h->trow.d(); P.tcol = h->tcol.d(); P.tsp = h->tsp.d();
+        P.tspr = h->tspr.d(); P.tspc = h->tspc.d();
+        P.tticket = static_cast<unsigned*>(h->tticket.p);
     }
     return LBFGSB_OK;
 }
@@ -498,6 +551,7 @@ static void rec_event(Group& g, int idx)
 static int per_iteration_launches(const Group& g)
 {
     const int sep = g.Ps[0].GS > 0;
+    if (g.Ps[0].tp) return 3;
     return g.sharded ? (int)g.hs.size() * (6 + sep) : 3 + sep;
 }
 
@@ -507,7 +561,16 @@ static int per_iteration_launches(const Group& g)
 static lbfgsb_err launch_iteration(Group& g, int ev_base)
 {
     cudaStream_t st = g.st;
-    if (!g.sharded) {
+    if (g.Ps[0].tp) {                                          // transport: k_dir k_tsum k_qpu
+        const Prob& P = g.Ps[0];
+        launch_dir(P, st, 0);
+        rec_event(g, ev_base >= 0 ? ev_base + 0 : -1);
+        launch_tsum(P, st, TS_ITER);
+        rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);
+        rec_event(g, ev_base >= 0 ? ev_base + 2 : -1);
+        launch_bwd(P, st, BWD_ITER, nullptr, nullptr);
+        rec_event(g, ev_base >= 0 ? ev_base + 3 : -1);
+    } else if (!g.sharded) {
         const Prob& P = g.Ps[0];
         launch_dir(P, st, 0);
         launch_sep(P, st, SEP_ITER, nullptr);
@@ -541,6 +604,11 @@ static lbfgsb_err launch_iteration(Group& g, int ev_base)
 static lbfgsb_err launch_fval(Group& g, bool clip)
 {
     cudaStream_t st = g.st;
+    if (g.Ps[0].tp) {
+        if (clip) launch_clip(g.Ps[0], st);
+        launch_tsum(g.Ps[0], st, TS_SETUP);
+        return LBFGSB_OK;
+    }
     FOR_RANKS {
         if (clip) launch_clip(PR, st);
         launch_sep(PR, st, SEP_SETUP, PR.x);
@@ -586,6 +654,12 @@ static lbfgsb_err launch_refresh(Group& g)
 // Stall continuation: next Armijo batch, then the gradient pass.
 static lbfgsb_err launch_ls_cont(Group& g)
 {
+    if (g.Ps[0].tp) {
+        launch_tsum(g.Ps[0], g.st, TS_NEXT);
+        launch_bwd(g.Ps[0], g.st, BWD_ITER, nullptr, nullptr);
+        g.h0()->launches += 2;
+        return LBFGSB_OK;
+    }
     FOR_RANKS launch_sep(PR, g.st, SEP_NEXT, nullptr);
     if (g.sharded && g.Ps[0].GS > 0) TRY(xchg(g, SEC_QS));
     FOR_RANKS launch_ls(PR, g.st, LS_NEXT, nullptr, nullptr, nullptr, 0);
@@ -851,6 +925,8 @@ extern "C" lbfgsb_err lbfgsb_solve(lbfgsb_t* h, const lbfgsb_objective* obj, dou
         if (h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "callback objectives are single-GPU");
         return solve_cb(h, obj, x, t, res);
     }
+    if (obj->kind == 2)
+        return fail(LBFGSB_ERR_UNSUPPORTED, "transport objectives are solved with al_solve_transport");
     Group g;
     TRY(single_group(h, obj, g));
     set_sep(g.Ps[0]);
@@ -1017,6 +1093,91 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
     R.rho = rho;
     if (lambda) for (int k = 0; k < neq; ++k) lambda[k] = lam[k];
     if (mu) for (int k = 0; k < nin; ++k) mu[k] = lam[neq + k];
+    if (res) *res = R;
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ Alg. 4, marginal constraints
+static const bool g_al_trace = std::getenv("LBFGSB_AL_TRACE") != nullptr;   // per-outer stderr line
+
+// Joint probability / regularised OT: the m + n
+// equalities h(P) = [P 1 - u; P^T 1 - v] with device multipliers; otherwise
+// the rules of al_solve (R19-R22; the violation of equalities is ||h||_inf).
+extern "C" lbfgsb_err al_solve_transport(lbfgsb_t* h, const lbfgsb_objective* obj, const double* u,
+                                         const double* v, const al_opts* opts, double* x,
+                                         double* lambda, al_result* res)
+{
+    if (!h || !obj || !x || !u || !v) return fail(LBFGSB_ERR_ARG, "NULL handle, objective, u, v or x");
+    if (obj->kind != 2) return fail(LBFGSB_ERR_ARG, "al_solve_transport needs a transport objective");
+    al_opts ao;
+    al_opts_default(&ao);
+    if (opts) ao = *opts;
+    if (!(ao.rho0 > 0) || !(ao.rho_factor > 1) || ao.max_outer < 1)
+        return fail(LBFGSB_ERR_ARG, "invalid al_opts");
+    Group g;
+    TRY(single_group(h, obj, g));
+    Prob& P = g.Ps[0];
+    cudaStream_t st = h->st;
+    const int64_t K = P.tm + P.tn;
+    CK(cudaMemcpyAsync(h->te.d(), u, sizeof(double) * P.tm, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(h->te.d() + P.tm, v, sizeof(double) * P.tn, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(P.tlam, 0, sizeof(double) * K, st));            // lambda^0 = 0
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * h->n, st));              // x^0 = clip(0) (R19)
+    const double tol = h->o.tol;
+    double rho = ao.rho0;
+    double* vout = h->tvout.d();
+    auto violation = [&](int update, double& out) -> lbfgsb_err {
+        launch_tviol(P, st, rho, update, vout);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&out, vout, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return LBFGSB_OK;
+    };
+    h->hc->rho = rho;
+    CK(cudaMemcpyAsync(P.x, x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, st));
+    init_ctrl(h, tol);
+    TRY(ctrl_to_dev(g));
+    TRY(launch_fval(g, true));
+    CK(cudaGetLastError());
+    TRY(ctrl_to_host(g));
+    CK(cudaMemcpyAsync(x, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, st));
+    double vprev = 0.0;
+    TRY(violation(0, vprev));
+    al_result R{};
+    R.status = AL_MAX_OUTER;
+    lbfgsb_result ir{};
+    double* xs[1] = {x};
+    double vlast = vprev;
+    for (int it = 0; it < ao.max_outer; ++it) {
+        const double tin = 0.1 * vprev > tol ? 0.1 * vprev : tol;      // R22
+        h->hc->rho = rho;
+        TRY(solve_group(g, xs, tin, &ir));                            // Alg. 4 line 5
+        R.inner_iters_total += ir.iters;
+        R.outer_iters = it + 1;
+        R.pg_inf = ir.pg_inf;
+        R.f = h->hc->f_base;
+        if (ir.status == LBFGSB_LINESEARCH_FAILURE) { R.status = AL_INNER_FAILURE; break; }
+        double vv = 0.0;
+        TRY(violation(1, vv));                                         // line 6: lam += rho h
+        vlast = vv;
+        if (g_al_trace)
+            std::fprintf(stderr, "[al_transport] outer %d rho %.3e tol_in %.3e inner %lld status %d "
+                         "pg %.3e viol %.3e f %.15g\n", it, rho, tin, (long long)ir.iters, ir.status,
+                         ir.pg_inf, vv, h->hc->f_base);
+        if (vv > 0.5 * vprev) {                                        // line 8 (R20)
+            rho = rho * ao.rho_factor;
+            if (rho > ao.rho_cap) rho = ao.rho_cap;
+        }
+        vprev = vv;
+        if (ir.status == LBFGSB_CONVERGED && vv <= ao.feas_tol && tin == tol) {
+            R.status = LBFGSB_CONVERGED;
+            break;
+        }
+    }
+    R.violation_inf = vlast;
+    R.rho = rho;
+    if (lambda) CK(cudaMemcpyAsync(lambda, P.tlam, sizeof(double) * K, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
     if (res) *res = R;
     return LBFGSB_OK;
 }
