@@ -885,6 +885,24 @@ __global__ void __launch_bounds__(NT, 1) k_qepi(Prob P, int mode)
     const bool small = n < (1LL << 31);
     const int nh = E.nh;
     for (int64_t v = (int64_t)blockIdx.x * NT + threadIdx.x; v < n; v += (int64_t)gridDim.x * NT) {
+        // ---- every load of the variable first (memory-level parallelism: the
+        // stores below may alias nothing we read later, but the compiler
+        // cannot prove it)
+        const double xo = P.x[v], lv = P.l[v], uv = P.u[v];
+        const double pv = E.iter ? (E.branch ? P.pp[v] : P.pt[v]) : 0.0;
+        const double cv = P.c ? P.c[v] : 0.0;
+        const double go = E.iter ? P.g[v] : 0.0;
+        double bv[NBX];
+#pragma unroll
+        for (int b = 0; b < NBX; ++b) {
+            double val = 0.0;
+            if (E.gram && b < 2 * nh) {
+                const int bb = b < nh ? b : b - nh;
+                const bool cur = E.iter && ring_slot(E.head, nh, bb, E.mh) == E.slot;
+                if (!cur) val = __ldcs(E.bptr[b] + v);
+            }
+            bv[b] = val;
+        }
         double w;
         if (P.tp) {
             int64_t i, j;
@@ -905,21 +923,40 @@ __global__ void __launch_bounds__(NT, 1) k_qepi(Prob P, int mode)
                 wnext[v] = w;
             }
         }
-        double xn, gn, sv, yv;
-        const bool fixed = epi_core(P, C, E, v, w, xn, gn, sv, yv, gmax, cnt);
+        // ---- epilogue (the arithmetic of epi_core, on the preloaded values)
+        const double xn = E.iter ? clipd(fma(E.alpha, pv, xo), lv, uv) : xo;   // Alg. 1 line 7
+        double gn = w;
+        if (P.c) gn = gn + cv;
+        gn = gn + P.delta * xn;
+        if (P.ent != 0.0) gn = gn + P.ent * (log(xn) + 1.0);
+        for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * P.Ecol[k][v];
+        double sv = 0.0, yv = 0.0;
+        if (E.iter) {
+            const int64_t so = (int64_t)E.slot * n + v;
+            sv = xn - xo;                                       // s^k
+            yv = gn - go;                                       // y^k
+            P.S[so] = sv;
+            P.Y[so] = yv;
+        }
+        P.x[v] = xn;
+        P.g[v] = gn;
+        const bool fixed = (xn <= lv + P.eps && gn >= 0.0) || (xn >= uv - P.eps && gn <= 0.0);
+        P.mask[v] = fixed ? 0 : 1;                              // S^{k+1}, Eq. (1)
+        if (!fixed) {
+            const double ag = fabs(gn);
+            gmax = ag > gmax ? ag : gmax;
+            cnt += 1.0;
+        }
         if (!E.gram) continue;
-        double bv[NBX];
 #pragma unroll
         for (int b = 0; b < NBX; ++b) {
-            double val = 0.0;
             if (b < 2 * nh) {
                 const int bb = b < nh ? b : b - nh;
                 const bool cur = E.iter && ring_slot(E.head, nh, bb, E.mh) == E.slot;
-                val = cur ? (b < nh ? sv : yv) : E.bptr[b][v];
+                if (cur) bv[b] = b < nh ? sv : yv;
             } else if (b == 2 * nh) {
-                val = gn;
+                bv[b] = gn;
             }
-            bv[b] = val;
         }
         int idx = 0;
 #pragma unroll
@@ -1042,6 +1079,213 @@ __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* r
     gram_tail(P, C, E, ent, gacc, gmax, cnt, red, buf, BWD_BUF, stash, Gs);
 }
 
+// ---------------------------------------------------------------- k_qepi_t (TMA-staged)
+// Same epilogue and register Gram as k_qepi, with every per-variable input
+// streamed into shared memory by cp.async.bulk: persistent CTAs walk tiles
+// of QT variables; thread 0 issues one bulk copy per input vector per tile
+// into a 2-stage ring (mbarrier complete_tx), so ~QT * nvec * 8 bytes per SM
+// are in flight independently of the (register-heavy) consumer threads.
+// Inputs per tile: x, l, u, [g, p] (iteration), [c], [w, q] (QP), the S / Y
+// columns of every pair except the one this iteration overwrites.  The
+// partial last tile (n % QT variables) is read directly from global memory.
+constexpr int QT = 512;                      // variables per tile (2 per thread)
+constexpr int QV_MAX = 8 + 2 * MAXH;         // staged vectors per tile (upper bound)
+
+template <int NBX>
+__global__ void __launch_bounds__(NT, 1) k_qepi_t(Prob P, int mode)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    constexpr int NE = NBX * (NBX + 1) / 2, NA = NE + NBX;
+    extern __shared__ __align__(128) double stg[];           // [2][nvec][QT]
+    __shared__ double red[NT / 32];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    __shared__ double buf[NT / 32 * NA > 4096 ? NT / 32 * NA : 4096];
+    __shared__ const double* vsrc[QV_MAX];
+    __shared__ int vslot_b[2 * MAXH];                        // staged slot of Gram vector b (-1: cur)
+    __shared__ __align__(8) uint64_t full_bar[2];
+    const bool iter = mode == BWD_ITER;
+    const double* wcur = P.rbuf[C->rsel];
+    double* wnext = P.rbuf[C->rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    const double rho = C->rho;
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    const int64_t n = P.n;
+    const int nh = E.nh;
+    // staged vector list (same order in every CTA)
+    enum { VX = 0, VL = 1, VU = 2, VG = 3, VP = 4, VC = 5, VW = 6, VQ = 7 };
+    if (threadIdx.x == 0) {
+        vsrc[VX] = P.x; vsrc[VL] = P.l; vsrc[VU] = P.u;
+        vsrc[VG] = iter ? P.g : nullptr;
+        vsrc[VP] = iter ? (E.branch ? P.pp : P.pt) : nullptr;
+        vsrc[VC] = P.c;
+        vsrc[VW] = P.qp ? wcur : nullptr;
+        vsrc[VQ] = (P.qp && iter) ? P.q : nullptr;
+        int k = 8;
+        for (int b = 0; b < 2 * nh; ++b) {
+            const int bb = b < nh ? b : b - nh;
+            const bool cur = E.iter && ring_slot(E.head, nh, bb, E.mh) == E.slot;
+            if (!E.gram || cur) { vslot_b[b] = -1; continue; }
+            vslot_b[b] = k;
+            vsrc[k++] = E.bptr[b];
+        }
+        for (; k < QV_MAX; ++k) vsrc[k] = nullptr;
+        mbar_init(&full_bar[0], 1);
+        mbar_init(&full_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int nvec = 8 + 2 * nh;                              // slot stride (some slots unused)
+    const int64_t nfull = n / QT;
+    const int64_t ntiles = (n + QT - 1) / QT;
+    unsigned bytes_tile = 0;
+    for (int k = 0; k < nvec; ++k) if (vsrc[k]) bytes_tile += QT * 8;
+    auto issue = [&](int64_t t, int sidx) {                  // thread 0 only
+        double* base = stg + (size_t)sidx * nvec * QT;
+        mbar_arrive_tx(&full_bar[sidx], bytes_tile);
+        for (int k = 0; k < nvec; ++k)
+            if (vsrc[k]) bulk_g2s(base + (size_t)k * QT, vsrc[k] + t * QT, QT * 8, &full_bar[sidx]);
+    };
+    if (P.tp && iter) {                                         // carried h' = h + alpha A p (N2)
+        const int64_t K = P.tm + P.tn;
+        for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < K; k += (int64_t)gridDim.x * NT)
+            wnext[k] = fma(alpha, P.tap[k], wcur[k]);
+    }
+    double acc[NA];
+#pragma unroll
+    for (int k = 0; k < NA; ++k) acc[k] = 0.0;
+    double gmax = 0.0, cnt = 0.0;
+    const bool small = n < (1LL << 31);
+    // prologue: first full tile of this CTA
+    int64_t t0 = blockIdx.x;
+    if (threadIdx.x == 0 && t0 < nfull) issue(t0, 0);
+    int li = 0;
+    for (int64_t t = t0; t < ntiles; t += gridDim.x, ++li) {
+        const int sidx = li & 1;
+        const bool staged = t < nfull;
+        if (staged) {
+            const int64_t tn = t + gridDim.x;                   // prefetch the next tile
+            if (threadIdx.x == 0 && tn < nfull) issue(tn, sidx ^ 1);
+            mbar_wait(&full_bar[sidx], (unsigned)((li >> 1) & 1));
+        }
+        const double* base = stg + (size_t)sidx * nvec * QT;
+#pragma unroll 1
+        for (int e = threadIdx.x; e < QT; e += NT) {
+            const int64_t v = t * QT + e;
+            if (v >= n) break;
+            auto ld = [&](int k) -> double { return staged ? base[(size_t)k * QT + e] : vsrc[k][v]; };
+            const double xo = ld(VX), lv = ld(VL), uv = ld(VU);
+            const double pv = iter ? ld(VP) : 0.0;
+            const double go = iter ? ld(VG) : 0.0;
+            const double cv = P.c ? ld(VC) : 0.0;
+            double w;
+            if (P.tp) {
+                int64_t i, j;
+                if (small) {
+                    const unsigned vv = (unsigned)v, tmu = (unsigned)P.tm;
+                    j = vv / tmu; i = vv - (unsigned)j * tmu;
+                } else {
+                    j = v / P.tm; i = v - j * P.tm;
+                }
+                const int64_t kj = P.tm + j;
+                double hi = wcur[i], hj = wcur[kj];
+                if (iter) { hi = fma(alpha, P.tap[i], hi); hj = fma(alpha, P.tap[kj], hj); }
+                w = (rho * hi + P.tlam[i]) + (rho * hj + P.tlam[kj]);
+            } else {
+                w = ld(VW);
+                if (iter) {
+                    w = fma(alpha, ld(VQ), w);                  // carried w' = Q~ x'
+                    wnext[v] = w;
+                }
+            }
+            const double xn = iter ? clipd(fma(alpha, pv, xo), lv, uv) : xo;   // Alg. 1 line 7
+            double gn = w;
+            if (P.c) gn = gn + cv;
+            gn = gn + P.delta * xn;
+            if (P.ent != 0.0) gn = gn + P.ent * (log(xn) + 1.0);
+            for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * P.Ecol[k][v];
+            double sv = 0.0, yv = 0.0;
+            if (iter) {
+                const int64_t so = (int64_t)E.slot * n + v;
+                sv = xn - xo;                                   // s^k
+                yv = gn - go;                                   // y^k
+                P.S[so] = sv;
+                P.Y[so] = yv;
+            }
+            P.x[v] = xn;
+            P.g[v] = gn;
+            const bool fixed = (xn <= lv + P.eps && gn >= 0.0) || (xn >= uv - P.eps && gn <= 0.0);
+            P.mask[v] = fixed ? 0 : 1;                          // S^{k+1}, Eq. (1)
+            if (!fixed) {
+                const double ag = fabs(gn);
+                gmax = ag > gmax ? ag : gmax;
+                cnt += 1.0;
+            }
+            if (!E.gram) continue;
+            double bv[NBX];
+#pragma unroll
+            for (int b = 0; b < NBX; ++b) {
+                double val = 0.0;
+                if (b < 2 * nh) {
+                    const int k = vslot_b[b];
+                    val = k < 0 ? (b < nh ? sv : yv) : ld(k);
+                } else if (b == 2 * nh) {
+                    val = gn;
+                }
+                bv[b] = val;
+            }
+            int idx = 0;
+#pragma unroll
+            for (int a = 0; a < NBX; ++a) {
+                const double ma = fixed ? 0.0 : bv[a];
+#pragma unroll
+                for (int b = a; b < NBX; ++b) {
+                    acc[idx] = fma(ma, bv[b], acc[idx]);
+                    ++idx;
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < NBX; ++b) acc[NE + b] = fma(bv[b], bv[b], acc[NE + b]);
+        }
+        // every thread is done with this stage before it is refilled (two tiles on)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+    }
+    if (!E.gram) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+        const double s = warp_red<0>(acc[k]);
+        if (lane == 0) buf[wid * NA + k] = s;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < NA; k += NT) {
+        double s = buf[k];
+        for (int w = 1; w < NT / 32; ++w) s += buf[w * NA + k];
+        stash[k] = s;
+    }
+    __syncthreads();
+    const int nb = E.nb, ne = nb * (nb + 1) / 2;
+    const int ntot = ne + (P.screen_full ? nh : 0);
+    double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
+    for (int e = threadIdx.x; e < ntot; e += NT) {
+        int k;
+        if (e < ne) {
+            int aa = 0, rem = e;
+            while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
+            const int bb = aa + rem;
+            k = aa * NBX - aa * (aa - 1) / 2 + (bb - aa);
+        } else {
+            k = NE + nh + (e - ne);
+        }
+        out[e] = stash[k];
+    }
+    __syncthreads();
+    gram_tail_after(P, C, E, gmax, cnt, red, buf, 4096, stash, Gs);
+}
+
 // ---------------------------------------------------------------- launch
 static int g_bwd_occ = 0, g_bwdw_occ = 0;
 // k_bwd_c (TMA, CTA pairs) is opt-in: on C2 it measured 275-335 us vs 268 us for k_bwd_s
@@ -1050,6 +1294,7 @@ static bool g_no_tma = getenv("LBFGSB_TMA") == nullptr;
 // k_qepi (register Gram) is the QP / transport epilogue for m_hist <= 5; LBFGSB_NO_QEPI=1
 // selects the shared-memory tile kernel k_qpu instead (A/B experiments)
 static bool g_no_qepi = getenv("LBFGSB_NO_QEPI") != nullptr;
+static bool g_no_qepi_t = getenv("LBFGSB_NO_QEPI_T") != nullptr;   // register-Gram kernel without TMA staging
 constexpr int BWD_W_MAXM = 2048;
 constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + 64);
 static bool g_bwd_init = false;
@@ -1100,6 +1345,23 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         if (!occ) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qepi<11>, NT, 0);
             if (occ < 1) occ = 1;
+        }
+        // staged (TMA) variant when every staged vector is 16-byte aligned
+        bool al16 = true;
+        const void* ptrs[] = {P.x, P.l, P.u, P.g, P.pp, P.pt, P.c, P.rbuf[0], P.rbuf[1], P.q, P.S, P.Y};
+        for (const void* p : ptrs) al16 = al16 && ((reinterpret_cast<uintptr_t>(p) & 15u) == 0);
+        al16 = al16 && (P.n % 2 == 0);                          // S / Y slot starts stay aligned
+        if (al16 && !g_no_qepi_t && P.n >= QT) {
+            const size_t smem = sizeof(double) * 2 * (size_t)(8 + 2 * P.mh) * QT;
+            static size_t smem_set = 0;
+            if (smem_set < smem) {
+                cudaFuncSetAttribute(k_qepi_t<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                smem_set = smem;
+            }
+            int64_t g = (P.n + QT - 1) / QT;
+            if (g > sm_count()) g = sm_count();
+            k_qepi_t<11><<<(int)g, NT, smem, st>>>(P, mode);
+            return;
         }
         int64_t g = (P.n + NT - 1) / NT;
         const int64_t cap = (int64_t)sm_count() * occ;

@@ -1162,8 +1162,10 @@ extern "C" lbfgsb_err al_solve_transport(lbfgsb_t* h, const lbfgsb_objective* ob
         vlast = vv;
         if (g_al_trace)
             std::fprintf(stderr, "[al_transport] outer %d rho %.3e tol_in %.3e inner %lld status %d "
-                         "pg %.3e viol %.3e f %.15g\n", it, rho, tin, (long long)ir.iters, ir.status,
-                         ir.pg_inf, vv, h->hc->f_base);
+                         "pg %.3e viol %.3e f %.15g n_fg %lld n_bt %lld fallbacks %lld %.3fs\n", it, rho,
+                         tin, (long long)ir.iters, ir.status, ir.pg_inf, vv, h->hc->f_base,
+                         (long long)ir.n_fg, (long long)ir.n_backtracks, (long long)ir.n_fallbacks,
+                         ir.seconds);
         if (vv > 0.5 * vprev) {                                        // line 8 (R20)
             rho = rho * ao.rho_factor;
             if (rho > ao.rho_cap) rho = ao.rho_cap;
