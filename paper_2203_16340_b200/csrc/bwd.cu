@@ -1085,175 +1085,154 @@ __global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* r
 // of QT variables; thread 0 issues one bulk copy per input vector per tile
 // into a 2-stage ring (mbarrier complete_tx), so ~QT * nvec * 8 bytes per SM
 // are in flight independently of the (register-heavy) consumer threads.
-// Inputs per tile: x, l, u, [g, p] (iteration), [c], [w, q] (QP), the S / Y
-// columns of every pair except the one this iteration overwrites.  The
-// partial last tile (n % QT variables) is read directly from global memory.
+// The body is instantiated per history length NH = C->nh (0..5, a uniform
+// switch at kernel entry): the Gram basis (S_0..S_{NH-1}, Y_0..Y_{NH-1}, g)
+// and its (2NH+1)(2NH+2)/2 + 2NH+1 accumulators are compile-time, and in an
+// iteration the newest pair (basis NH-1 and 2NH-1, the ring slot this
+// iteration writes) comes from registers.  Staged slots: 0 x, 1 l, 2 u, 3 g,
+// 4 p, 5 c, 6 w, 7 q (QP), 8 + b the b-th Gram basis vector.  The partial
+// last tile (n % QT variables) is read directly from global memory.
 constexpr int QT = 512;                      // variables per tile (2 per thread)
-constexpr int QV_MAX = 8 + 2 * MAXH;         // staged vectors per tile (upper bound)
+constexpr int QMH = 5;                       // largest m_hist with a k_qepi_t instance
+constexpr int QV = 8 + 2 * QMH;              // staged vector slots per tile
 
-template <int NBX>
-__global__ void __launch_bounds__(NT, 1) k_qepi_t(Prob P, int mode)
+struct QCtx {
+    const double* wcur;
+    double* wnext;
+    double alpha, rho;
+    bool small;
+};
+
+template <int NH, bool GRAM, bool ITER, bool STAGED>
+__device__ __forceinline__ void qepi_elem(const Prob& P, const Ctrl* C, const EpiCtx& E, const QCtx& Q,
+                                          const double* base, const double* const* vsrc, int e,
+                                          int64_t v, double* acc, double& gmax, double& cnt)
 {
-    Ctrl* C = P.ctrl;
-    if (mode == BWD_ITER && halted(C)) return;
-    constexpr int NE = NBX * (NBX + 1) / 2, NA = NE + NBX;
-    extern __shared__ __align__(128) double stg[];           // [2][nvec][QT]
-    __shared__ double red[NT / 32];
-    __shared__ double stash[NT];
-    __shared__ double Gs[MAXE + MAXH + 2];
-    __shared__ double buf[NT / 32 * NA > 4096 ? NT / 32 * NA : 4096];
-    __shared__ const double* vsrc[QV_MAX];
-    __shared__ int vslot_b[2 * MAXH];                        // staged slot of Gram vector b (-1: cur)
-    __shared__ __align__(8) uint64_t full_bar[2];
-    const bool iter = mode == BWD_ITER;
-    const double* wcur = P.rbuf[C->rsel];
-    double* wnext = P.rbuf[C->rsel ^ 1];
-    const double alpha = iter ? C->alpha : 0.0;
-    const double rho = C->rho;
-    EpiCtx E;
-    epi_init(P, C, mode, E);
-    const int64_t n = P.n;
-    const int nh = E.nh;
-    // staged vector list (same order in every CTA)
-    enum { VX = 0, VL = 1, VU = 2, VG = 3, VP = 4, VC = 5, VW = 6, VQ = 7 };
-    if (threadIdx.x == 0) {
-        vsrc[VX] = P.x; vsrc[VL] = P.l; vsrc[VU] = P.u;
-        vsrc[VG] = iter ? P.g : nullptr;
-        vsrc[VP] = iter ? (E.branch ? P.pp : P.pt) : nullptr;
-        vsrc[VC] = P.c;
-        vsrc[VW] = P.qp ? wcur : nullptr;
-        vsrc[VQ] = (P.qp && iter) ? P.q : nullptr;
-        int k = 8;
-        for (int b = 0; b < 2 * nh; ++b) {
-            const int bb = b < nh ? b : b - nh;
-            const bool cur = E.iter && ring_slot(E.head, nh, bb, E.mh) == E.slot;
-            if (!E.gram || cur) { vslot_b[b] = -1; continue; }
-            vslot_b[b] = k;
-            vsrc[k++] = E.bptr[b];
+    constexpr int NB = 2 * NH + 1, NE = NB * (NB + 1) / 2;
+    auto ld = [&](int k) -> double { return STAGED ? base[k * QT + e] : vsrc[k][v]; };
+    const double xo = ld(0), lv = ld(1), uv = ld(2);
+    const double go = ITER ? ld(3) : 0.0;
+    const double pv = ITER ? ld(4) : 0.0;
+    const double cv = P.c ? ld(5) : 0.0;
+    double bv[NB];
+    if (GRAM) {
+#pragma unroll
+        for (int b = 0; b < 2 * NH; ++b)
+            if (!(ITER && (b == NH - 1 || b == 2 * NH - 1))) bv[b] = ld(8 + b);
+    }
+    double w;
+    if (P.tp) {
+        int64_t i, j;
+        if (Q.small) {
+            const unsigned vv = (unsigned)v, tmu = (unsigned)P.tm;
+            j = vv / tmu; i = vv - (unsigned)j * tmu;
+        } else {
+            j = v / P.tm; i = v - j * P.tm;
         }
-        for (; k < QV_MAX; ++k) vsrc[k] = nullptr;
-        mbar_init(&full_bar[0], 1);
-        mbar_init(&full_bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const int64_t kj = P.tm + j;
+        double hi = Q.wcur[i], hj = Q.wcur[kj];
+        if (ITER) { hi = fma(Q.alpha, P.tap[i], hi); hj = fma(Q.alpha, P.tap[kj], hj); }
+        w = (Q.rho * hi + P.tlam[i]) + (Q.rho * hj + P.tlam[kj]);
+    } else {
+        w = ld(6);
+        if (ITER) {
+            w = fma(Q.alpha, ld(7), w);                         // carried w' = Q~ x'
+            Q.wnext[v] = w;
+        }
     }
-    __syncthreads();
-    const int nvec = 8 + 2 * nh;                              // slot stride (some slots unused)
-    const int64_t nfull = n / QT;
-    const int64_t ntiles = (n + QT - 1) / QT;
-    unsigned bytes_tile = 0;
-    for (int k = 0; k < nvec; ++k) if (vsrc[k]) bytes_tile += QT * 8;
-    auto issue = [&](int64_t t, int sidx) {                  // thread 0 only
-        double* base = stg + (size_t)sidx * nvec * QT;
-        mbar_arrive_tx(&full_bar[sidx], bytes_tile);
-        for (int k = 0; k < nvec; ++k)
-            if (vsrc[k]) bulk_g2s(base + (size_t)k * QT, vsrc[k] + t * QT, QT * 8, &full_bar[sidx]);
-    };
-    if (P.tp && iter) {                                         // carried h' = h + alpha A p (N2)
-        const int64_t K = P.tm + P.tn;
-        for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < K; k += (int64_t)gridDim.x * NT)
-            wnext[k] = fma(alpha, P.tap[k], wcur[k]);
+    const double xn = ITER ? clipd(fma(Q.alpha, pv, xo), lv, uv) : xo;   // Alg. 1 line 7
+    double gn = w;
+    if (P.c) gn = gn + cv;
+    gn = gn + P.delta * xn;
+    if (P.ent != 0.0) gn = gn + P.ent * (log(xn) + 1.0);
+    for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * P.Ecol[k][v];
+    double sv = 0.0, yv = 0.0;
+    if (ITER) {
+        const int64_t so = (int64_t)E.slot * P.n + v;
+        sv = xn - xo;                                           // s^k
+        yv = gn - go;                                           // y^k
+        P.S[so] = sv;
+        P.Y[so] = yv;
     }
+    P.x[v] = xn;
+    P.g[v] = gn;
+    const bool fixed = (xn <= lv + P.eps && gn >= 0.0) || (xn >= uv - P.eps && gn <= 0.0);
+    P.mask[v] = fixed ? 0 : 1;                                  // S^{k+1}, Eq. (1)
+    if (!fixed) {
+        const double ag = fabs(gn);
+        gmax = ag > gmax ? ag : gmax;
+        cnt += 1.0;
+    }
+    if (!GRAM) return;
+    if (ITER && NH > 0) { bv[NH - 1] = sv; bv[2 * NH - 1] = yv; }
+    bv[2 * NH] = gn;
+    int idx = 0;
+#pragma unroll
+    for (int a = 0; a < NB; ++a) {
+        const double ma = fixed ? 0.0 : bv[a];
+#pragma unroll
+        for (int b = a; b < NB; ++b) {
+            acc[idx] = fma(ma, bv[b], acc[idx]);
+            ++idx;
+        }
+    }
+    if (P.screen_full) {
+#pragma unroll
+        for (int k = 0; k < NH; ++k) acc[NE + k] = fma(bv[NH + k], bv[NH + k], acc[NE + k]);
+    }
+}
+
+template <int NH, bool GRAM>
+__device__ __forceinline__ void qepi_body(const Prob& P, Ctrl* C, const EpiCtx& E, const QCtx& Q,
+                                          double* stg, uint64_t* full_bar, const double* const* vsrc,
+                                          bool iter, double* buf, double* stash, double& gmax,
+                                          double& cnt)
+{
+    constexpr int NB = 2 * NH + 1, NE = NB * (NB + 1) / 2, NA = NE + NH;
     double acc[NA];
 #pragma unroll
     for (int k = 0; k < NA; ++k) acc[k] = 0.0;
-    double gmax = 0.0, cnt = 0.0;
-    const bool small = n < (1LL << 31);
-    // prologue: first full tile of this CTA
-    int64_t t0 = blockIdx.x;
-    if (threadIdx.x == 0 && t0 < nfull) issue(t0, 0);
+    const int64_t n = P.n;
+    const int64_t nfull = n / QT, ntiles = (n + QT - 1) / QT;
+    unsigned bytes_tile = 0;
+    for (int k = 0; k < QV; ++k) if (vsrc[k]) bytes_tile += QT * 8;
+    auto issue = [&](int64_t t, int sidx) {                  // thread 0 only
+        double* base = stg + (size_t)sidx * QV * QT;
+        mbar_arrive_tx(&full_bar[sidx], bytes_tile);
+        for (int k = 0; k < QV; ++k)
+            if (vsrc[k]) bulk_g2s(base + (size_t)k * QT, vsrc[k] + t * QT, QT * 8, &full_bar[sidx]);
+    };
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < nfull) issue(blockIdx.x, 0);
     int li = 0;
-    for (int64_t t = t0; t < ntiles; t += gridDim.x, ++li) {
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
         const int sidx = li & 1;
-        const bool staged = t < nfull;
-        if (staged) {
+        const double* base = stg + (size_t)sidx * QV * QT;
+        if (t < nfull) {
             const int64_t tn = t + gridDim.x;                   // prefetch the next tile
             if (threadIdx.x == 0 && tn < nfull) issue(tn, sidx ^ 1);
             mbar_wait(&full_bar[sidx], (unsigned)((li >> 1) & 1));
-        }
-        const double* base = stg + (size_t)sidx * nvec * QT;
 #pragma unroll 1
-        for (int e = threadIdx.x; e < QT; e += NT) {
-            const int64_t v = t * QT + e;
-            if (v >= n) break;
-            auto ld = [&](int k) -> double { return staged ? base[(size_t)k * QT + e] : vsrc[k][v]; };
-            const double xo = ld(VX), lv = ld(VL), uv = ld(VU);
-            const double pv = iter ? ld(VP) : 0.0;
-            const double go = iter ? ld(VG) : 0.0;
-            const double cv = P.c ? ld(VC) : 0.0;
-            double w;
-            if (P.tp) {
-                int64_t i, j;
-                if (small) {
-                    const unsigned vv = (unsigned)v, tmu = (unsigned)P.tm;
-                    j = vv / tmu; i = vv - (unsigned)j * tmu;
-                } else {
-                    j = v / P.tm; i = v - j * P.tm;
-                }
-                const int64_t kj = P.tm + j;
-                double hi = wcur[i], hj = wcur[kj];
-                if (iter) { hi = fma(alpha, P.tap[i], hi); hj = fma(alpha, P.tap[kj], hj); }
-                w = (rho * hi + P.tlam[i]) + (rho * hj + P.tlam[kj]);
-            } else {
-                w = ld(VW);
-                if (iter) {
-                    w = fma(alpha, ld(VQ), w);                  // carried w' = Q~ x'
-                    wnext[v] = w;
-                }
+            for (int e = threadIdx.x; e < QT; e += NT) {
+                const int64_t v = t * QT + e;
+                if (iter) qepi_elem<NH, GRAM, true, true>(P, C, E, Q, base, vsrc, e, v, acc, gmax, cnt);
+                else qepi_elem<NH, GRAM, false, true>(P, C, E, Q, base, vsrc, e, v, acc, gmax, cnt);
             }
-            const double xn = iter ? clipd(fma(alpha, pv, xo), lv, uv) : xo;   // Alg. 1 line 7
-            double gn = w;
-            if (P.c) gn = gn + cv;
-            gn = gn + P.delta * xn;
-            if (P.ent != 0.0) gn = gn + P.ent * (log(xn) + 1.0);
-            for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * P.Ecol[k][v];
-            double sv = 0.0, yv = 0.0;
-            if (iter) {
-                const int64_t so = (int64_t)E.slot * n + v;
-                sv = xn - xo;                                   // s^k
-                yv = gn - go;                                   // y^k
-                P.S[so] = sv;
-                P.Y[so] = yv;
+        } else {
+#pragma unroll 1
+            for (int e = threadIdx.x; e < QT; e += NT) {
+                const int64_t v = t * QT + e;
+                if (v >= n) break;
+                if (iter) qepi_elem<NH, GRAM, true, false>(P, C, E, Q, base, vsrc, e, v, acc, gmax, cnt);
+                else qepi_elem<NH, GRAM, false, false>(P, C, E, Q, base, vsrc, e, v, acc, gmax, cnt);
             }
-            P.x[v] = xn;
-            P.g[v] = gn;
-            const bool fixed = (xn <= lv + P.eps && gn >= 0.0) || (xn >= uv - P.eps && gn <= 0.0);
-            P.mask[v] = fixed ? 0 : 1;                          // S^{k+1}, Eq. (1)
-            if (!fixed) {
-                const double ag = fabs(gn);
-                gmax = ag > gmax ? ag : gmax;
-                cnt += 1.0;
-            }
-            if (!E.gram) continue;
-            double bv[NBX];
-#pragma unroll
-            for (int b = 0; b < NBX; ++b) {
-                double val = 0.0;
-                if (b < 2 * nh) {
-                    const int k = vslot_b[b];
-                    val = k < 0 ? (b < nh ? sv : yv) : ld(k);
-                } else if (b == 2 * nh) {
-                    val = gn;
-                }
-                bv[b] = val;
-            }
-            int idx = 0;
-#pragma unroll
-            for (int a = 0; a < NBX; ++a) {
-                const double ma = fixed ? 0.0 : bv[a];
-#pragma unroll
-                for (int b = a; b < NBX; ++b) {
-                    acc[idx] = fma(ma, bv[b], acc[idx]);
-                    ++idx;
-                }
-            }
-#pragma unroll
-            for (int b = 0; b < NBX; ++b) acc[NE + b] = fma(bv[b], bv[b], acc[NE + b]);
         }
         // every thread is done with this stage before it is refilled (two tiles on)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
     }
-    if (!E.gram) return;
+    if (!GRAM) return;
+    // CTA reduction (warps in order) and this CTA's partial in gram_tail's
+    // enumeration: (a <= b < NB) row-major, then the unmasked ||y_k||^2
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int k = 0; k < NA; ++k) {
@@ -1261,28 +1240,71 @@ __global__ void __launch_bounds__(NT, 1) k_qepi_t(Prob P, int mode)
         if (lane == 0) buf[wid * NA + k] = s;
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < NA; k += NT) {
+    const int ntot = NE + (P.screen_full ? NH : 0);
+    double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
+    for (int k = threadIdx.x; k < ntot; k += NT) {
         double s = buf[k];
         for (int w = 1; w < NT / 32; ++w) s += buf[w * NA + k];
-        stash[k] = s;
+        out[k] = s;
     }
     __syncthreads();
-    const int nb = E.nb, ne = nb * (nb + 1) / 2;
-    const int ntot = ne + (P.screen_full ? nh : 0);
-    double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
-    for (int e = threadIdx.x; e < ntot; e += NT) {
-        int k;
-        if (e < ne) {
-            int aa = 0, rem = e;
-            while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
-            const int bb = aa + rem;
-            k = aa * NBX - aa * (aa - 1) / 2 + (bb - aa);
-        } else {
-            k = NE + nh + (e - ne);
+}
+
+__global__ void __launch_bounds__(NT, 1) k_qepi_t(Prob P, int mode)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    extern __shared__ __align__(128) double stg[];           // [2][QV][QT]
+    __shared__ double red[NT / 32];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    __shared__ double buf[4096];
+    __shared__ const double* vsrc[QV];
+    __shared__ __align__(8) uint64_t full_bar[2];
+    const bool iter = mode == BWD_ITER;
+    QCtx Q;
+    Q.wcur = P.rbuf[C->rsel];
+    Q.wnext = P.rbuf[C->rsel ^ 1];
+    Q.alpha = iter ? C->alpha : 0.0;
+    Q.rho = C->rho;
+    Q.small = P.n < (1LL << 31);
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    const int nh = E.nh;
+    if (threadIdx.x == 0) {
+        vsrc[0] = P.x; vsrc[1] = P.l; vsrc[2] = P.u;
+        vsrc[3] = iter ? P.g : nullptr;
+        vsrc[4] = iter ? (E.branch ? P.pp : P.pt) : nullptr;
+        vsrc[5] = P.c;
+        vsrc[6] = P.qp ? Q.wcur : nullptr;
+        vsrc[7] = (P.qp && iter) ? P.q : nullptr;
+        for (int b = 0; b < 2 * QMH; ++b) {
+            const bool cur = iter && (b == nh - 1 || b == 2 * nh - 1);
+            vsrc[8 + b] = (E.gram && b < 2 * nh && !cur) ? E.bptr[b] : nullptr;
         }
-        out[e] = stash[k];
+        mbar_init(&full_bar[0], 1);
+        mbar_init(&full_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (P.tp && iter) {                                         // carried h' = h + alpha A p (N2)
+        const int64_t K = P.tm + P.tn;
+        for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < K; k += (int64_t)gridDim.x * NT)
+            Q.wnext[k] = fma(Q.alpha, P.tap[k], Q.wcur[k]);
+    }
+    double gmax = 0.0, cnt = 0.0;
+    if (!E.gram) {
+        qepi_body<0, false>(P, C, E, Q, stg, full_bar, vsrc, iter, buf, stash, gmax, cnt);
+        return;
+    }
+    switch (nh) {
+        case 0: qepi_body<0, true>(P, C, E, Q, stg, full_bar, vsrc, iter, buf, stash, gmax, cnt); break;
+        case 1: qepi_body<1, true>(P, C, E, Q, stg, full_bar, vsrc, iter, buf, stash, gmax, cnt); break;
+        case 2: qepi_body<2, true>(P, C, E, Q, stg, full_bar, vsrc, iter, buf, stash, gmax, cnt); break;
+        case 3: qepi_body<3, true>(P, C, E, Q, stg, full_bar, vsrc, iter, buf, stash, gmax, cnt); break;
+        case 4: qepi_body<4, true>(P, C, E, Q, stg, full_bar, vsrc, iter, buf, stash, gmax, cnt); break;
+        default: qepi_body<5, true>(P, C, E, Q, stg, full_bar, vsrc, iter, buf, stash, gmax, cnt); break;
+    }
     gram_tail_after(P, C, E, gmax, cnt, red, buf, 4096, stash, Gs);
 }
 
@@ -1352,15 +1374,15 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         for (const void* p : ptrs) al16 = al16 && ((reinterpret_cast<uintptr_t>(p) & 15u) == 0);
         al16 = al16 && (P.n % 2 == 0);                          // S / Y slot starts stay aligned
         if (al16 && !g_no_qepi_t && P.n >= QT) {
-            const size_t smem = sizeof(double) * 2 * (size_t)(8 + 2 * P.mh) * QT;
-            static size_t smem_set = 0;
-            if (smem_set < smem) {
-                cudaFuncSetAttribute(k_qepi_t<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                smem_set = smem;
+            const size_t smem = sizeof(double) * 2 * (size_t)QV * QT;
+            static bool smem_set = false;
+            if (!smem_set) {
+                cudaFuncSetAttribute(k_qepi_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                smem_set = true;
             }
             int64_t g = (P.n + QT - 1) / QT;
             if (g > sm_count()) g = sm_count();
-            k_qepi_t<11><<<(int)g, NT, smem, st>>>(P, mode);
+            k_qepi_t<<<(int)g, NT, smem, st>>>(P, mode);
             return;
         }
         int64_t g = (P.n + NT - 1) / NT;

@@ -53,6 +53,7 @@ struct Ctrl {
     long long n_fg, n_bt, n_fallbacks, nfree;
     long long nact;         // sum over iterations of active columns read by k_fwd
     int done, status, stall, nh, head, branch, fallback, ls_batch;
+    int ls_tried, cont;     // trials evaluated this search; 1: device-side continuation pending (N2)
     int slot;               // ring slot the current iteration writes
     int nonfinite;
     int rsel;               // which residual buffer holds r(x^k)
@@ -156,7 +157,7 @@ enum FwdMode : int { FWD_ITER = 0, FWD_SETUP = 1, FWD_P = 2 };
 enum BwdMode : int { BWD_ITER = 0, BWD_SETUP = 1, BWD_PLAIN = 2, BWD_REFRESH = 3 };
 enum SepMode : int { SEP_ITER = 0, SEP_NEXT = 1, SEP_SETUP = 2, SEP_OP = 3 };
 enum LsMode : int { LS_NEXT = 0, LS_OP = 1, LS_SH_ITER = 2, LS_SH_SETUP = 3 };
-enum TsMode : int { TS_ITER = 0, TS_NEXT = 1, TS_SETUP = 2 };
+enum TsMode : int { TS_ITER = 0, TS_NEXT = 1, TS_SETUP = 2, TS_CONT = 3 };
 constexpr int TCOLS = 16;                  // k_tsum columns per CTA
 constexpr int TT = 4;                      // entropy Armijo trials per batch
 constexpr int TNS = 3 + TT;                // k_tsum per-CTA sums

@@ -39,6 +39,8 @@ __device__ __forceinline__ void dir_decide(const Prob& P, Ctrl* C, const double*
     C->amax = amax;
     C->alpha0 = amax < 1.0 ? amax : 1.0;                        // R10
     C->ls_batch = 0;
+    C->ls_tried = 0;
+    C->cont = 0;
     if (op_mode) return;
     if (!(gp < 0.0)) {                                          // guard (R14)
         if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }

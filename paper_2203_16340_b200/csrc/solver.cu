@@ -551,7 +551,7 @@ static void rec_event(Group& g, int idx)
 static int per_iteration_launches(const Group& g)
 {
     const int sep = g.Ps[0].GS > 0;
-    if (g.Ps[0].tp) return 3;
+    if (g.Ps[0].tp) return g.Ps[0].ent != 0.0 ? 4 : 3;
     return g.sharded ? (int)g.hs.size() * (6 + sep) : 3 + sep;
 }
 
@@ -566,6 +566,7 @@ static lbfgsb_err launch_iteration(Group& g, int ev_base)
         launch_dir(P, st, 0);
         rec_event(g, ev_base >= 0 ? ev_base + 0 : -1);
         launch_tsum(P, st, TS_ITER);
+        if (P.ent != 0.0) launch_tsum(P, st, TS_CONT);          // no-op unless trial 0 failed
         rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);
         rec_event(g, ev_base >= 0 ? ev_base + 2 : -1);
         launch_bwd(P, st, BWD_ITER, nullptr, nullptr);

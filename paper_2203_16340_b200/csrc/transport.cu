@@ -24,6 +24,22 @@ namespace lb {
 
 __device__ __forceinline__ double xlogx_d(double x) { return x > 0.0 ? x * log(x) : 0.0; }
 
+// sum_{c < cnt} p[c * stride] in ascending c, 8 loads in flight (L2-resident partials)
+__device__ __forceinline__ double sum_strided(const double* p, int64_t stride, int cnt)
+{
+    double a = 0.0;
+    int c = 0;
+    for (; c + 8 <= cnt; c += 8) {
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = __ldcg(p + (int64_t)(c + q) * stride);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a += t[q];
+    }
+    for (; c < cnt; ++c) a += __ldcg(p + (int64_t)c * stride);
+    return a;
+}
+
 // last of `total` arrivals where this CTA contributes `nf` arrivals
 __device__ __forceinline__ bool last_of(unsigned* ticket, unsigned total, unsigned nf)
 {
@@ -41,36 +57,48 @@ __device__ __forceinline__ bool last_of(unsigned* ticket, unsigned total, unsign
 }
 
 // Armijo decision in the difference form (R29) for the transport objective;
-// S = (c^T p, x^T p, p^T p, E_0..E_{TT-1}) and Sta, Saa the AL sums.
-__device__ void transport_decide(const Prob& P, Ctrl* C, const double* S, double Sta, double Saa)
+// S = (c^T p, x^T p, p^T p, E_0..E_{ntr-1}) and Sta, Saa the AL sums.  The
+// Gaussian case is closed form in alpha: all max_bt + 1 trials at once.  The
+// entropy needs per-trial sums: ntr of them per pass (1 in the iteration's
+// pass, TT in a continuation pass); a failed pass continues on the device
+// (cont = 1: the graph's k_tsum(TS_CONT) runs next) or through the host
+// (stall), until max_bt + 1 trials have failed (R14 fallback).
+__device__ void transport_decide(const Prob& P, Ctrl* C, const double* S, double Sta, double Saa,
+                                 int ntr, bool allow_cont)
 {
     const double rho = C->rho;
     const double lin = S[0] + P.delta * S[1] + rho * Sta;
     const double qua = P.delta * S[2] + rho * Saa;
     double a = C->alpha0;
     const bool ent = P.ent != 0.0;
-    const int ntr = ent ? TT : P.max_bt + 1;
+    if (!ent) ntr = P.max_bt + 1;
+    int tried = 0;
     for (int t = 0; t < ntr; ++t) {
         if (t > 0) a = a * P.shrink;
-        if (C->ls_batch * TT + t > P.max_bt && ent) break;
+        if (C->ls_tried + t > P.max_bt) break;
+        ++tried;
         double dl = a * lin + 0.5 * a * a * qua;
         if (ent) dl += P.ent * S[3 + t];
         if (dl <= P.c1 * a * C->gp) {
             C->alpha = a;
             C->f = C->f + dl;
             C->f_new = C->f;
+            C->n_fg += C->ls_tried;
+            C->n_bt += C->ls_tried;
             accept_step(P, C, t);
             return;
         }
     }
-    C->n_fg += ntr;
-    C->n_bt += ntr;
-    if (ent && (C->ls_batch + 1) * TT <= P.max_bt) {         // next batch of TT trials
+    C->ls_tried += tried;
+    if (ent && C->ls_tried <= P.max_bt) {                    // more trials remain
         C->alpha0 = a * P.shrink;
         C->ls_batch += 1;
-        C->stall = ST_LS_CONT;
+        if (allow_cont) C->cont = 1;
+        else C->stall = ST_LS_CONT;
         return;
     }
+    C->n_fg += C->ls_tried;
+    C->n_bt += C->ls_tried;
     if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }
     else C->stall = ST_FALLBACK;
 }
@@ -80,6 +108,9 @@ __global__ void __launch_bounds__(NT) k_tsum(Prob P, int mode)
     Ctrl* C = P.ctrl;
     const bool setup = mode == TS_SETUP;
     if (!setup && halted(C)) return;
+    if (mode == TS_CONT && !C->cont) return;                  // no device-side continuation pending
+    // trials this pass: 1 in the iteration (usually accepted), TT in a continuation
+    const int ntr = mode == TS_ITER ? 1 : TT;
     __shared__ double tile[TCOLS][NT + 1];
     constexpr int NPART = NT / TCOLS, PROWS = NT / NPART;     // column reduction split
     __shared__ double cpart[NPART][TCOLS];
@@ -122,6 +153,7 @@ __global__ void __launch_bounds__(NT) k_tsum(Prob P, int mode)
                     const double lx = xv > 0.0 ? log(xv) : 0.0;
 #pragma unroll
                     for (int t = 0; t < TT; ++t) {
+                        if (t >= ntr) break;
                         // y log y - x log x = d log x + y log(y/x) (oracle armijo_delta)
                         const double y = clipd(fma(al[t], pj, xv), lv, uv), d = y - xv;
                         if (xv > 0.0 && y > 0.0) {
@@ -164,8 +196,7 @@ __global__ void __launch_bounds__(NT) k_tsum(Prob P, int mode)
     if (fr) {
         double v2[2] = {0.0, 0.0};
         if (rok) {
-            double a = 0.0;
-            for (int c = 0; c < P.TCB; ++c) a += __ldcg(P.trow + (int64_t)c * tm + i);
+            const double a = sum_strided(P.trow + i, tm, P.TCB);
             if (setup) {
                 const double hk = a - P.te[i];
                 P.rbuf[C->rsel][i] = hk;
@@ -188,8 +219,7 @@ __global__ void __launch_bounds__(NT) k_tsum(Prob P, int mode)
         double v2[2] = {0.0, 0.0};
         if ((int)threadIdx.x < ncol) {
             const int64_t j = j0 + threadIdx.x, k = tm + j;
-            double a = 0.0;
-            for (int r = 0; r < P.TRB; ++r) a += __ldcg(P.tcol + (int64_t)r * tn + j);
+            const double a = sum_strided(P.tcol + j, tn, P.TRB);
             if (setup) {
                 const double hk = a - P.te[k];
                 P.rbuf[C->rsel][k] = hk;
@@ -223,7 +253,8 @@ __global__ void __launch_bounds__(NT) k_tsum(Prob P, int mode)
         C->nonfinite = isfinite(f) ? 0 : 1;
         return;
     }
-    transport_decide(P, C, S, R2[0] + Q2[0], R2[1] + Q2[1]);
+    if (mode == TS_CONT) C->cont = 0;                         // every CTA has read it by now
+    transport_decide(P, C, S, R2[0] + Q2[0], R2[1] + Q2[1], ntr, mode == TS_ITER);
 }
 
 // AL bookkeeping on the device residual h = rbuf[rsel] (Alg. 4 line 6):
