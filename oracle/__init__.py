@@ -109,6 +109,10 @@ def _setup(L):
     L.orc_lsq_grad.argtypes = [C.POINTER(_Lsq), _dp, _dp]
     L.orc_armijo_delta.argtypes = [C.POINTER(_Lsq), i64, _dp, _dp, _dp, _dp, _dp, _dp, d]
     L.orc_armijo_delta.restype = d
+    L.orc_compact_m.argtypes = [i64, i32, _dp, _dp, d, _dp]
+    L.orc_compact_m.restype = i32
+    L.orc_cauchy_point.argtypes = [i64, _dp, _dp, _dp, _dp, i32, _dp, _dp, d, _dp, _dp]
+    L.orc_cauchy_point.restype = i64
     L.orc_armijo_scalar_quadratic.argtypes = [d, d, d, d, d, i32]
     L.orc_armijo_scalar_quadratic.restype = d
 
@@ -207,6 +211,38 @@ def max_step(x, p, l, u):
 def check_convergence(g, free, tol):
     g = _f64(g); fr = _u8(free)
     return bool(_L().orc_check_convergence(g.size, _ptr(g), fr.ctypes.data_as(_u8p), tol))
+
+
+def compact_m(S, Y, theta):
+    """M of the compact L-BFGS form B = theta I - W M W^T, W = [Y, theta S]
+    (Byrd-Lu-Nocedal-Zhu 1995).  S, Y: (h, n) pairs, oldest first."""
+    S = np.ascontiguousarray(S, dtype=np.float64); Y = np.ascontiguousarray(Y, dtype=np.float64)
+    h, n = S.shape
+    M = np.zeros((2 * h, 2 * h))
+    rc = _L().orc_compact_m(n, h, _ptr(S), _ptr(Y), float(theta), _ptr(M))
+    if rc:
+        raise np.linalg.LinAlgError("singular middle matrix")
+    return M
+
+
+def cauchy_point(x, g, l, u, S=None, Y=None, theta=1.0):
+    """Generalized Cauchy point of the original L-BFGS-B (Algorithm CP of
+    Byrd et al. 1995; the step PAPER.md:19-23, 436-440 removes).  Returns
+    (xcp, c = W^T (xcp - x), number of breakpoints passed)."""
+    x = _f64(x); g = _f64(g); n = len(x)
+    l = None if l is None else _f64(np.broadcast_to(l, (n,)))
+    u = None if u is None else _f64(np.broadcast_to(u, (n,)))
+    if S is None or len(S) == 0:
+        h = 0; Sp = np.zeros((1, n)); Yp = np.zeros((1, n))
+    else:
+        Sp = np.ascontiguousarray(S, dtype=np.float64); Yp = np.ascontiguousarray(Y, dtype=np.float64)
+        h = Sp.shape[0]
+    xcp = np.empty(n); c = np.zeros(max(2 * h, 1))
+    passed = _L().orc_cauchy_point(n, _ptr(x), _ptr(g), _ptr(l), _ptr(u), h, _ptr(Sp), _ptr(Yp),
+                                   float(theta), _ptr(xcp), _ptr(c))
+    if passed < 0:
+        raise np.linalg.LinAlgError("singular middle matrix")
+    return xcp, c[:2 * h], int(passed)
 
 
 def armijo_scalar_quadratic(x, p, amax=1.0, c1=1e-4, shrink=0.5, max_bt=50):

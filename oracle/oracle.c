@@ -741,3 +741,157 @@ double orc_armijo_scalar_quadratic(double x, double p, double amax, double c1, d
     }
     return -1.0;
 }
+
+/* ------------------------------------------------------------------ */
+/* the generalized Cauchy point of the ORIGINAL        */
+/* L-BFGS-B (Byrd, Lu, Nocedal, Zhu 1995, Algorithm CP), the step the   */
+/* paper removes ("The Cauchy point is         */
+/* computed by minimizing a quadratic approximation over the gradient   */
+/* projection path").  Compact form B = theta I - W M W^T, W = [Y, theta */
+/* S] (n x 2h), M = [[-D, L^T], [L, theta S^T S]]^{-1}, D = diag(s_i^T   */
+/* y_i), L_ij = s_i^T y_j (i > j).  Pairs oldest first, column i of S at */
+/* S + i n.  Breakpoints are visited in increasing (t_i, i) order.       */
+/* ------------------------------------------------------------------ */
+static int invert_small(int k, double* A /* k x k row-major, in: A, out: A^{-1} */)
+{
+    double* T = (double*)calloc((size_t)(k * 2 * k > 0 ? k * 2 * k : 1), sizeof(double));
+    for (int i = 0; i < k; ++i) {
+        for (int j = 0; j < k; ++j) T[i * 2 * k + j] = A[i * k + j];
+        T[i * 2 * k + k + i] = 1.0;
+    }
+    for (int c = 0; c < k; ++c) {                     /* Gauss-Jordan, partial pivoting */
+        int piv = c;
+        for (int r = c + 1; r < k; ++r)
+            if (fabs(T[r * 2 * k + c]) > fabs(T[piv * 2 * k + c])) piv = r;
+        if (T[piv * 2 * k + c] == 0.0) { free(T); return 1; }
+        if (piv != c)
+            for (int j = 0; j < 2 * k; ++j) {
+                const double t = T[c * 2 * k + j]; T[c * 2 * k + j] = T[piv * 2 * k + j]; T[piv * 2 * k + j] = t;
+            }
+        const double dv = T[c * 2 * k + c];
+        for (int j = 0; j < 2 * k; ++j) T[c * 2 * k + j] /= dv;
+        for (int r = 0; r < k; ++r) {
+            if (r == c) continue;
+            const double f = T[r * 2 * k + c];
+            if (f == 0.0) continue;
+            for (int j = 0; j < 2 * k; ++j) T[r * 2 * k + j] -= f * T[c * 2 * k + j];
+        }
+    }
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) A[i * k + j] = T[i * 2 * k + k + j];
+    free(T);
+    return 0;
+}
+
+/* M (2h x 2h, row-major) of the compact representation */
+int32_t orc_compact_m(int64_t n, int32_t h, const double* S, const double* Y, double theta, double* M)
+{
+    const int k = 2 * h;
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < h; ++j) {
+            const double sy = dotv(n, S + (int64_t)i * n, Y + (int64_t)j * n);
+            const double ss = dotv(n, S + (int64_t)i * n, S + (int64_t)j * n);
+            M[i * k + j] = (i == j) ? -sy : 0.0;                       /* -D */
+            M[(h + i) * k + j] = (i > j) ? sy : 0.0;                   /* L */
+            M[j * k + h + i] = (i > j) ? sy : 0.0;                     /* L^T */
+            M[(h + i) * k + h + j] = theta * ss;                       /* theta S^T S */
+        }
+    return invert_small(k, M);
+}
+
+/* out = M v (2h) */
+static void mat_vec_small(int k, const double* M, const double* v, double* out)
+{
+    for (int i = 0; i < k; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < k; ++j) s += M[i * k + j] * v[j];
+        out[i] = s;
+    }
+}
+
+typedef struct { double t; int64_t i; } orc_bp;
+static int bp_cmp(const void* a, const void* b)
+{
+    const orc_bp* x = (const orc_bp*)a; const orc_bp* y = (const orc_bp*)b;
+    if (x->t < y->t) return -1;
+    if (x->t > y->t) return 1;
+    return x->i < y->i ? -1 : (x->i > y->i ? 1 : 0);
+}
+
+/* Algorithm CP.  xcp (n) out; c (2h) out = W^T (xcp - x); returns the number
+ * of breakpoints passed (the sequential loop's trip count), or -1 if M is
+ * singular. */
+int64_t orc_cauchy_point(int64_t n, const double* x, const double* g, const double* l, const double* u,
+                         int32_t h, const double* S, const double* Y, double theta, double* xcp, double* c)
+{
+    const int k = 2 * h;
+    double* M = (double*)calloc((size_t)(k * k > 0 ? k * k : 1), sizeof(double));
+    if (h > 0 && orc_compact_m(n, h, S, Y, theta, M)) { free(M); return -1; }
+    double* d = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    orc_bp* F = (orc_bp*)malloc(sizeof(orc_bp) * (size_t)(n > 0 ? n : 1));
+    double p[2 * 64], cc[2 * 64], Mv[2 * 64], wb[2 * 64];
+    int64_t nf = 0;
+    for (int64_t i = 0; i < n; ++i) {                                   /* breakpoints */
+        double ti = INFINITY;
+        if (g[i] < 0.0 && u) ti = (x[i] - u[i]) / g[i];
+        else if (g[i] > 0.0 && l) ti = (x[i] - l[i]) / g[i];
+        d[i] = (ti == 0.0) ? 0.0 : -g[i];
+        xcp[i] = x[i];
+        if (ti > 0.0) { F[nf].t = ti; F[nf].i = i; ++nf; }
+    }
+    qsort(F, (size_t)nf, sizeof(orc_bp), bp_cmp);
+    for (int j = 0; j < k; ++j) { p[j] = 0.0; cc[j] = 0.0; }
+    for (int64_t i = 0; i < n; ++i) {                                   /* p = W^T d */
+        if (d[i] == 0.0) continue;
+        for (int a = 0; a < h; ++a) p[a] += Y[(int64_t)a * n + i] * d[i];
+        for (int a = 0; a < h; ++a) p[h + a] += theta * S[(int64_t)a * n + i] * d[i];
+    }
+    double fp = 0.0;
+    for (int64_t i = 0; i < n; ++i) fp -= d[i] * d[i];                 /* f' = -d^T d */
+    if (fp == 0.0) {                                                    /* d = 0: x is the Cauchy point */
+        for (int j = 0; j < k; ++j) c[j] = 0.0;
+        free(M); free(d); free(F);
+        return 0;
+    }
+    mat_vec_small(k, M, p, Mv);
+    double pMp = 0.0;
+    for (int j = 0; j < k; ++j) pMp += p[j] * Mv[j];
+    double fpp = -theta * fp - pMp;
+    double dtmin = -fp / fpp;
+    double told = 0.0;
+    int64_t it = 0, passed = 0;
+    double t = nf > 0 ? F[0].t : INFINITY;
+    double dt = t - told;
+    while (it < nf && dtmin >= dt) {
+        const int64_t b = F[it].i;
+        ++it; ++passed;
+        const double gb = g[b];
+        xcp[b] = d[b] > 0.0 ? u[b] : l[b];
+        const double zb = xcp[b] - x[b];
+        for (int j = 0; j < k; ++j) cc[j] += dt * p[j];
+        for (int a = 0; a < h; ++a) { wb[a] = Y[(int64_t)a * n + b]; wb[h + a] = theta * S[(int64_t)a * n + b]; }
+        double wMc = 0.0, wMp = 0.0, wMw = 0.0;
+        mat_vec_small(k, M, cc, Mv);
+        for (int j = 0; j < k; ++j) wMc += wb[j] * Mv[j];
+        mat_vec_small(k, M, p, Mv);
+        for (int j = 0; j < k; ++j) wMp += wb[j] * Mv[j];
+        mat_vec_small(k, M, wb, Mv);
+        for (int j = 0; j < k; ++j) wMw += wb[j] * Mv[j];
+        fp = fp + dt * fpp + gb * gb + theta * gb * zb - gb * wMc;
+        fpp = fpp - theta * gb * gb - 2.0 * gb * wMp - gb * gb * wMw;
+        for (int j = 0; j < k; ++j) p[j] += gb * wb[j];
+        d[b] = 0.0;
+        dtmin = -fp / fpp;
+        told = t;
+        t = it < nf ? F[it].t : INFINITY;
+        dt = t - told;
+    }
+    if (dtmin < 0.0) dtmin = 0.0;
+    told = told + dtmin;
+    for (int64_t i = 0; i < n; ++i)
+        if (d[i] != 0.0) xcp[i] = x[i] + told * d[i];
+    for (int j = 0; j < k; ++j) cc[j] += dtmin * p[j];
+    for (int j = 0; j < k; ++j) c[j] = cc[j];
+    free(M); free(d); free(F);
+    return passed;
+}
