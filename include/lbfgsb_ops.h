@@ -61,6 +61,21 @@ lbfgsb_err lbfgsb_op_trials(lbfgsb_t* h, const lbfgsb_objective* obj, const doub
                             const double* q, const double* x, const double* p, double alpha0,
                             int32_t ntrials, double* f_out);
 
+/* the generalized Cauchy point of the ORIGINAL L-BFGS-B
+ * (Byrd, Lu, Nocedal, Zhu 1995, Algorithm CP), the sequential step the paper
+ * removes, on the GPU as the baseline: the
+ * breakpoints, reductions and final update in parallel kernels, the
+ * breakpoint loop (a (t_i, i)-keyed binary heap, O(h^2) per breakpoint) on
+ * ONE thread.  x, g: n DEVICE (n = the handle's); the box is the handle's;
+ * nh <= 8 pairs S, Y (DEVICE, nh*n each, pair i at S + i*n, OLDEST first;
+ * the compact form B = theta I - W M W^T, W = [Y, theta S]).  Outputs:
+ * xcp (n, DEVICE); (host, may be NULL) c (2*nh) = W^T (xcp - x), *passed =
+ * breakpoints passed by the loop, *scan_ms = device time of the
+ * single-thread loop (CUDA events).  Errors: ARG, UNSUPPORTED, CUDA. */
+lbfgsb_err lbfgsb_op_cauchy_point(lbfgsb_t* h, const double* x, const double* g, int32_t nh,
+                                  const double* S, const double* Y, double theta, double* xcp,
+                                  double* c, int64_t* passed, double* scan_ms);
+
 /* Loopback verification of the column-sharded path on ONE device: the nranks
  * handles hs[p] (created with lbfgsb_create, n = that shard's variables, all
  * on the same device) act as logical ranks p = 0..nranks-1 of a sharded

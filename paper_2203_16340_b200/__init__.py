@@ -107,8 +107,10 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
     L.lbfgsb_op_gaussian_kernel.argtypes = [vp, _c_i64, _c_i64, _c_d, vp, _c_i64, vp]
     L.lbfgsb_objective_transport.argtypes = [vp, _c_i64, _c_i64, _c_i32, _c_d, C.POINTER(vp)]
+    L.lbfgsb_op_cauchy_point.argtypes = [vp, vp, vp, _c_i32, vp, vp, _c_d, vp, C.POINTER(_c_d),
+                                         C.POINTER(_c_i64), C.POINTER(_c_d)]
     L.al_solve_transport.argtypes = [vp, vp, vp, vp, C.POINTER(_AlOpts), vp, vp, C.POINTER(_AlRes)]
-    for name in ("lbfgsb_objective_transport", "al_solve_transport",
+    for name in ("lbfgsb_objective_transport", "al_solve_transport", "lbfgsb_op_cauchy_point",
                  "lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
                  "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
@@ -416,6 +418,21 @@ class Solver:
                         r.status, [], [])
 
     # ---- op-level entry points (lbfgsb_ops.h) ----
+    def op_cauchy_point(self, x, g, S=None, Y=None, theta=1.0):
+        """Generalized Cauchy point of the original L-BFGS-B (baseline):
+        returns dict(xcp, c, passed, scan_ms)."""
+        import torch
+        nh = 0 if S is None else S.shape[0]
+        xcp = torch.empty_like(x)
+        c = (_c_d * max(2 * nh, 1))()
+        passed = _c_i64()
+        ms = _c_d()
+        Sc = None if S is None else S.contiguous()
+        Yc = None if Y is None else Y.contiguous()
+        _check(_lib.lbfgsb_op_cauchy_point(self._h, _ptr(x), _ptr(g), nh, _ptr(Sc), _ptr(Yc), float(theta),
+                                           _ptr(xcp), c, C.byref(passed), C.byref(ms)))
+        return dict(xcp=xcp, c=list(c)[:2 * nh], passed=passed.value, scan_ms=ms.value)
+
     def op_direction(self, x, g, S=None, Y=None):
         """Working set + vector-free Alg. 3 + Alg. 2 on (x, g, pairs oldest first)."""
         import torch

@@ -185,6 +185,12 @@ void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);
 void launch_cb_trial(const Prob& P, cudaStream_t st, double alpha, double* xt);
 void launch_cb_commit(const Prob& P, cudaStream_t st, const double* xt, const double* gt, int slot);
+// cauchy.cu: generalized Cauchy point of the original L-BFGS-B
+int launch_cauchy(int64_t n, const double* x, const double* g, const double* l, const double* u, int h,
+                  const double* S, const double* Y, double theta, double* d, double* tk, double* xcp,
+                  double* part, double* red, unsigned* ticket, double* heap_g, double* scal,
+                  cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1);
+int cauchy_nr();
 // transport.cu
 void launch_tsum(const Prob& P, cudaStream_t st, int mode);
 void launch_tviol(const Prob& P, cudaStream_t st, double rho, int update, double* out_dev);

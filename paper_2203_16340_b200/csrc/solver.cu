@@ -120,6 +120,8 @@ struct lbfgsb_t {
     DevBuf Mh, bh, xh;
     // transport objective
     DevBuf tlam, te, tap, trow, tcol, tsp, tspr, tspc, tticket, tvout;
+    // Cauchy-point op
+    DevBuf cp_d, cp_t, cp_xcp, cp_part, cp_red, cp_heap, cp_scal, cp_ticket;
     Ctrl* ctrl = nullptr;           // device
     Ctrl* hc = nullptr;             // pinned host mirror
     // graph cache
@@ -288,7 +290,9 @@ extern "C" void lbfgsb_destroy(lbfgsb_t* h)
                       &h->tickets, &h->sep_part, &h->r0, &h->r1, &h->q, &h->qpart, &h->lsp,
                       &h->fout, &h->Mh, &h->bh, &h->xh, &h->pk_loc, &h->qs_all, &h->dir_all,
                       &h->gram_all, &h->kkt_all, &h->tlam, &h->te, &h->tap, &h->trow,
-                      &h->tcol, &h->tsp, &h->tspr, &h->tspc, &h->tticket, &h->tvout};
+                      &h->tcol, &h->tsp, &h->tspr, &h->tspc, &h->tticket, &h->tvout, &h->cp_d,
+                      &h->cp_t, &h->cp_xcp, &h->cp_part, &h->cp_red, &h->cp_heap, &h->cp_scal,
+                      &h->cp_ticket};
     for (DevBuf* b : bufs) b->release();
     if (h->ctrl) cudaFree(h->ctrl);
     if (h->hc) cudaFreeHost(h->hc);
@@ -1182,6 +1186,42 @@ extern "C" lbfgsb_err al_solve_transport(lbfgsb_t* h, const lbfgsb_objective* ob
     if (lambda) CK(cudaMemcpyAsync(lambda, P.tlam, sizeof(double) * K, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     if (res) *res = R;
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ N3: Cauchy point op
+extern "C" lbfgsb_err lbfgsb_op_cauchy_point(lbfgsb_t* h, const double* x, const double* g, int32_t nh,
+                                             const double* S, const double* Y, double theta, double* xcp,
+                                             double* c, int64_t* passed, double* scan_ms)
+{
+    if (!h || !x || !g || !xcp) return fail(LBFGSB_ERR_ARG, "NULL handle, x, g or xcp");
+    if (nh < 0 || nh > 8 || (nh > 0 && (!S || !Y))) return fail(LBFGSB_ERR_ARG, "0 <= nh <= 8 pairs required");
+    if (h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "single-GPU op");
+    const int64_t n = h->n;
+    const size_t nb = sizeof(double) * (size_t)n;
+    TRY(h->cp_d.ensure(nb)); TRY(h->cp_t.ensure(nb)); TRY(h->cp_heap.ensure(2 * nb));
+    TRY(h->cp_part.ensure(sizeof(double) * (size_t)(2 * sm_count()) * cauchy_nr()));
+    TRY(h->cp_red.ensure(sizeof(double) * (size_t)cauchy_nr()));
+    TRY(h->cp_scal.ensure(sizeof(double) * 32));
+    TRY(h->cp_ticket.ensure(sizeof(unsigned) * 4, true));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (scan_ms) { CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1)); }
+    if (launch_cauchy(n, x, g, h->l.d(), h->u.d(), nh, S, Y, theta, h->cp_d.d(), h->cp_t.d(), xcp,
+                      h->cp_part.d(), h->cp_red.d(), static_cast<unsigned*>(h->cp_ticket.p), h->cp_heap.d(),
+                      h->cp_scal.d(), h->st, e0, e1))
+        return fail(LBFGSB_ERR_ARG, "bad history length");
+    CK(cudaGetLastError());
+    double sc[32];
+    CK(cudaMemcpyAsync(sc, h->cp_scal.d(), sizeof sc, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (passed) *passed = (int64_t)sc[1];
+    if (c) for (int j = 0; j < 2 * nh; ++j) c[j] = sc[2 + j];
+    if (scan_ms) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        *scan_ms = ms;
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+    }
     return LBFGSB_OK;
 }
 
