@@ -5,7 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2203_16340_b200 as lb
 import synth
-for N, d in [(10000, 22), (30000, 22)]:
+sizes = [int(a) for a in sys.argv[1:]] or [10000, 30000]
+for N, d in [(N, 22) for N in sizes]:
     X, y = synth.blobs(N, d, seed=10, sep=2.0, scale=1.0 / np.sqrt(d))
     Xd = torch.from_numpy(X).cuda(); yd = torch.from_numpy(y).cuda()
     torch.cuda.synchronize(); t0 = time.perf_counter()
