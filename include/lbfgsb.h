@@ -214,6 +214,23 @@ lbfgsb_err lbfgsb_solve_lsq_host(lbfgsb_t* h, const double* M_host, int64_t m, i
                                  const double* b_host, double* x_host, double tol,
                                  lbfgsb_result* res);
 
+/* SURVEY 8(f) N4 "replicas": `batch` independent LSQ problems of one shape,
+ *   min 1/2 ||A_k x - b_k||^2  s.t.  l_k <= x <= u_k,   k = 0..batch-1,
+ * each solved by Alg. 1 in ONE CTA (A_k resident in shared
+ * memory when m*n*8 plus the vectors fit in 200 KB, e.g. the C1 size 200 x
+ * 100; larger problems up to the shared-memory limit read A_k from global
+ * memory).  All DEVICE pointers: M batch x (m x n column-major, problem k at
+ * M + k*m*n); b batch x m; lower / upper batch x n each (NULL = -inf / +inf);
+ * x batch x n, in x^0 (clipped) / out x*.  res (host) receives `batch`
+ * results (seconds = the whole call).  opts as lbfgsb_create (NULL =
+ * defaults; check_every / use_graph / profile / armijo_diff unused); tol
+ * overrides opts.tol when > 0.  Synchronous on cuda_stream (NULL = legacy).
+ * Errors: ARG, DIM (batch < 0, shape too large for one CTA), CUDA. */
+lbfgsb_err lbfgsb_solve_batched_lsq(int32_t batch, int64_t m, int64_t n, const double* M, const double* b,
+                                    const double* lower, const double* upper, double* x, int32_t m_hist,
+                                    const lbfgsb_opts* opts, double tol, void* cuda_stream,
+                                    lbfgsb_result* res);
+
 /* ---- Alg. 4 -------------------------------------------------------------- */
 
 typedef struct {

@@ -20,7 +20,7 @@ from . import _build
 __all__ = ["Options", "ALOptions", "Result", "ALResult", "Solver", "LSQObjective",
            "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor",
            "solve_loopback", "nccl_unique_id", "QPObjective", "op_gaussian_kernel",
-           "TransportObjective"]
+           "TransportObjective", "solve_batched_lsq", "colmajor_batch"]
 
 _c_d, _c_i32, _c_i64, _c_vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
 
@@ -107,10 +107,13 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
     L.lbfgsb_op_gaussian_kernel.argtypes = [vp, _c_i64, _c_i64, _c_d, vp, _c_i64, vp]
     L.lbfgsb_objective_transport.argtypes = [vp, _c_i64, _c_i64, _c_i32, _c_d, C.POINTER(vp)]
+    L.lbfgsb_solve_batched_lsq.argtypes = [_c_i32, _c_i64, _c_i64, vp, vp, vp, vp, vp, _c_i32,
+                                           C.POINTER(_Opts), _c_d, vp, C.POINTER(_Res)]
     L.lbfgsb_op_cauchy_point.argtypes = [vp, vp, vp, _c_i32, vp, vp, _c_d, vp, C.POINTER(_c_d),
                                          C.POINTER(_c_i64), C.POINTER(_c_d)]
     L.al_solve_transport.argtypes = [vp, vp, vp, vp, C.POINTER(_AlOpts), vp, vp, C.POINTER(_AlRes)]
     for name in ("lbfgsb_objective_transport", "al_solve_transport", "lbfgsb_op_cauchy_point",
+                 "lbfgsb_solve_batched_lsq",
                  "lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
                  "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
@@ -201,6 +204,11 @@ class Result:
     @property
     def status_name(self):
         return STATUS_NAMES.get(self.status, str(self.status))
+
+    @classmethod
+    def from_c(cls, r):
+        return cls(r.f, r.pg_inf, r.gfree_inf, r.seconds, r.iters, r.n_fg, r.n_backtracks, r.n_free,
+                   r.n_fallbacks, r.status, r.last_branch)
 
 
 @dataclass
@@ -494,6 +502,34 @@ def op_gaussian_kernel(X, gamma, stream=None):
     _check(load().lbfgsb_op_gaussian_kernel(_ptr(Xc), N, d, float(gamma), _ptr(Kt), N,
                                             _stream_ptr(stream)))
     return Kt.T
+
+
+def solve_batched_lsq(M, b, x, lower=None, upper=None, m_hist=5, opts: Options | None = None, tol=0.0):
+    """N4 replicas (lbfgsb_solve_batched_lsq): M (batch, n, m) CUDA fp64 whose
+    [k] is A_k stored column-major (i.e. A_k^T contiguous, see ``colmajor_batch``),
+    b (batch, m), x (batch, n) in/out, lower/upper (batch, n) or None.  One CTA
+    per problem.  Returns a list of Result."""
+    import torch
+    L = load()
+    B, n, m = M.shape
+    o = (opts or Options())._c()
+    res = (_Res * max(B, 1))()
+    for t in (M, b, x):
+        if not t.is_contiguous():
+            raise LbfgsbError("M, b, x must be contiguous")
+    lo = None if lower is None else lower.contiguous()
+    up = None if upper is None else upper.contiguous()
+    stream = torch.cuda.current_stream().cuda_stream
+    _check(L.lbfgsb_solve_batched_lsq(B, m, n, _ptr(M), _ptr(b), _ptr(lo), _ptr(up), _ptr(x), m_hist,
+                                      C.byref(o), float(tol), C.c_void_p(stream), res))
+    return [Result.from_c(res[i]) for i in range(B)]
+
+
+def colmajor_batch(A):
+    """(batch, m, n) host/CUDA array -> CUDA fp64 (batch, n, m) contiguous (each A_k column-major)."""
+    import torch
+    t = torch.as_tensor(A, dtype=torch.float64)
+    return t.transpose(1, 2).contiguous().cuda()
 
 
 def op_gemv(obj: LSQObjective, p, q, stream=None):

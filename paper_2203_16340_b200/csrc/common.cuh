@@ -288,6 +288,29 @@ __device__ __forceinline__ void recur_decide(const Prob& P, Ctrl* C, const doubl
     for (int b = 0; b < nb; ++b) C->coef[b] = -w[b];
 }
 
+// Alg. 2 line 3 decision (R9) and the line-search bound alpha_0 (R10).
+__device__ __forceinline__ void dir_decide(const Prob& P, Ctrl* C, const double* res, int op_mode)
+{
+    const double eps = P.eps;
+    const double Spg = res[0], Spp = res[1], Stg = res[2], amin_all = res[3];
+    const int projected = (!P.no_projection && Spg <= -eps * Spp && Spp >= eps) ? 1 : 0;  // Alg. 2 line 3
+    double amax = projected ? 1.0 : amin_all;
+    if (amax < 0.0) amax = 0.0;
+    const double gp = projected ? Spg : Stg;
+    C->branch = projected;
+    C->gp = gp;
+    C->amax = amax;
+    C->alpha0 = amax < 1.0 ? amax : 1.0;                        // R10
+    C->ls_batch = 0;
+    C->ls_tried = 0;
+    C->cont = 0;
+    if (op_mode) return;
+    if (!(gp < 0.0)) {                                          // guard (R14)
+        if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }
+        else C->stall = ST_FALLBACK;
+    }
+}
+
 // Trial objective from reduced sums (oracle order: 1/2 S + phi,
 // phi = c^T x + delta/2 ||x||^2, then the AL terms of Eq. (3)).
 __device__ __forceinline__ double trial_value(const Prob& P, const Ctrl* C, double quad, const double* sep,

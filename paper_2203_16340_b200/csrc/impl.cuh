@@ -185,6 +185,10 @@ void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);
 void launch_cb_trial(const Prob& P, cudaStream_t st, double alpha, double* xt);
 void launch_cb_commit(const Prob& P, cudaStream_t st, const double* xt, const double* gt, int slot);
+// batch.cu: one CTA per small LSQ problem
+int launch_batch(int32_t batch, int64_t m, int64_t n, const double* M, const double* b, const double* lo,
+                 const double* up, double* x, int mh, const lbfgsb_opts& o, double tol, lbfgsb_result* res,
+                 cudaStream_t st);
 // cauchy.cu: generalized Cauchy point of the original L-BFGS-B
 int launch_cauchy(int64_t n, const double* x, const double* g, const double* l, const double* u, int h,
                   const double* S, const double* Y, double theta, double* d, double* tk, double* xcp,

@@ -1225,6 +1225,38 @@ extern "C" lbfgsb_err lbfgsb_op_cauchy_point(lbfgsb_t* h, const double* x, const
     return LBFGSB_OK;
 }
 
+// ------------------------------------------------------------------ N4: batched small problems
+extern "C" lbfgsb_err lbfgsb_solve_batched_lsq(int32_t batch, int64_t m, int64_t n, const double* M,
+                                               const double* b, const double* lower, const double* upper,
+                                               double* x, int32_t m_hist, const lbfgsb_opts* opts,
+                                               double tol, void* cuda_stream, lbfgsb_result* res)
+{
+    if (batch < 0 || m <= 0 || n <= 0) return fail(LBFGSB_ERR_DIM, "bad batch shape");
+    if (batch == 0) return LBFGSB_OK;
+    if (!M || !b || !x || !res) return fail(LBFGSB_ERR_ARG, "NULL M, b, x or res");
+    if (m_hist < 1 || m_hist > LBFGSB_MAX_HIST) return fail(LBFGSB_ERR_ARG, "bad m_hist");
+    lbfgsb_opts o;
+    lbfgsb_opts_default(&o);
+    if (opts) o = *opts;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(LBFGSB_ERR_CUDA, "no CUDA device available (the library has no CPU path)");
+    init_kernels();
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    lbfgsb_result* dres = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dres), sizeof(lbfgsb_result) * (size_t)batch, st));
+    auto t0 = std::chrono::steady_clock::now();
+    const int rc = launch_batch(batch, m, n, M, b, lower, upper, x, m_hist, o, tol > 0 ? tol : o.tol, dres, st);
+    if (rc) { cudaFreeAsync(dres, st); return fail(LBFGSB_ERR_DIM, "problem too large for one CTA's shared memory"); }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(res, dres, sizeof(lbfgsb_result) * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(dres, st));
+    CK(cudaStreamSynchronize(st));
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int32_t i = 0; i < batch; ++i) res[i].seconds = secs;
+    return LBFGSB_OK;
+}
+
 // ------------------------------------------------------------------ sharded (NCCL)
 extern "C" lbfgsb_err lbfgsb_nccl_unique_id(void* out)
 {

@@ -11,7 +11,8 @@ ap.add_argument("--cases", default="ds2:entropy:1000")
 ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--max-outer", type=int, default=100)
 ap.add_argument("--max-iters", type=int, default=100000)
-ap.add_argument("--eps", type=float, default=1e-9)
+ap.add_argument("--eps", type=float, default=None,
+                help="epsilon of Eq. (1) (default: 1e-20 for the entropy, 1e-9 for the Gaussian; reading R30)")
 a = ap.parse_args()
 for case in a.cases.split(","):
     ds, reg, n = case.split(":"); n = int(n)
@@ -20,7 +21,8 @@ for case in a.cases.split(","):
     Md = torch.from_numpy(t.cost.reshape(-1, order="F")).cuda().reshape(n, m).T
     obj = lb.TransportObjective(Md, reg, t.lam)
     lo = torch.full((m * n,), 1e-300 if reg == "entropy" else 0.0, dtype=torch.float64, device="cuda")
-    s = lb.Solver(m * n, 5, lower=lo, opts=lb.Options(tol=a.tol, max_iters=a.max_iters, eps=a.eps))
+    s = lb.Solver(m * n, 5, lower=lo, opts=lb.Options(tol=a.tol, max_iters=a.max_iters,
+                                                      eps=a.eps if a.eps is not None else (1e-20 if reg == "entropy" else 1e-9)))
     x = torch.zeros(m * n, dtype=torch.float64, device="cuda")
     u = torch.from_numpy(t.u).cuda(); v = torch.from_numpy(t.v).cuda()
     torch.cuda.synchronize(); t0 = time.perf_counter()
