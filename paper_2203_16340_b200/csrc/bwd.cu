@@ -1308,6 +1308,228 @@ __global__ void __launch_bounds__(NT, 1) k_qepi_t(Prob P, int mode)
     gram_tail_after(P, C, E, gmax, cnt, red, buf, 4096, stash, Gs);
 }
 
+// ---------------------------------------------------------------- k_qepi_d (TMA + DMMA Gram)
+// The QP / transport epilogue with the masked Gram on the FP64 tensor cores.
+// Tiles of QD = 256 variables (one per thread) are staged by cp.async.bulk
+// into a 2-stage ring exactly as in k_qepi_t (slot stride QDP = QD + 4
+// doubles: the 8 basis rows a warp reads per k-step fall on distinct bank
+// groups); the epilogue writes the tile's new s, y, g and the Eq. (1) mask to
+// shared memory; then each warp accumulates the Gram of its 32 variables with
+// mma.sync.m8n8k4 f64 (DMMA): the basis {S_0..S_{NH-1}, Y_0..Y_{NH-1}, g} is
+// padded to 16 rows (two 8-blocks), A = (mask * B)^T, B = B, and the three
+// upper blocks (0,0), (0,1), (1,1) take 3 DMMA per 4 variables.  Accumulators
+// are 6 doubles per lane, so two CTAs fit per SM.  The partial last tile is
+// copied to the same shared layout by the threads (zero-filled beyond n).
+constexpr int QD = 256;
+constexpr int QDP = QD + 4;
+constexpr int QDV = 8 + 2 * QMH;             // staged slots (same map as k_qepi_t)
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(NT, 2) k_qepi_d(Prob P, int mode)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    extern __shared__ __align__(128) double stg[];           // [2][QDV][QDP] | new[3][QD] | mk[QD]
+    __shared__ double red[NT / 32];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    __shared__ double gw[NT / 32][3][64];                    // per-warp Gram blocks
+    __shared__ const double* vsrc[QDV];
+    __shared__ __align__(8) uint64_t full_bar[2];
+    double* nw = stg + 2 * (size_t)QDV * QDP;                // new s | new y | g
+    double* mkv = nw + 3 * QD;
+    const bool iter = mode == BWD_ITER;
+    const double* wcur = P.rbuf[C->rsel];
+    double* wnext = P.rbuf[C->rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    const double rho = C->rho;
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    const int nh = E.nh;
+    const int64_t n = P.n;
+    const bool gram = E.gram;
+    if (threadIdx.x == 0) {
+        vsrc[0] = P.x; vsrc[1] = P.l; vsrc[2] = P.u;
+        vsrc[3] = iter ? P.g : nullptr;
+        vsrc[4] = iter ? (E.branch ? P.pp : P.pt) : nullptr;
+        vsrc[5] = P.c;
+        vsrc[6] = P.qp ? wcur : nullptr;
+        vsrc[7] = (P.qp && iter) ? P.q : nullptr;
+        for (int b = 0; b < 2 * QMH; ++b) {
+            const bool cur = iter && (b == nh - 1 || b == 2 * nh - 1);
+            vsrc[8 + b] = (gram && b < 2 * nh && !cur) ? E.bptr[b] : nullptr;
+        }
+        mbar_init(&full_bar[0], 1);
+        mbar_init(&full_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (P.tp && iter) {                                         // carried h' = h + alpha A p (N2)
+        const int64_t K = P.tm + P.tn;
+        for (int64_t k = (int64_t)blockIdx.x * NT + threadIdx.x; k < K; k += (int64_t)gridDim.x * NT)
+            wnext[k] = fma(alpha, P.tap[k], wcur[k]);
+    }
+    const int64_t nfull = n / QD, ntiles = (n + QD - 1) / QD;
+    unsigned bytes_tile = 0;
+    for (int k = 0; k < QDV; ++k) if (vsrc[k]) bytes_tile += QD * 8;
+    auto issue = [&](int64_t t, int sidx) {                  // thread 0 only
+        double* base = stg + (size_t)sidx * QDV * QDP;
+        mbar_arrive_tx(&full_bar[sidx], bytes_tile);
+        for (int k = 0; k < QDV; ++k)
+            if (vsrc[k]) bulk_g2s(base + (size_t)k * QDP, vsrc[k] + t * QD, QD * 8, &full_bar[sidx]);
+    };
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // this lane's two basis rows (block 0: j0 = lane/4, block 1: j1 = 8 + lane/4)
+    const int j0 = lane >> 2, j1 = 8 + (lane >> 2);
+    auto src_of = [&](int j, const double* base) -> const double* {   // nullptr = padding row
+        if (j >= 2 * nh + 1) return nullptr;
+        if (j == 2 * nh) return nw + 2 * QD;                              // g
+        if (iter && j == nh - 1) return nw;                               // newest s
+        if (iter && j == 2 * nh - 1) return nw + QD;                      // newest y
+        return base + (size_t)(8 + j) * QDP;
+    };
+    double a00 = 0.0, a01 = 0.0, b00 = 0.0, b01 = 0.0, c00 = 0.0, c01 = 0.0;  // blocks (0,0) (0,1) (1,1)
+    double fullacc[QMH];
+#pragma unroll
+    for (int k = 0; k < QMH; ++k) fullacc[k] = 0.0;
+    double gmax = 0.0, cnt = 0.0;
+    const bool small = n < (1LL << 31);
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < nfull) issue(blockIdx.x, 0);
+    int li = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
+        const int sidx = li & 1;
+        double* base = stg + (size_t)sidx * QDV * QDP;
+        const int e = threadIdx.x;
+        const int64_t v = t * QD + e;
+        if (t < nfull) {
+            const int64_t tn = t + gridDim.x;
+            if (threadIdx.x == 0 && tn < nfull) issue(tn, sidx ^ 1);
+            mbar_wait(&full_bar[sidx], (unsigned)((li >> 1) & 1));
+        } else {                                                // partial tile: threads fill the stage
+            for (int k = 0; k < QDV; ++k)
+                if (vsrc[k]) base[(size_t)k * QDP + e] = v < n ? vsrc[k][v] : 0.0;
+            __syncthreads();
+        }
+        // ---- epilogue (one variable per thread)
+        double sv = 0.0, yv = 0.0, gn = 0.0;
+        bool fixed = true;
+        if (v < n) {
+            auto ld = [&](int k) -> double { return base[(size_t)k * QDP + e]; };
+            const double xo = ld(0), lv = ld(1), uv = ld(2);
+            const double go = iter ? ld(3) : 0.0;
+            const double pv = iter ? ld(4) : 0.0;
+            const double cv = P.c ? ld(5) : 0.0;
+            double w;
+            if (P.tp) {
+                int64_t i, j;
+                if (small) {
+                    const unsigned vv = (unsigned)v, tmu = (unsigned)P.tm;
+                    j = vv / tmu; i = vv - (unsigned)j * tmu;
+                } else {
+                    j = v / P.tm; i = v - j * P.tm;
+                }
+                const int64_t kj = P.tm + j;
+                double hi = wcur[i], hj = wcur[kj];
+                if (iter) { hi = fma(alpha, P.tap[i], hi); hj = fma(alpha, P.tap[kj], hj); }
+                w = (rho * hi + P.tlam[i]) + (rho * hj + P.tlam[kj]);
+            } else {
+                w = ld(6);
+                if (iter) {
+                    w = fma(alpha, ld(7), w);                   // carried w' = Q~ x'
+                    wnext[v] = w;
+                }
+            }
+            const double xn = iter ? clipd(fma(alpha, pv, xo), lv, uv) : xo;   // Alg. 1 line 7
+            gn = w;
+            if (P.c) gn = gn + cv;
+            gn = gn + P.delta * xn;
+            if (P.ent != 0.0) gn = gn + P.ent * (log(xn) + 1.0);
+            for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * P.Ecol[k][v];
+            if (iter) {
+                const int64_t so = (int64_t)E.slot * n + v;
+                sv = xn - xo;                                   // s^k
+                yv = gn - go;                                   // y^k
+                P.S[so] = sv;
+                P.Y[so] = yv;
+            }
+            P.x[v] = xn;
+            P.g[v] = gn;
+            fixed = (xn <= lv + P.eps && gn >= 0.0) || (xn >= uv - P.eps && gn <= 0.0);
+            P.mask[v] = fixed ? 0 : 1;                          // S^{k+1}, Eq. (1)
+            if (!fixed) {
+                const double ag = fabs(gn);
+                gmax = ag > gmax ? ag : gmax;
+                cnt += 1.0;
+            }
+            if (gram && P.screen_full) {                        // unmasked ||y_k||^2 (R3 option)
+#pragma unroll
+                for (int k = 0; k < QMH; ++k) {
+                    if (k >= nh) break;
+                    const double yk = (iter && k == nh - 1) ? yv : ld(8 + nh + k);
+                    fullacc[k] = fma(yk, yk, fullacc[k]);
+                }
+            }
+        }
+        if (gram) {
+            nw[e] = sv; nw[QD + e] = yv; nw[2 * QD + e] = gn;
+            mkv[e] = fixed ? 0.0 : 1.0;
+            __syncthreads();
+            // ---- warp Gram of variables [32 wid, 32 wid + 32) on DMMA
+            const double* r0 = src_of(j0, base);
+            const double* r1 = src_of(j1, base);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int vv = wid * 32 + ks * 4 + (lane & 3);
+                const double m = mkv[vv];
+                const double x0 = r0 ? r0[vv] : 0.0, x1 = r1 ? r1[vv] : 0.0;
+                const double m0 = m * x0, m1 = m * x1;
+                dmma884(a00, a01, m0, x0);                      // block (0,0)
+                dmma884(b00, b01, m0, x1);                      // block (0,1)
+                dmma884(c00, c01, m1, x1);                      // block (1,1)
+            }
+        }
+        // every thread is done with this stage before it is refilled (two tiles on)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+    }
+    if (!gram) return;
+    // ---- CTA reduction: warps' blocks in order, then the enumeration of gram_tail
+    {
+        const int ra = lane >> 2, cb = 2 * (lane & 3);
+        gw[wid][0][ra * 8 + cb] = a00; gw[wid][0][ra * 8 + cb + 1] = a01;
+        gw[wid][1][ra * 8 + cb] = b00; gw[wid][1][ra * 8 + cb + 1] = b01;
+        gw[wid][2][ra * 8 + cb] = c00; gw[wid][2][ra * 8 + cb + 1] = c01;
+    }
+    double fr[QMH];
+#pragma unroll
+    for (int k = 0; k < QMH; ++k) fr[k] = P.screen_full ? block_reduce<0>(fullacc[k], red) : 0.0;
+    __syncthreads();
+    const int nb = E.nb, ne = nb * (nb + 1) / 2;
+    const int ntot = ne + (P.screen_full ? nh : 0);
+    double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
+    for (int q = threadIdx.x; q < ntot; q += NT) {
+        double sum = 0.0;
+        if (q < ne) {
+            int aa = 0, rem = q;
+            while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
+            const int bb = aa + rem;                                  // aa <= bb
+            const int blk = aa < 8 ? (bb < 8 ? 0 : 1) : 2;
+            const int r = aa & 7, c = bb & 7;
+            for (int w = 0; w < NT / 32; ++w) sum += gw[w][blk][r * 8 + c];
+        } else {
+            sum = fr[q - ne];
+        }
+        out[q] = sum;
+    }
+    __syncthreads();
+    gram_tail_after(P, C, E, gmax, cnt, red, &gw[0][0][0], NT / 32 * 3 * 64, stash, Gs);
+}
+
 // ---------------------------------------------------------------- launch
 static int g_bwd_occ = 0, g_bwdw_occ = 0;
 // k_bwd_c (TMA, CTA pairs) is opt-in: on C2 it measured 275-335 us vs 268 us for k_bwd_s
@@ -1317,6 +1539,7 @@ static bool g_no_tma = getenv("LBFGSB_TMA") == nullptr;
 // selects the shared-memory tile kernel k_qpu instead (A/B experiments)
 static bool g_no_qepi = getenv("LBFGSB_NO_QEPI") != nullptr;
 static bool g_no_qepi_t = getenv("LBFGSB_NO_QEPI_T") != nullptr;   // register-Gram kernel without TMA staging
+static bool g_qepi_reg = getenv("LBFGSB_QEPI_REG") != nullptr;      // k_qepi_t (register Gram) instead of k_qepi_d (DMMA)
 constexpr int BWD_W_MAXM = 2048;
 constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + 64);
 static bool g_bwd_init = false;
@@ -1373,6 +1596,18 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         const void* ptrs[] = {P.x, P.l, P.u, P.g, P.pp, P.pt, P.c, P.rbuf[0], P.rbuf[1], P.q, P.S, P.Y};
         for (const void* p : ptrs) al16 = al16 && ((reinterpret_cast<uintptr_t>(p) & 15u) == 0);
         al16 = al16 && (P.n % 2 == 0);                          // S / Y slot starts stay aligned
+        if (al16 && !g_no_qepi_t && !g_qepi_reg && P.n >= QD && 2 * P.mh + 1 <= 16) {
+            const size_t smem = sizeof(double) * (2 * (size_t)QDV * QDP + 4 * (size_t)QD);
+            static bool smem_set_d = false;
+            if (!smem_set_d) {
+                cudaFuncSetAttribute(k_qepi_d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                smem_set_d = true;
+            }
+            int64_t g = (P.n + QD - 1) / QD;
+            if (g > 2LL * sm_count()) g = 2LL * sm_count();
+            k_qepi_d<<<(int)g, NT, smem, st>>>(P, mode);
+            return;
+        }
         if (al16 && !g_no_qepi_t && P.n >= QT) {
             const size_t smem = sizeof(double) * 2 * (size_t)QV * QT;
             static bool smem_set = false;
