@@ -204,8 +204,8 @@ static lbfgsb_err alloc_n(lbfgsb_t* h)
     const int64_t parts = 64LL * sms;     // >= max(GB, G1) for any occupancy
     TRY(h->gram_part.ensure(sizeof(double) * parts * GRAM_STRIDE));
     TRY(h->gram_grp.ensure(sizeof(double) * cdiv(parts, GRP) * GRAM_STRIDE));
-    TRY(h->dir_part.ensure(sizeof(double) * 2LL * sms * 4));
-    TRY(h->kkt_part.ensure(sizeof(double) * 2LL * sms * 3));
+    TRY(h->dir_part.ensure(sizeof(double) * 4LL * sms * 4));
+    TRY(h->kkt_part.ensure(sizeof(double) * 4LL * sms * 3));
     TRY(h->sep_part.ensure(sizeof(double) * (SEP_MAXG + 1) * KT * NSEP));
     TRY(h->tickets.ensure(sizeof(unsigned) * (NTICKETS + 8192), true));
     TRY(h->fout.ensure(sizeof(double) * KT));
@@ -402,7 +402,7 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
     P.dir_part = h->dir_part.d(); P.kkt_part = h->kkt_part.d(); P.sep_part = h->sep_part.d();
     P.tickets = static_cast<unsigned*>(h->tickets.p);
     P.ctrl = h->ctrl;
-    P.G1 = (int)clampi(cdiv(h->n, NT), 1, 2LL * sms);
+    P.G1 = (int)clampi(cdiv(h->n, NT), 1, 4LL * sms);        // 4 CTAs / SM: latency hiding at large n
     P.nranks = h->nranks;
     P.sharded = h->sharded ? 1 : 0;
     if (ob && ob->kind == 0) {
