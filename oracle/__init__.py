@@ -113,6 +113,8 @@ def _setup(L):
     L.orc_compact_m.restype = i32
     L.orc_cauchy_point.argtypes = [i64, _dp, _dp, _dp, _dp, i32, _dp, _dp, d, _dp, _dp]
     L.orc_cauchy_point.restype = i64
+    L.orc_lbfgsb_original.argtypes = [C.POINTER(_Lsq), _dp, _dp, i32, C.POINTER(_Opts), _dp,
+                                      C.POINTER(_Res), C.POINTER(d)]
     L.orc_armijo_scalar_quadratic.argtypes = [d, d, d, d, d, i32]
     L.orc_armijo_scalar_quadratic.restype = d
 
@@ -409,6 +411,26 @@ def minimize_lsq(P: LSQ, l=None, u=None, x0=None, m_hist=5, opts: Options | None
                           C.byref(res))
     return Result(x, res.f, res.pg_inf, res.gfree_inf, res.iters, res.n_fg, res.n_backtracks,
                   res.n_free, res.status, res.last_branch, res.n_fallbacks)
+
+
+def minimize_lsq_original(P: LSQ, l=None, u=None, x0=None, m_hist=5, opts: Options | None = None):
+    """The ORIGINAL L-BFGS-B (Byrd et al. 1995: Cauchy point + direct primal
+    subspace minimisation + backtracking; SURVEY N3 baseline).
+    Returns (Result, seconds spent in the Cauchy point)."""
+    o = opts or Options()
+    assert o.m_hist_ok(m_hist) if hasattr(o, "m_hist_ok") else m_hist <= 16
+    x = np.zeros(P.nvars) if x0 is None else _f64(x0).copy()
+    l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
+    u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
+    so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
+               int(o.no_projection), int(o.armijo_diff), o.max_iters)
+    res = _Res()
+    tcp = C.c_double(0.0)
+    s = P._struct()
+    _L().orc_lbfgsb_original(C.byref(s), _ptr(l), _ptr(u), m_hist, C.byref(so), _ptr(x), C.byref(res),
+                             C.byref(tcp))
+    return (Result(x, res.f, res.pg_inf, res.gfree_inf, res.iters, res.n_fg, res.n_backtracks,
+                   res.n_free, res.status, res.last_branch, res.n_fallbacks), tcp.value)
 
 
 @dataclass

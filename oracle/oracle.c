@@ -23,10 +23,12 @@
  * "parity unpinned" except the iteration COUNT of orc_minimize (the paper
  * prints no trajectory; PAPER.md:438 gives only "30-40 iterations").
  */
+#define _POSIX_C_SOURCE 199309L   /* clock_gettime for the N3 Cauchy-point timer */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 /* ------------------------------------------------------------------ */
 /* Elementwise pieces                                                  */
@@ -894,4 +896,165 @@ int64_t orc_cauchy_point(int64_t n, const double* x, const double* g, const doub
     for (int j = 0; j < k; ++j) c[j] = cc[j];
     free(M); free(d); free(F);
     return passed;
+}
+
+/* ------------------------------------------------------------------ */
+/* the ORIGINAL L-BFGS-B (Byrd, Lu, Nocedal, Zhu 1995) */
+/* on the LSQ objective, the baseline of PAPER.md:441-457 ("L-BFGS-B   */
+/* CPU"): per iteration                                                */
+/*   1. stop when ||P(x - g) - x||_inf <= tol (the projected gradient);  */
+/*   2. generalized Cauchy point x^c (Algorithm CP, orc_cauchy_point);   */
+/*   3. direct primal subspace minimisation over the free set F of x^c   */
+/*      (BLNZ section 5.1): r^c = Z^T (g + theta (x^c - x) - W M c),     */
+/*      d^u = -(1/theta) r^c - (1/theta^2) Z^T W N^{-1} M W^T Z r^c,     */
+/*      N = I - (1/theta) M W^T Z Z^T W, then the largest a* <= 1 keeping */
+/*      x^c + a* d^u in the box (backtrack);                             */
+/*   4. Armijo backtracking (same c1 / shrink as the modified method,    */
+/*      reading R34) along d = xbar - x from alpha = 1;                   */
+/*   5. the pair (s, y) is kept iff s^T y > eps y^T y (BLNZ: skip        */
+/*      otherwise), theta = y^T y / s^T y of the newest kept pair, m_hist */
+/*      pairs.                                                            */
+/* *cp_seconds receives the total time spent in step 2.                 */
+/* ------------------------------------------------------------------ */
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+void orc_lbfgsb_original(const orc_lsq* P, const double* l, const double* u, int32_t m_hist,
+                         const orc_opts* o, double* x, orc_result* res, double* cp_seconds)
+{
+    const int64_t nv = lsq_nvars(P), m = P->m;
+    const size_t nvb = sizeof(double) * (size_t)(nv > 0 ? nv : 1);
+    const size_t mb = sizeof(double) * (size_t)(m > 0 ? m : 1);
+    double *g = malloc(nvb), *gn = malloc(nvb), *xc = malloc(nvb), *xb = malloc(nvb), *d = malloc(nvb);
+    double *xt = malloc(nvb), *r = malloc(mb), *rt = malloc(mb), *q = malloc(mb), *rc = malloc(nvb);
+    double *S = malloc(nvb * (size_t)(m_hist > 0 ? m_hist : 1)), *Y = malloc(nvb * (size_t)(m_hist > 0 ? m_hist : 1));
+    int32_t h = 0;
+    double theta = 1.0, tcp = 0.0;
+    memset(res, 0, sizeof(*res));
+    orc_clip(nv, x, l, u, x);
+    lsq_residual(P, x, r);
+    double f = quad_value(P, x, r) + lsq_phi(P, x, NULL, NULL);
+    lsq_grad(P, x, r, g);
+    res->n_fg = 1;
+    int64_t k = 0;
+    int32_t status = ORC_MAX_ITERS;
+    for (;;) {
+        double pg = 0.0;
+        for (int64_t j = 0; j < nv; ++j) {
+            const double v = fabs(clip1(x[j] - g[j], l, u, j) - x[j]);
+            if (v > pg) pg = v;
+        }
+        if (pg <= o->tol) { status = ORC_CONVERGED; break; }
+        if (k >= o->max_iters) { status = ORC_MAX_ITERS; break; }
+        /* 2. generalized Cauchy point */
+        double c[32];
+        const double t0 = now_s();
+        if (orc_cauchy_point(nv, x, g, l, u, h, S, Y, theta, xc, c) < 0) { status = ORC_LINESEARCH_FAILURE; break; }
+        tcp += now_s() - t0;
+        /* 3. subspace minimisation over F = {i : l_i < xc_i < u_i} */
+        const int kk = 2 * h;
+        double M[32 * 32], v[32], Kf[32 * 32], Nm[32 * 32], tmp[32];   /* 2 m_hist <= 32 */
+        if (h > 0) orc_compact_m(nv, h, S, Y, theta, M);
+        double Mc[32];
+        mat_vec_small(kk, M, c, Mc);
+        for (int a = 0; a < kk; ++a) v[a] = 0.0;
+        for (int a = 0; a < kk * kk; ++a) Kf[a] = 0.0;
+        for (int64_t i = 0; i < nv; ++i) {
+            const int fr = (!l || xc[i] > l[i]) && (!u || xc[i] < u[i]);
+            if (!fr) { rc[i] = 0.0; continue; }
+            double wi[32];
+            for (int a = 0; a < h; ++a) { wi[a] = Y[(int64_t)a * nv + i]; wi[h + a] = theta * S[(int64_t)a * nv + i]; }
+            double wMc = 0.0;
+            for (int a = 0; a < kk; ++a) wMc += wi[a] * Mc[a];
+            rc[i] = g[i] + theta * (xc[i] - x[i]) - wMc;                /* reduced gradient */
+            for (int a = 0; a < kk; ++a) {
+                v[a] += wi[a] * rc[i];                                   /* W^T Z r^c */
+                for (int b = 0; b < kk; ++b) Kf[a * kk + b] += wi[a] * wi[b];   /* W^T Z Z^T W */
+            }
+        }
+        if (h > 0) {
+            mat_vec_small(kk, M, v, tmp);                                /* M W^T Z r^c */
+            for (int a = 0; a < kk; ++a)
+                for (int b = 0; b < kk; ++b) {
+                    double s = 0.0;
+                    for (int e = 0; e < kk; ++e) s += M[a * kk + e] * Kf[e * kk + b];
+                    Nm[a * kk + b] = (a == b ? 1.0 : 0.0) - s / theta;
+                }
+            invert_small(kk, Nm);
+            mat_vec_small(kk, Nm, tmp, v);                               /* N^{-1} M W^T Z r^c */
+        }
+        double astar = 1.0;
+        for (int64_t i = 0; i < nv; ++i) {
+            const int fr = (!l || xc[i] > l[i]) && (!u || xc[i] < u[i]);
+            if (!fr) { d[i] = 0.0; continue; }
+            double wv = 0.0;
+            for (int a = 0; a < h; ++a) wv += Y[(int64_t)a * nv + i] * v[a] + theta * S[(int64_t)a * nv + i] * v[h + a];
+            const double du = -rc[i] / theta - wv / (theta * theta);
+            d[i] = du;
+            if (du > 0.0 && u) { const double t = (u[i] - xc[i]) / du; if (t < astar) astar = t; }
+            if (du < 0.0 && l) { const double t = (l[i] - xc[i]) / du; if (t < astar) astar = t; }
+        }
+        if (astar < 0.0) astar = 0.0;
+        for (int64_t i = 0; i < nv; ++i) xb[i] = xc[i] + astar * d[i];
+        for (int64_t i = 0; i < nv; ++i) d[i] = xb[i] - x[i];            /* search direction */
+        /* 4. Armijo along d from alpha = 1 */
+        double gd = 0.0;
+        for (int64_t i = 0; i < nv; ++i) gd += g[i] * d[i];
+        if (!(gd < 0.0)) { if (h == 0) { status = ORC_LINESEARCH_FAILURE; break; } h = 0; theta = 1.0; continue; }
+        lsq_apply(P, d, q);
+        double alpha = 1.0, fnew = f;
+        int acc = 0;
+        for (int32_t t = 0; t <= o->max_backtracks; ++t) {
+            if (t > 0) alpha = o->shrink * alpha;
+            for (int64_t j = 0; j < nv; ++j) xt[j] = clip1(fma(alpha, d[j], x[j]), l, u, j);
+            for (int64_t i = 0; i < m; ++i) rt[i] = fma(alpha, q[i], r[i]);
+            res->n_fg += 1;
+            if (o->armijo_diff) {                                       /* R29 */
+                const double dl = orc_armijo_delta(P, nv, x, r, q, d, l, u, alpha);
+                if (dl <= o->c1 * alpha * gd) { acc = 1; fnew = f + dl; break; }
+                res->n_backtracks += 1;
+                continue;
+            }
+            const double ft = quad_value(P, xt, rt) + lsq_phi(P, xt, NULL, NULL);
+            if (ft <= f + o->c1 * alpha * gd) { acc = 1; fnew = ft; break; }
+            res->n_backtracks += 1;
+        }
+        if (!acc) { if (h == 0) { status = ORC_LINESEARCH_FAILURE; break; } h = 0; theta = 1.0; continue; }
+        lsq_grad(P, xt, rt, gn);
+        /* 5. pair update */
+        double sy = 0.0, yy = 0.0;
+        for (int64_t j = 0; j < nv; ++j) {
+            const double sj = xt[j] - x[j], yj = gn[j] - g[j];
+            sy += sj * yj; yy += yj * yj;
+        }
+        if (sy > o->eps * yy && m_hist > 0) {
+            if (h == m_hist) {
+                memmove(S, S + nv, nvb * (size_t)(m_hist - 1));
+                memmove(Y, Y + nv, nvb * (size_t)(m_hist - 1));
+                h = m_hist - 1;
+            }
+            for (int64_t j = 0; j < nv; ++j) { S[(int64_t)h * nv + j] = xt[j] - x[j]; Y[(int64_t)h * nv + j] = gn[j] - g[j]; }
+            h += 1;
+            theta = yy / sy;
+        }
+        memcpy(x, xt, nvb); memcpy(g, gn, nvb); memcpy(r, rt, mb);
+        f = fnew;
+        ++k;
+    }
+    lsq_residual(P, x, r);
+    f = quad_value(P, x, r) + lsq_phi(P, x, NULL, NULL);
+    lsq_grad(P, x, r, g);
+    double pg = 0.0;
+    for (int64_t j = 0; j < nv; ++j) {
+        const double v = fabs(clip1(x[j] - g[j], l, u, j) - x[j]);
+        if (v > pg) pg = v;
+    }
+    res->f = f; res->pg_inf = pg; res->iters = k; res->status = status;
+    if (cp_seconds) *cp_seconds = tcp;
+    free(g); free(gn); free(xc); free(xb); free(d); free(xt); free(r); free(rt); free(q); free(rc);
+    free(S); free(Y);
 }
