@@ -104,4 +104,4 @@ def test_oracle_independent_of_product():
             for m in imp.finditer(src):
                 assert "paper_2203_16340_b200" not in m.group(2), (f, m.group(0))
             for m in inc.finditer(src):
-                assert m.group(1) in ("math.h", "stdint.h", "stdlib.h", "string.h"), (f, m.group(0))
+                assert m.group(1) in ("math.h", "stdint.h", "stdlib.h", "string.h", "time.h"), (f, m.group(0))
