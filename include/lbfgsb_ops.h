@@ -76,6 +76,19 @@ lbfgsb_err lbfgsb_op_cauchy_point(lbfgsb_t* h, const double* x, const double* g,
                                   const double* S, const double* Y, double theta, double* xcp,
                                   double* c, int64_t* passed, double* scan_ms);
 
+/* the ORIGINAL L-BFGS-B (Byrd, Lu, Nocedal, Zhu 1995) on the
+ * GPU, the paper's "L-BFGS-B GPU" baseline: per iteration
+ * the projected-gradient test, the generalized Cauchy point (breakpoint loop
+ * on one thread, as lbfgsb_op_cauchy_point), the direct primal subspace
+ * minimisation with backtracking, Armijo (c1, shrink of the options) along
+ * xbar - x, the pair kept iff s^T y > eps y^T y.  Host-driven, one sync per
+ * step.  obj: an LSQ objective without c / delta (plain least squares); the
+ * handle's box; m_hist <= 8.  x (DEVICE) in x^0 / out x*.  res->f is
+ * 1/2 ||M~x - b||^2 at x*; (host, may be NULL) *cp_ms = device time of the
+ * single-thread Cauchy-point loops.  Errors: ARG, UNSUPPORTED, CUDA. */
+lbfgsb_err lbfgsb_solve_original(lbfgsb_t* h, const lbfgsb_objective* obj, double* x, double tol,
+                                 lbfgsb_result* res, double* cp_ms);
+
 /* Loopback verification of the column-sharded path on ONE device: the nranks
  * handles hs[p] (created with lbfgsb_create, n = that shard's variables, all
  * on the same device) act as logical ranks p = 0..nranks-1 of a sharded

@@ -107,13 +107,14 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
     L.lbfgsb_op_gaussian_kernel.argtypes = [vp, _c_i64, _c_i64, _c_d, vp, _c_i64, vp]
     L.lbfgsb_objective_transport.argtypes = [vp, _c_i64, _c_i64, _c_i32, _c_d, C.POINTER(vp)]
+    L.lbfgsb_solve_original.argtypes = [vp, vp, vp, _c_d, C.POINTER(_Res), C.POINTER(_c_d)]
     L.lbfgsb_solve_batched_lsq.argtypes = [_c_i32, _c_i64, _c_i64, vp, vp, vp, vp, vp, _c_i32,
                                            C.POINTER(_Opts), _c_d, vp, C.POINTER(_Res)]
     L.lbfgsb_op_cauchy_point.argtypes = [vp, vp, vp, _c_i32, vp, vp, _c_d, vp, C.POINTER(_c_d),
                                          C.POINTER(_c_i64), C.POINTER(_c_d)]
     L.al_solve_transport.argtypes = [vp, vp, vp, vp, C.POINTER(_AlOpts), vp, vp, C.POINTER(_AlRes)]
     for name in ("lbfgsb_objective_transport", "al_solve_transport", "lbfgsb_op_cauchy_point",
-                 "lbfgsb_solve_batched_lsq",
+                 "lbfgsb_solve_batched_lsq", "lbfgsb_solve_original",
                  "lbfgsb_create", "lbfgsb_create_sharded", "lbfgsb_objective_lsq",
                  "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
@@ -426,6 +427,13 @@ class Solver:
                         r.status, [], [])
 
     # ---- op-level entry points (lbfgsb_ops.h) ----
+    def solve_original(self, obj, x, tol: float = 0.0):
+        """The original L-BFGS-B (SURVEY N3 baseline): returns (Result, Cauchy-point ms)."""
+        r = _Res()
+        ms = _c_d()
+        _check(_lib.lbfgsb_solve_original(self._h, obj._h, _ptr(x), float(tol), C.byref(r), C.byref(ms)))
+        return Result.from_c(r), ms.value
+
     def op_cauchy_point(self, x, g, S=None, Y=None, theta=1.0):
         """Generalized Cauchy point of the original L-BFGS-B (baseline):
         returns dict(xcp, c, passed, scan_ms)."""

@@ -37,6 +37,7 @@ struct CpArgs {
     double* heap_g;                          // global heap (2 doubles per entry) when smem is short
     int64_t heap_cap_smem;                   // entries that fit in dynamic smem
     double* scal;                            // out: [0] t_old, [1] passed, [2..2+2h) c
+    double* Mout;                            // out (may be NULL): M (2h x 2h row-major), then M c (2h)
 };
 
 __global__ void __launch_bounds__(NT) k_cp_prep(CpArgs A)
@@ -164,6 +165,10 @@ __global__ void k_cp_scan(CpArgs A)
     if (fp == 0.0) {                                            // d = 0: x is the Cauchy point
         A.scal[0] = 0.0; A.scal[1] = 0.0;
         for (int j = 0; j < k; ++j) A.scal[2 + j] = 0.0;
+        if (A.Mout) {
+            for (int j = 0; j < k * k; ++j) A.Mout[j] = M[j];
+            for (int j = 0; j < k; ++j) A.Mout[k * k + j] = 0.0;
+        }
         return;
     }
     // heap of the breakpoints {t_i > 0}, keyed (t_i, i)
@@ -218,6 +223,11 @@ __global__ void k_cp_scan(CpArgs A)
     A.scal[0] = told;
     A.scal[1] = (double)passed;
     for (int j = 0; j < k; ++j) A.scal[2 + j] = c[j];
+    if (A.Mout) {                                               // for the subspace minimisation
+        for (int j = 0; j < k * k; ++j) A.Mout[j] = M[j];
+        cp_matvec(k, M, c, Mv);
+        for (int j = 0; j < k; ++j) A.Mout[k * k + j] = Mv[j];
+    }
 }
 
 __global__ void __launch_bounds__(NT) k_cp_final(CpArgs A)
@@ -233,10 +243,11 @@ __global__ void __launch_bounds__(NT) k_cp_final(CpArgs A)
 int launch_cauchy(int64_t n, const double* x, const double* g, const double* l, const double* u, int h,
                   const double* S, const double* Y, double theta, double* d, double* tk, double* xcp,
                   double* part, double* red, unsigned* ticket, double* heap_g, double* scal,
-                  cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1)
+                  cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, double* Mout)
 {
     if (h < 0 || h > CP_MAXH) return 1;
     CpArgs A;
+    A.Mout = Mout;
     A.n = n; A.x = x; A.g = g; A.l = l; A.u = u; A.h = h; A.S = S; A.Y = Y; A.theta = theta;
     A.d = d; A.tk = tk; A.xcp = xcp; A.part = part; A.red = red; A.ticket = ticket;
     A.heap_g = heap_g; A.scal = scal;

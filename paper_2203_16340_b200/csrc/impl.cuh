@@ -193,8 +193,32 @@ int launch_batch(int32_t batch, int64_t m, int64_t n, const double* M, const dou
 int launch_cauchy(int64_t n, const double* x, const double* g, const double* l, const double* u, int h,
                   const double* S, const double* Y, double theta, double* d, double* tk, double* xcp,
                   double* part, double* red, unsigned* ticket, double* heap_g, double* scal,
-                  cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1);
+                  cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, double* Mout = nullptr);
 int cauchy_nr();
+// original.cu: the rest of the original L-BFGS-B iteration
+struct OrigArgs {
+    int64_t n, m;
+    const double* x; const double* g; const double* l; const double* u;
+    const double* xc;                        // Cauchy point
+    int h;                                   // pairs (compact, oldest first)
+    const double* S; const double* Y;
+    double theta;
+    const double* Mm;                        // M (2h x 2h) then M c (2h) from the Cauchy scan
+    double* rc;                              // n: reduced gradient on F (0 elsewhere)
+    double* du;                              // n: subspace step on F
+    double* d;                               // n: search direction xbar - x
+    double* part; double* red; unsigned* ticket;
+    double* z;                               // 2h: N^{-1} M W^T Z r^c
+    double* out;                             // scalars: [0] alpha*, [1] g^T d, [2] pg, [3] s^T y, [4] y^T y, [5] sum r^2
+};
+void launch_orig_pg(const OrigArgs& A, cudaStream_t st);
+void launch_orig_subspace(const OrigArgs& A, cudaStream_t st);
+void launch_orig_step(const OrigArgs& A, double* x, const double* dvec, double* r, const double* q, double alpha,
+                      double* s_out, cudaStream_t st);
+void launch_orig_pair(const OrigArgs& A, const double* gnew, const double* gold, const double* s, double* y_out,
+                      cudaStream_t st);
+void launch_orig_residual(const OrigArgs& A, double* r, const double* b, cudaStream_t st);
+int orig_nr();
 // transport.cu
 void launch_tsum(const Prob& P, cudaStream_t st, int mode);
 void launch_tviol(const Prob& P, cudaStream_t st, double rho, int update, double* out_dev);

@@ -120,8 +120,10 @@ struct lbfgsb_t {
     DevBuf Mh, bh, xh;
     // transport objective
     DevBuf tlam, te, tap, trow, tcol, tsp, tspr, tspc, tticket, tvout;
-    // Cauchy-point op
+    // Cauchy-point op and the original L-BFGS-B
     DevBuf cp_d, cp_t, cp_xcp, cp_part, cp_red, cp_heap, cp_scal, cp_ticket;
+    DevBuf og_S, og_Y, og_s, og_y, og_rc, og_du, og_d, og_gn, og_r, og_q, og_M, og_part, og_red, og_z, og_out,
+        og_ticket;
     Ctrl* ctrl = nullptr;           // device
     Ctrl* hc = nullptr;             // pinned host mirror
     // graph cache
@@ -292,7 +294,9 @@ extern "C" void lbfgsb_destroy(lbfgsb_t* h)
                       &h->gram_all, &h->kkt_all, &h->tlam, &h->te, &h->tap, &h->trow,
                       &h->tcol, &h->tsp, &h->tspr, &h->tspc, &h->tticket, &h->tvout, &h->cp_d,
                       &h->cp_t, &h->cp_xcp, &h->cp_part, &h->cp_red, &h->cp_heap, &h->cp_scal,
-                      &h->cp_ticket};
+                      &h->cp_ticket, &h->og_S, &h->og_Y, &h->og_s, &h->og_y, &h->og_rc, &h->og_du,
+                      &h->og_d, &h->og_gn, &h->og_r, &h->og_q, &h->og_M, &h->og_part, &h->og_red,
+                      &h->og_z, &h->og_out, &h->og_ticket};
     for (DevBuf* b : bufs) b->release();
     if (h->ctrl) cudaFree(h->ctrl);
     if (h->hc) cudaFreeHost(h->hc);
@@ -1254,6 +1258,184 @@ extern "C" lbfgsb_err lbfgsb_solve_batched_lsq(int32_t batch, int64_t m, int64_t
     CK(cudaStreamSynchronize(st));
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     for (int32_t i = 0; i < batch; ++i) res[i].seconds = secs;
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ N3: the original L-BFGS-B
+// Host-driven loop (one synchronisation per step, as the baseline ran):
+// projected-gradient test; generalized Cauchy point (cauchy.cu: parallel
+// breakpoints, ONE-thread breakpoint loop); direct primal subspace
+// minimisation and backtrack (original.cu); Armijo along d = xbar - x with
+// the same trial machinery as lbfgsb_op_trials; pair kept iff s^T y > eps
+// y^T y; theta = y^T y / s^T y.  Mirrors orc_lbfgsb_original.
+extern "C" lbfgsb_err lbfgsb_solve_original(lbfgsb_t* h, const lbfgsb_objective* obj, double* x_user, double tol,
+                                            lbfgsb_result* res, double* cp_ms)
+{
+    if (!h || !obj || !x_user) return fail(LBFGSB_ERR_ARG, "NULL handle, objective or x");
+    if (obj->kind != 0 || obj->qp || obj->c || obj->delta != 0.0)
+        return fail(LBFGSB_ERR_UNSUPPORTED, "the original L-BFGS-B runs plain least squares (no c, delta)");
+    if (h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "single-GPU");
+    if (h->mh > 8) return fail(LBFGSB_ERR_UNSUPPORTED, "m_hist <= 8");
+    auto t0 = std::chrono::steady_clock::now();
+    const double tl = tol > 0 ? tol : h->o.tol;
+    Prob P;
+    TRY(make_prob(h, obj, P));
+    set_sep(P);
+    cudaStream_t st = h->st;
+    const int64_t n = h->n, m = P.m, mh = h->mh;
+    const size_t nb = sizeof(double) * (size_t)n, mb = sizeof(double) * (size_t)m;
+    TRY(h->og_S.ensure(nb * mh)); TRY(h->og_Y.ensure(nb * mh)); TRY(h->og_s.ensure(nb)); TRY(h->og_y.ensure(nb));
+    TRY(h->og_rc.ensure(nb)); TRY(h->og_du.ensure(nb)); TRY(h->og_d.ensure(nb)); TRY(h->og_gn.ensure(nb));
+    TRY(h->og_r.ensure(mb)); TRY(h->og_q.ensure(mb));
+    TRY(h->og_M.ensure(sizeof(double) * 300)); TRY(h->og_z.ensure(sizeof(double) * 32));
+    TRY(h->og_out.ensure(sizeof(double) * 8));
+    TRY(h->og_part.ensure(sizeof(double) * (size_t)(2 * sm_count()) * (orig_nr() > 4 ? orig_nr() : 4)));
+    TRY(h->og_red.ensure(sizeof(double) * (size_t)orig_nr()));
+    TRY(h->og_ticket.ensure(sizeof(unsigned) * 8, true));
+    TRY(h->cp_d.ensure(nb)); TRY(h->cp_t.ensure(nb)); TRY(h->cp_xcp.ensure(nb)); TRY(h->cp_heap.ensure(2 * nb));
+    TRY(h->cp_part.ensure(sizeof(double) * (size_t)(2 * sm_count()) * cauchy_nr()));
+    TRY(h->cp_red.ensure(sizeof(double) * (size_t)cauchy_nr()));
+    TRY(h->cp_scal.ensure(sizeof(double) * 32));
+    TRY(h->cp_ticket.ensure(sizeof(unsigned) * 4, true));
+    double* x = P.x;
+    double* g = P.g;
+    double* gn = h->og_gn.d();
+    double* r = h->og_r.d();
+    double* q = h->og_q.d();
+    CK(cudaMemcpyAsync(x, x_user, nb, cudaMemcpyDeviceToDevice, st));
+    launch_clip(P, st);
+    OrigArgs A{};
+    A.n = n; A.m = m; A.l = P.l; A.u = P.u; A.xc = h->cp_xcp.d();
+    A.S = h->og_S.d(); A.Y = h->og_Y.d(); A.Mm = h->og_M.d();
+    A.rc = h->og_rc.d(); A.du = h->og_du.d(); A.d = h->og_d.d();
+    A.part = h->og_part.d(); A.red = h->og_red.d(); A.ticket = static_cast<unsigned*>(h->og_ticket.p);
+    A.z = h->og_z.d(); A.out = h->og_out.d();
+    double out[8];
+    auto read_out = [&]() -> lbfgsb_err {
+        CK(cudaMemcpyAsync(out, A.out, sizeof out, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return LBFGSB_OK;
+    };
+    // f, r = M~x - b, g
+    auto eval = [&](double* gout, double& f) -> lbfgsb_err {
+        launch_fwd(P, st, FWD_P, x, r);
+        A.x = x;
+        launch_orig_residual(A, r, P.b, st);
+        launch_bwd(P, st, BWD_PLAIN, r, gout);
+        CK(cudaGetLastError());
+        TRY(read_out());
+        f = 0.5 * out[5];
+        return LBFGSB_OK;
+    };
+    double f = 0.0;
+    TRY(eval(g, f));
+    int hp = 0;
+    double theta = 1.0, tcp = 0.0;
+    long long k = 0, nfg = 1, nbt = 0, nfb = 0;
+    int status = S_MAX_ITERS;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    for (;;) {
+        A.x = x; A.g = g; A.h = hp; A.theta = theta;
+        launch_orig_pg(A, st);
+        TRY(read_out());
+        if (out[2] <= tl) { status = S_CONVERGED; break; }
+        if (k >= h->o.max_iters) { status = S_MAX_ITERS; break; }
+        // generalized Cauchy point (the single-thread loop is bracketed by e0 / e1)
+        if (launch_cauchy(n, x, g, P.l, P.u, hp, A.S, A.Y, theta, h->cp_d.d(), h->cp_t.d(), h->cp_xcp.d(),
+                          h->cp_part.d(), h->cp_red.d(), static_cast<unsigned*>(h->cp_ticket.p), h->cp_heap.d(),
+                          h->cp_scal.d(), st, e0, e1, h->og_M.d()))
+            return fail(LBFGSB_ERR_ARG, "history too long");
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        tcp += ms;
+        // subspace minimisation, backtrack, direction, g^T d
+        launch_orig_subspace(A, st);
+        CK(cudaGetLastError());
+        TRY(read_out());
+        const double gd = out[1];
+        if (!(gd < 0.0)) {
+            if (hp == 0) { status = S_LS_FAIL; break; }
+            hp = 0; theta = 1.0; ++nfb;
+            continue;
+        }
+        // Armijo on the carried residual along d (alpha = 1, shrink, ...)
+        launch_fwd(P, st, FWD_P, A.d, q);
+        double alpha = 1.0, fnew = f;
+        bool acc = false;
+        for (int t0b = 0; t0b <= h->o.max_backtracks && !acc; t0b += KT) {
+            init_ctrl(h, tl);
+            h->hc->alpha0 = alpha;
+            h->hc->rho = 1.0;
+            TRY(ctrl_to_dev(h, st));
+            Prob PT = P;
+            PT.x = x;
+            launch_sep(PT, st, SEP_OP, A.d);
+            launch_ls(PT, st, LS_OP, r, q, h->fout.d(), KT);
+            double ft[KT];
+            CK(cudaMemcpyAsync(ft, h->fout.p, sizeof ft, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            double a = alpha;
+            for (int t = 0; t < KT && t0b + t <= h->o.max_backtracks; ++t) {
+                if (t > 0) a = a * h->o.shrink;
+                ++nfg;
+                if (ft[t] <= f + h->o.c1 * a * gd) { acc = true; alpha = a; fnew = ft[t]; break; }
+                ++nbt;
+            }
+            if (!acc) alpha = a * h->o.shrink;
+        }
+        if (!acc) {
+            if (hp == 0) { status = S_LS_FAIL; break; }
+            hp = 0; theta = 1.0; ++nfb;
+            continue;
+        }
+        launch_orig_step(A, x, A.d, r, q, alpha, h->og_s.d(), st);
+        launch_bwd(P, st, BWD_PLAIN, r, gn);
+        launch_orig_pair(A, gn, g, h->og_s.d(), h->og_y.d(), st);
+        CK(cudaGetLastError());
+        TRY(read_out());
+        const double sy = out[3], yy = out[4];
+        if (sy > h->o.eps * yy) {
+            if (hp == mh) {                                      // drop the oldest pair
+                for (int i = 1; i < mh; ++i) {
+                    CK(cudaMemcpyAsync(h->og_S.d() + (int64_t)(i - 1) * n, h->og_S.d() + (int64_t)i * n, nb,
+                                       cudaMemcpyDeviceToDevice, st));
+                    CK(cudaMemcpyAsync(h->og_Y.d() + (int64_t)(i - 1) * n, h->og_Y.d() + (int64_t)i * n, nb,
+                                       cudaMemcpyDeviceToDevice, st));
+                }
+                hp = mh - 1;
+            }
+            CK(cudaMemcpyAsync(h->og_S.d() + (int64_t)hp * n, h->og_s.d(), nb, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(h->og_Y.d() + (int64_t)hp * n, h->og_y.d(), nb, cudaMemcpyDeviceToDevice, st));
+            ++hp;
+            theta = yy / sy;
+        }
+        CK(cudaMemcpyAsync(g, gn, nb, cudaMemcpyDeviceToDevice, st));
+        f = fnew;
+        ++k;
+    }
+    // final refresh: r = M~x - b, f, g, pg
+    double ff = 0.0;
+    TRY(eval(g, ff));
+    A.x = x; A.g = g;
+    launch_orig_pg(A, st);
+    TRY(read_out());
+    CK(cudaMemcpyAsync(x_user, x, nb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    if (res) {
+        std::memset(res, 0, sizeof *res);
+        res->f = ff;                                             // 1/2 ||r||^2 (plain LSQ)
+        res->pg_inf = out[2];
+        res->iters = k;
+        res->n_fg = nfg;
+        res->n_backtracks = nbt;
+        res->n_fallbacks = nfb;
+        res->status = status;
+        res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (cp_ms) *cp_ms = tcp;
     return LBFGSB_OK;
 }
 
