@@ -227,10 +227,9 @@ __device__ void gram_tail(const Prob& P, Ctrl* C, const EpiCtx& E, const GramEnt
                           double gmax, double cnt, double* red, double* buf, int bufn, double* stash,
                           double* Gs)
 {
-    const int G = gridDim.x, cta = blockIdx.x;
     const int nh = E.nh, nb = E.nb, ne = nb * (nb + 1) / 2;
     const int ntot = ne + (P.screen_full ? nh : 0);
-    double* out = P.gram_part + (int64_t)cta * GRAM_STRIDE;
+    double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
     ent.finalize(gacc, stash, out, ntot);
     gram_tail_after(P, C, E, gmax, cnt, red, buf, bufn, stash, Gs);
 }
