@@ -288,7 +288,13 @@ def run_ours(args):
 
 def run_sharded(args) -> int:
     """N > 1 step: every rank holds a C2-sized column block (weak scaling,
-    n = 10000 N); value = Alg. 1 iterations x N / max-over-ranks device time."""
+    n = 10000 N); value = Alg. 1 iterations x N / max-over-ranks device time.
+    The per-iteration exchange runs over peer memory (--xchg p2p, the
+    default: the producing kernels store their packs into every rank's CUDA-IPC
+    mapped mailbox) or through the library's NCCL communicator (--xchg nccl);
+    if any rank cannot map its peers, all ranks fall back to NCCL and the
+    line says so."""
+    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2203_16340_b200 as lb
@@ -310,7 +316,23 @@ def run_sharded(args) -> int:
     b = torch.from_numpy(p.b).to(dev)
     lo = torch.zeros(ncl, dtype=torch.float64, device=dev)
     stream = torch.cuda.Stream(device=dev)
-    solver = sharded.make_sharded_solver(ncl, ncl * world, mh, lo, lb.Options(tol=tol, profile=True), stream)
+    opts = lb.Options(tol=tol, profile=True)
+    xchg = args.xchg
+    solver, err = None, ""
+    if xchg == "p2p":
+        try:
+            solver = lb.Solver(ncl, mh, lower=lo, opts=opts, stream=stream, rank=rank, nranks=world,
+                               n_global=ncl * world, p2p_m_max=m)
+            solver.p2p_open(sharded.all_gather_bytes(solver.ipc_handle()))
+        except Exception as e:          # noqa: BLE001 -- collective decision below
+            solver, err = None, f"{type(e).__name__}: {e}"[:200]
+        oks = sharded.all_gather_bytes(b"1" if solver is not None else err.encode() or b"0")
+        if any(o != b"1" for o in oks):
+            solver, xchg = None, "nccl"
+            err = "; ".join(o.decode() for o in oks if o != b"1")
+        dist.barrier()
+    if solver is None:
+        solver = sharded.make_sharded_solver(ncl, ncl * world, mh, lo, opts, stream, xchg="nccl")
     obj = lb.LSQObjective(M, b=b)
     x = torch.zeros(ncl, dtype=torch.float64, device=dev)
     with torch.cuda.stream(stream):
@@ -322,21 +344,56 @@ def run_sharded(args) -> int:
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
         iters = 0
-        for _ in range(args.steps):
-            x.zero_()
-            r = solver.solve(obj, x)
-            iters += r.iters
-        e1.record(stream)
-        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                x.zero_()
+                r = solver.solve(obj, x)
+                iters += r.iters
+            e1.record(stream)
+            torch.cuda.synchronize()
         dist.barrier()
         ms = sharded.max_over_ranks(e0.elapsed_time(e1), device=dev)
     prof = solver.profile(reset=True)
+    clocks = clk.summary()
+    all_reasons = sharded.all_gather_bytes(json.dumps(clocks.get("reasons", [])).encode())
+
+    # ---- e2e through the public API: per step, H2D of this rank's A block and b
+    # from pinned host memory, the solve, D2H of x (host wall clock, max over ranks)
+    Mh = torch.from_numpy(np.ascontiguousarray(p.M.T)).pin_memory()     # (ncl, m) row-major = A col-major
+    bh = torch.from_numpy(p.b.copy()).pin_memory()
+    xh = torch.zeros(ncl, dtype=torch.float64).pin_memory()
+    Md = torch.empty((ncl, m), dtype=torch.float64, device=dev)
+    bd = torch.empty(m, dtype=torch.float64, device=dev)
+    obj_e = lb.LSQObjective(Md.t(), b=bd)
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            Md.copy_(Mh, non_blocking=True)
+            bd.copy_(bh, non_blocking=True)
+            x.zero_()
+            rr = solver.solve(obj_e, x)
+            xh.copy_(x, non_blocking=True)
+            stream.synchronize()
+        return rr.iters
+
+    e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    e2e_iters = sum(e2e_step() for _ in range(e2e_steps))
+    e2e_dt = sharded.max_over_ranks(time.perf_counter() - t0, device=dev)
     if rank == 0:
+        peak, peak_src = _peaks()
         value = iters * world / (ms / 1e3)
         bwd_ms, bwd_n = prof["gemvT_epi (k_bwd)"]
         bwd_bytes = 8 * m * ncl + 8 * m + 9 * 8 * ncl
+        achieved = (bwd_bytes / (bwd_ms / bwd_n / 1e3) / 1e9) if bwd_n else None
+        reasons = sorted({x for rs in all_reasons for x in json.loads(rs)})
+        clocks["reasons"] = reasons
+        clocks["note"] = "sm_mhz sampled on rank 0's GPU; reasons merged over all ranks"
         line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -344,15 +401,27 @@ def run_sharded(args) -> int:
                 "config": {"workload": f"column-sharded NNLS m={m} n={ncl}x{world} fp64 "
                                        f"(C2-sized block per GPU, weak scaling)",
                            "m": m, "n_local": ncl, "n_global": ncl * world, "m_hist": mh,
-                           "tol": tol, "parallelism": f"column-sharded x{world} (NCCL all-gather)",
+                           "tol": tol,
+                           "parallelism": f"column-sharded x{world} ("
+                                          + ("P2P mailboxes over NVLink, pushes fused in the producing "
+                                             "kernels" if xchg == "p2p" else "NCCL all-gather") + ")",
+                           "xchg": xchg, "xchg_fallback_reason": err or None,
                            "l2": "inputs larger than L2"},
                 "iters_per_solve": r.iters, "f": r.f, "pg_inf": r.pg_inf,
-                "roofline": {"bound": "hbm", "unit": "GB/s",
-                             "achieved": (bwd_bytes / (bwd_ms / bwd_n / 1e3) / 1e9) if bwd_n else None,
+                "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": peak,
+                             "frac": (achieved / peak) if achieved else None, "traffic": None,
+                             "peak_source": peak_src, "bytes_per_launch": bwd_bytes,
+                             "avg_launch_us": 1e3 * bwd_ms / max(bwd_n, 1),
                              "kernel": "k_bwd_s (rank 0)"},
-                "gpu_launches": prof["all_kernel_launches"][1]}
+                "e2e": {"value": e2e_iters * world / e2e_dt, "unit": "iters/s",
+                        "h2d_bytes_per_step": 8 * (m * ncl + m) * world, "d2h_bytes_per_step": 8 * ncl * world,
+                        "steps": e2e_steps, "ms_per_step": 1e3 * e2e_dt / e2e_steps,
+                        "api": "Solver.solve (lbfgsb_solve) after pinned H2D of every rank's A block and b, "
+                               "D2H of x; host wall clock, max over ranks"},
+                "gpu_launches": prof["all_kernel_launches"][1], "clocks": clocks}
         print(json.dumps(line), flush=True)
     dist.barrier()
+    solver.close()
     dist.destroy_process_group()
     return 0
 
@@ -364,8 +433,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--xchg", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 exchange: peer-memory mailboxes (default) or NCCL all-gather")
     ap.add_argument("--force-sharded", action="store_true",
-                    help="run the N>1 sharded code path even at N=1 (1-rank NCCL communicator)")
+                    help="run the N>1 sharded code path even at N=1 (1-rank communicator)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

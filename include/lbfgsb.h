@@ -144,6 +144,42 @@ lbfgsb_err lbfgsb_create_sharded(int64_t n_local, int64_t n_global, int32_t m_hi
 /* Fill out (host, 128 bytes) with a fresh ncclUniqueId (call on rank 0). */
 lbfgsb_err lbfgsb_nccl_unique_id(void* out);
 
+/* Column-sharded handle whose per-iteration exchange (SURVEY.md 8(a) a9,
+ * 8(e)) runs over PEER MEMORY instead of NCCL: every rank owns a mailbox
+ * (device, cudaMalloc, owned by the handle) holding the four gathered pack
+ * sections for residual length m <= m_max; the kernels that produce a pack
+ * (k_dir, k_fwd row blocks -- the m-length q partial -- k_bwd's Gram tail,
+ * k_kkt) store it straight into slot [rank] of every rank's mailbox and bump
+ * a counter there, and a one-thread wait kernel gates the rank-order
+ * reduction, so the exchanged bytes and their order equal the all-gather's
+ * (bit-identical solves).  Same arguments as lbfgsb_create_sharded, no
+ * NCCL id; nranks <= 8 (one NVSwitch box).  Connect with
+ * lbfgsb_p2p_ipc_handle on every rank, an all-gather of the 64-byte handles
+ * by the caller (e.g. torch.distributed), then lbfgsb_p2p_open; all ranks
+ * must be connected before any rank solves.  Errors: ARG (rank / nranks),
+ * DIM (m_max < 1, n_global < n_local), OOM, CUDA.  A peer that stops
+ * signalling makes lbfgsb_solve return LBFGSB_ERR_NCCL after 60 s. */
+lbfgsb_err lbfgsb_create_sharded_p2p(int64_t n_local, int64_t n_global, int32_t m_hist,
+                                     const double* lower_local, const double* upper_local,
+                                     const lbfgsb_opts* opts, void* cuda_stream, int32_t rank,
+                                     int32_t nranks, int64_t m_max, lbfgsb_t** out);
+
+/* out (host, 64 bytes): the cudaIpcMemHandle_t of this rank's mailbox. */
+lbfgsb_err lbfgsb_p2p_ipc_handle(lbfgsb_t* h, void* out);
+
+/* handles (host, nranks x 64 bytes, rank order, as gathered from
+ * lbfgsb_p2p_ipc_handle): map every peer's mailbox into this process
+ * (cudaIpcOpenMemHandle, peer access over NVLink enabled lazily; closed by
+ * lbfgsb_destroy).  The own slot is ignored.  Errors: ARG, CUDA. */
+lbfgsb_err lbfgsb_p2p_open(lbfgsb_t* h, const void* handles);
+
+/* Loopback form of the P2P exchange: nranks plain single-GPU handles of one
+ * process get mailboxes (m <= m_max) wired to each other directly, so that
+ * lbfgsb_solve_loopback (lbfgsb_ops.h) runs the P2P protocol -- pushes
+ * from the producing kernels, counter waits -- among logical ranks on one
+ * device.  Errors: ARG, DIM, OOM. */
+lbfgsb_err lbfgsb_p2p_connect_local(lbfgsb_t* const* hs, int32_t nranks, int64_t m_max);
+
 void lbfgsb_destroy(lbfgsb_t* h);
 
 /* ---- objectives --------------------------------------------------------- */

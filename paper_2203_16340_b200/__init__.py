@@ -20,7 +20,7 @@ from . import _build
 __all__ = ["Options", "ALOptions", "Result", "ALResult", "Solver", "LSQObjective",
            "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor",
            "solve_loopback", "nccl_unique_id", "QPObjective", "op_gaussian_kernel",
-           "TransportObjective", "solve_batched_lsq", "colmajor_batch"]
+           "TransportObjective", "solve_batched_lsq", "colmajor_batch", "p2p_connect_local"]
 
 _c_d, _c_i32, _c_i64, _c_vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
 
@@ -104,6 +104,11 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_solve_loopback.argtypes = [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), _c_i32, _c_d,
                                         C.POINTER(_Res)]
     L.lbfgsb_nccl_unique_id.argtypes = [vp]
+    L.lbfgsb_create_sharded_p2p.argtypes = [_c_i64, _c_i64, _c_i32, vp, vp, C.POINTER(_Opts), vp, _c_i32,
+                                            _c_i32, _c_i64, C.POINTER(vp)]
+    L.lbfgsb_p2p_ipc_handle.argtypes = [vp, vp]
+    L.lbfgsb_p2p_open.argtypes = [vp, vp]
+    L.lbfgsb_p2p_connect_local.argtypes = [C.POINTER(vp), _c_i32, _c_i64]
     L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
     L.lbfgsb_op_gaussian_kernel.argtypes = [vp, _c_i64, _c_i64, _c_d, vp, _c_i64, vp]
     L.lbfgsb_objective_transport.argtypes = [vp, _c_i64, _c_i64, _c_i32, _c_d, C.POINTER(vp)]
@@ -119,7 +124,8 @@ def load(build_if_needed: bool = True):
                  "lbfgsb_objective_callback", "lbfgsb_solve", "lbfgsb_solve_lsq_host", "al_solve",
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
                  "lbfgsb_profile_get", "lbfgsb_solve_loopback", "lbfgsb_nccl_unique_id",
-                 "lbfgsb_objective_qp", "lbfgsb_op_gaussian_kernel"):
+                 "lbfgsb_objective_qp", "lbfgsb_op_gaussian_kernel", "lbfgsb_create_sharded_p2p",
+                 "lbfgsb_p2p_ipc_handle", "lbfgsb_p2p_open", "lbfgsb_p2p_connect_local"):
         getattr(L, name).restype = _c_i32
     _lib = L
     return L
@@ -339,17 +345,26 @@ class Solver:
     """lbfgsb_create handle: n variables, box [lower, upper] (CUDA fp64 tensors
     or None for -inf / +inf), m_hist curvature pairs.  With ``nccl_id`` (the
     128-byte ncclUniqueId), ``rank`` and ``nranks`` it is an
-    lbfgsb_create_sharded handle owning n of ``n_global`` variables."""
+    lbfgsb_create_sharded handle owning n of ``n_global`` variables.  With
+    ``p2p_m_max`` instead (and rank / nranks) it is an
+    lbfgsb_create_sharded_p2p handle: the exchange runs over peer memory
+    (connect with ipc_handle() on every rank, then p2p_open(all handles))."""
 
     def __init__(self, n, m_hist=5, lower=None, upper=None, opts: Options | None = None,
-                 stream=None, nccl_id: bytes | None = None, rank=0, nranks=1, n_global=None):
+                 stream=None, nccl_id: bytes | None = None, rank=0, nranks=1, n_global=None,
+                 p2p_m_max: int | None = None):
         L = load()
         self.n = int(n)
         self.m_hist = int(m_hist)
         self.opts = opts or Options()
         o = self.opts._c()
         h = C.c_void_p()
-        if nccl_id is None:
+        if p2p_m_max is not None:
+            _check(L.lbfgsb_create_sharded_p2p(self.n, int(n_global if n_global is not None else n),
+                                               self.m_hist, _ptr(lower), _ptr(upper), C.byref(o),
+                                               _stream_ptr(stream), int(rank), int(nranks),
+                                               int(p2p_m_max), C.byref(h)))
+        elif nccl_id is None:
             _check(L.lbfgsb_create(self.n, self.m_hist, _ptr(lower), _ptr(upper), C.byref(o),
                                    _stream_ptr(stream), C.byref(h)))
         else:
@@ -359,6 +374,17 @@ class Solver:
                                            _stream_ptr(stream), C.cast(idb, C.c_void_p), int(rank),
                                            int(nranks), C.byref(h)))
         self._h = h
+
+    def ipc_handle(self) -> bytes:
+        """lbfgsb_p2p_ipc_handle: the 64-byte CUDA IPC handle of this rank's mailbox."""
+        buf = C.create_string_buffer(64)
+        _check(_lib.lbfgsb_p2p_ipc_handle(self._h, C.cast(buf, C.c_void_p)))
+        return buf.raw
+
+    def p2p_open(self, handles):
+        """lbfgsb_p2p_open: map the mailboxes of all ranks (list of 64-byte handles, rank order)."""
+        blob = C.create_string_buffer(b"".join(bytes(h) for h in handles), 64 * len(handles))
+        _check(_lib.lbfgsb_p2p_open(self._h, C.cast(blob, C.c_void_p)))
 
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -485,6 +511,14 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(load().lbfgsb_nccl_unique_id(C.cast(buf, C.c_void_p)))
     return buf.raw
+
+
+def p2p_connect_local(solvers, m_max):
+    """lbfgsb_p2p_connect_local: give len(solvers) single-GPU handles wired
+    mailboxes so that solve_loopback runs the P2P exchange protocol."""
+    R = len(solvers)
+    hs = (_c_vp * R)(*[s._h.value for s in solvers])
+    _check(load().lbfgsb_p2p_connect_local(hs, R, int(m_max)))
 
 
 def solve_loopback(solvers, objs, xs, tol=0.0) -> Result:

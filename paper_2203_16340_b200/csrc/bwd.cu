@@ -258,6 +258,7 @@ __device__ void gram_tail_after(const Prob& P, Ctrl* C, const EpiCtx& E, double 
     reduce_parts(P.gram_grp, ngrp, GRAM_STRIDE, nent, sel, buf, bufn, stash, Gs);
     if (P.sharded) {                                         // sharded: local Gram pack
         for (int e = threadIdx.x; e < nent; e += blockDim.x) P.pk_loc[off_gram(P) + e] = Gs[e];
+        if (P.p2p) p2p_push(P, XS_GRAM, off_gram(P), GRAM_STRIDE);
         return;
     }
     if (threadIdx.x != 0) return;
@@ -755,6 +756,190 @@ k_bwd_c(Prob P, int mode, const double* rvec, double* gout, int hmax, int cmax)
     }
     if (!E.gram) return;
     gram_tail(P, C, E, ent, gacc, gmax, cnt, red, stage, 4096, stash, Gs);
+}
+
+// ---------------------------------------------------------------- k_bwd_t
+// TMA variant for 2048 <= m <= 20480 (C2, C3): r' lives in REGISTERS, so
+// shared memory is a ring of ns x 32 KB cp.async.bulk stages for the column
+// stream.  Every WARP is its own pipeline: the CTA's balanced column range is
+// walked in 4096-row segments (NSC per column) and warp w owns rows
+// [512 w, 512 w + 512) of every segment (lane l: rows 512 w + 64 k + 2 l, +1),
+// so it issues its own 4 KB bulk copy per segment into its own slot of each
+// stage and waits on its own mbarrier; a slot is refilled by the same warp as
+// soon as its lanes are done with it.  No warp waits on another inside the
+// stream (a shared producer thread measured 295-395 us on C2: its refills
+// trail the slowest warp).  8 warps of <= 255 registers (2 per SMSP).
+// Column dots are reduced per group of 8; the epilogue, Gram and Alg. 3 tail
+// are those of k_bwd_s, with the ring as the tile buffer.
+constexpr int TT_THREADS = 256;
+constexpr int TT_WARPS = TT_THREADS / 32;
+constexpr int TT_ROWS = 4096;                 // rows per segment (32 KB)
+constexpr int TT_WROWS = TT_ROWS / TT_WARPS;  // rows per warp piece (512, 4 KB)
+constexpr int TT_STAGES = 6;
+constexpr int TT_KPS = TT_WROWS / 64;         // row pairs per lane per segment (8)
+constexpr int TT_NSC_MAX = 5;                 // m <= 20480
+constexpr int TT_CMAX = 2048;                 // dots slots (columns per CTA + 1); 192 + 16 KB + 8 KB static <= 227 KB
+
+template <int NSC>
+__global__ void __launch_bounds__(TT_THREADS, 1) k_bwd_t(Prob P, int mode, const double* rvec, double* gout, int ns)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    extern __shared__ __align__(1024) unsigned char smt[];
+    double* ring = reinterpret_cast<double*>(smt);                  // [ns][TT_WARPS][TT_WROWS]
+    double* dots = ring + (size_t)TT_STAGES * TT_ROWS;              // [cmax]
+    __shared__ __align__(8) uint64_t full[TT_STAGES][TT_WARPS];
+    __shared__ double red[TT_WARPS * BWD_NB];
+    __shared__ double stash[TT_THREADS];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
+    const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
+    const int64_t i0 = (int64_t)cta * m / G, i1 = (int64_t)(cta + 1) * m / G;
+    const bool iter = mode == BWD_ITER;
+    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
+    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
+    double* rnext = P.rbuf[rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t ccount = j1 - j0;
+
+    if (tid < TT_STAGES * TT_WARPS) mbar_init(&full[tid / TT_WARPS][tid % TT_WARPS], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    // this warp's issue cursor: column ic, segment is
+    int64_t ic = 0;
+    int is = 0, islot = 0;
+    const int64_t wrow0 = (int64_t)warp * TT_WROWS;
+    auto issue_next = [&]() {                                   // lane 0 only
+        if (ic >= ccount) return;
+        const int64_t r0 = (int64_t)is * TT_ROWS + wrow0;
+        const int64_t rows = m - r0 < TT_WROWS ? m - r0 : TT_WROWS;
+        uint64_t* bar = &full[islot][warp];
+        if (rows > 0) {
+            mbar_arrive_tx(bar, 8u * (unsigned)rows);
+            bulk_g2s(ring + ((size_t)islot * TT_WARPS + warp) * TT_WROWS, P.M + (j0 + ic) * ld + r0,
+                     8u * (unsigned)rows, bar);
+        } else {
+            mbar_arrive(bar);                                   // empty piece: complete the phase
+        }
+        if (++is == NSC) { is = 0; ++ic; }
+        if (++islot == ns) islot = 0;
+    };
+    if (lane == 0)
+        for (int e = 0; e < ns; ++e) issue_next();
+    // r' rows (512 w + 64 k + 2 lane, +1) of every segment into registers
+    double2 rr[NSC * TT_KPS];
+#pragma unroll
+    for (int k = 0; k < NSC * TT_KPS; ++k) {
+        const int64_t i = (int64_t)(k / TT_KPS) * TT_ROWS + wrow0 + (k % TT_KPS) * 64 + 2 * lane;
+        double2 r = make_double2(0.0, 0.0);
+        if (i < m) {                                            // m even: i + 1 < m
+            r = *reinterpret_cast<const double2*>(rcur + i);
+            if (iter) {
+                const double2 qq = *reinterpret_cast<const double2*>(P.q + i);
+                r.x = fma(alpha, qq.x, r.x);                    // carried residual (R13)
+                r.y = fma(alpha, qq.y, r.y);
+            }
+        }
+        rr[k] = r;
+    }
+    if (iter)
+        for (int64_t i = i0 + tid; i < i1; i += TT_THREADS) rnext[i] = fma(alpha, P.q[i], rcur[i]);
+    int slot = 0;
+    unsigned ph = 0;
+    for (int64_t jg = 0; jg < ccount; jg += BWD_NB) {
+        const int nc = (int)(ccount - jg < BWD_NB ? ccount - jg : BWD_NB);
+        double acc[BWD_NB];
+#pragma unroll
+        for (int c = 0; c < BWD_NB; ++c) {
+            acc[c] = 0.0;
+            if (c < nc) {
+#pragma unroll
+                for (int s = 0; s < NSC; ++s) {
+                    mbar_wait(&full[slot][warp], ph);
+                    const double2* src =
+                        reinterpret_cast<const double2*>(ring + ((size_t)slot * TT_WARPS + warp) * TT_WROWS) + lane;
+#pragma unroll
+                    for (int kk = 0; kk < TT_KPS; ++kk) {
+                        const int k = s * TT_KPS + kk;
+                        if ((int64_t)s * TT_ROWS + wrow0 + kk * 64 + 2 * lane < m) {
+                            const double2 a = src[kk * 32];
+                            acc[c] = fma(a.x, rr[k].x, acc[c]);
+                            acc[c] = fma(a.y, rr[k].y, acc[c]);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) {                            // refill this warp's slot
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue_next();
+                    }
+                    if (++slot == ns) { slot = 0; ph ^= 1u; }
+                }
+            }
+        }
+        // group complete: deterministic reduction of the nc column dots
+#pragma unroll
+        for (int c = 0; c < BWD_NB; ++c) {
+            const double v = warp_red<0>(acc[c]);
+            if (lane == 0) red[warp * BWD_NB + c] = v;
+        }
+        __syncthreads();
+        if (tid < nc) {
+            double v = red[tid];
+            for (int w = 1; w < TT_WARPS; ++w) v += red[w * BWD_NB + tid];
+            dots[jg + tid] = v;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    const int nvg = P.split ? 2 : 1;
+    const int nvar = (int)ccount * nvg;
+    if (mode == BWD_PLAIN) {
+        for (int t = tid; t < nvar; t += TT_THREADS) {
+            const int jj = t % (int)ccount, vv = t / (int)ccount;
+            const int64_t j = j0 + jj;
+            const double dot = dots[jj];
+            double dval = vv ? -dot : dot;
+            if (P.colscale) dval = P.colscale[j] * dot;
+            gout[j + vv * ncols] = dval;
+        }
+        return;
+    }
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    GramEnt ent;
+    const int ne = E.nb * (E.nb + 1) / 2;
+    ent.init(E.nb, ne, ne + (P.screen_full ? E.nh : 0), E.nh);
+    double gacc[3] = {0.0, 0.0, 0.0};
+    double gmax = 0.0, cnt = 0.0;
+    double* tile = ring;                                        // the ring is free now
+    double* mk = ring + (int64_t)EPI_TILE * E.nb;
+    for (int vb = 0; vb < nvar; vb += EPI_TILE) {
+        const int rows = nvar - vb < EPI_TILE ? nvar - vb : EPI_TILE;
+        if (tid < rows) {
+            const int idx = vb + tid;
+            const int jj = idx % (int)ccount, vv = idx / (int)ccount;
+            const int64_t j = j0 + jj;
+            const double dot = dots[jj];
+            double dval = vv ? -dot : dot;
+            if (P.colscale) dval = P.colscale[j] * dot;
+            epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)tid * E.nb, mk + tid, gmax, cnt);
+        }
+        if (E.gram) {
+            __syncthreads();
+            ent.accumulate(tile, mk, rows, E.nb, gacc);
+        }
+        __syncthreads();
+    }
+    if (!E.gram) return;
+    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, ring, 4096, stash, Gs);
+}
+
+static size_t bwd_t_smem(const Prob& P, int G)
+{
+    const int64_t cmax = (P.ncols + G - 1) / G;
+    return sizeof(double) * ((size_t)TT_STAGES * TT_ROWS + (size_t)cmax + 1);
 }
 
 // smem k_bwd_c needs (0 = does not fit / not applicable)
@@ -1538,6 +1723,12 @@ static bool g_no_tma = getenv("LBFGSB_TMA") == nullptr;
 // selects the shared-memory tile kernel k_qpu instead (A/B experiments)
 static bool g_no_qepi = getenv("LBFGSB_NO_QEPI") != nullptr;
 static bool g_no_qepi_t = getenv("LBFGSB_NO_QEPI_T") != nullptr;   // register-Gram kernel without TMA staging
+// k_bwd_t (register r', per-warp TMA pipelines) is opt-in (LBFGSB_BWD_T=1, ring depth
+// LBFGSB_TT_STAGES, default 3): on C2 it streams at 6.30 TB/s against k_bwd_s's 6.25 TB/s
+// as a plain GEMV^T but runs 275 vs 270 us inside the solve (tools/bwd_sweep.py,
+// profiles/r01_bwd_sweep.txt), so k_bwd_s stays the default.
+static bool g_no_bwd_t = getenv("LBFGSB_BWD_T") == nullptr;
+static int g_tt_stages = getenv("LBFGSB_TT_STAGES") ? atoi(getenv("LBFGSB_TT_STAGES")) : 3;
 static bool g_qepi_reg = getenv("LBFGSB_QEPI_REG") != nullptr;      // k_qepi_t (register Gram) instead of k_qepi_d (DMMA)
 constexpr int BWD_W_MAXM = 2048;
 constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + 64);
@@ -1553,6 +1744,14 @@ static void bwd_init()
     cudaFuncSetAttribute(k_qpu, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(double) * (NT * (MAXB + 1) > 4096 ? NT * (MAXB + 1) : 4096)));
     cudaFuncSetAttribute(k_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+    {
+        const int tsm = (int)(sizeof(double) * ((size_t)TT_STAGES * TT_ROWS + TT_CMAX));
+        cudaFuncSetAttribute(k_bwd_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+    }
     cudaFuncSetAttribute(k_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_W_SMEM_MAX);
     o = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_w, NT, BWD_W_SMEM_MAX);
@@ -1649,6 +1848,19 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         if (mpad < 4096 / 2) mpad = 4096 / 2;     // tail reduce buffer reuses r' space
         const size_t sm = sizeof(double) * ((size_t)mpad + WTILE * (MAXB + 1));
         k_bwd_w<<<G, NT, sm, st>>>(P, mode, rvec, gout, mpad);
+        return;
+    }
+    if (aligned && !g_no_bwd_t && P.m % 2 == 0 && P.m >= BWD_W_MAXM &&
+        P.m <= (int64_t)TT_NSC_MAX * TT_ROWS && (P.ncols + Gs_ - 1) / Gs_ < TT_CMAX) {
+        const size_t tsm = bwd_t_smem(P, Gs_);
+        const int ns = g_tt_stages >= 2 && g_tt_stages <= TT_STAGES ? g_tt_stages : 3;
+        switch ((int)((P.m + TT_ROWS - 1) / TT_ROWS)) {
+            case 1: k_bwd_t<1><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            case 2: k_bwd_t<2><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            case 3: k_bwd_t<3><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            case 4: k_bwd_t<4><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            default: k_bwd_t<5><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+        }
         return;
     }
     if (aligned && !g_no_tma) {

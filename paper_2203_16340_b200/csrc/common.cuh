@@ -82,6 +82,33 @@ __device__ __forceinline__ void block_sum_multi(const double* v, double* sh, dou
 
 __device__ __forceinline__ bool halted(const Ctrl* C) { return (C->done | C->stall) != 0; }
 
+// ---- P2P exchange: the fused "collective" half of a
+// producing kernel's tail.  Every thread of the calling CTA takes part:
+// this rank's pack section pk_loc[off .. off + cnt) is stored into slot
+// [rank_id] of section `sec` of EVERY rank's mailbox (peer memory over
+// NVLink, or own memory), then one system-scope release per peer bumps that
+// peer's section counter.  k_p2p_wait on the peer waits for the count.
+__device__ __forceinline__ void p2p_signal(const Prob& P, int sec)
+{
+    for (int r = 0; r < P.nranks; ++r) {
+        unsigned long long* c = reinterpret_cast<unsigned long long*>(P.peer_mb[r]) + sec;
+        atomicAdd_system(c, 1ULL);
+    }
+}
+__device__ __forceinline__ void p2p_push(const Prob& P, int sec, int64_t off, int64_t cnt)
+{
+    __syncthreads();                                    // pk_loc section written by this CTA
+    for (int r = 0; r < P.nranks; ++r) {
+        double* dst = P.peer_mb[r] + mb_off(P, sec) + (int64_t)P.rank_id * cnt;
+        for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = P.pk_loc[off + i];
+    }
+    __syncthreads();                                    // CTA's stores ordered before thread 0's fence
+    if (threadIdx.x == 0) {
+        __threadfence_system();                         // one system-scope release per CTA (cumulative)
+        p2p_signal(P, sec);
+    }
+}
+
 // Last-CTA ticket: true in every thread of the last of `total` CTAs to arrive.
 // Partials written before the call by the other CTAs are visible afterwards.
 __device__ __forceinline__ bool last_cta(unsigned* ticket, unsigned total)

@@ -28,6 +28,7 @@
 namespace lb {
 
 constexpr int MAXH = LBFGSB_MAX_HIST;
+constexpr int P2P_MAXR = 8;                        // ranks of a P2P-exchange group (one NVSwitch box)
 constexpr int MAXB = 2 * MAXH + 1;                 // Gram basis {s_i, y_i, g}
 constexpr int MAXE = MAXB * (MAXB + 1) / 2;        // upper-triangle entries
 constexpr int GRAM_STRIDE = MAXE + MAXH + 4;       // + full ||y||^2 + (gfree, nfree)
@@ -127,6 +128,15 @@ struct Prob {
     double* dir_all;        // [nranks][4]
     double* gram_all;       // [nranks][GRAM_STRIDE]
     double* kkt_all;        // [nranks][4]
+    // P2P exchange (p2p.cu): instead of an NCCL all-gather,
+    // the producing kernel's tail stores this rank's pack straight into slot
+    // [rank_id] of every peer's mailbox (NVLink / CUDA IPC mapped) and bumps
+    // the peer's section counter; k_p2p_wait spins on the local counter.
+    int p2p;
+    int rank_id;
+    double* peer_mb[P2P_MAXR];          // mailbox base of every rank (own one included)
+    unsigned long long* mb_hdr;         // own mailbox header: [4] section counters, [4] timeout flag
+    unsigned long long* p2p_tgt;        // [4] counts consumed so far (own device memory)
     // joint-probability / regularised OT objective (transport.cu):
     // x = vec(P), P tm x tn column-major; c = cost; delta (Gaussian) or ent
     // (entropy) weight; rbuf[rsel] holds the carried marginal residual
@@ -151,6 +161,17 @@ __host__ __device__ inline int64_t off_dir(const Prob& P) { return qs_len(P); }
 __host__ __device__ inline int64_t off_gram(const Prob& P) { return qs_len(P) + 4; }
 __host__ __device__ inline int64_t off_kkt(const Prob& P) { return qs_len(P) + 4 + GRAM_STRIDE; }
 __host__ __device__ inline int64_t pk_len(const Prob& P) { return qs_len(P) + 4 + GRAM_STRIDE + 4; }
+// mailbox layout (doubles): header (8 x u64), then [R][qs_len] | [R][4] | [R][GRAM_STRIDE] | [R][4],
+// i.e. the four gathered sections in pack order; section sec starts at mb_off(P, sec)
+enum XSec : int { XS_QS = 0, XS_DIR = 1, XS_GRAM = 2, XS_KKT = 3 };
+constexpr int MB_HDR = 8;
+__host__ __device__ inline int64_t mb_off(const Prob& P, int sec)
+{
+    const int64_t R = P.nranks;
+    const int64_t o[4] = {0, qs_len(P), qs_len(P) + 4, qs_len(P) + 4 + GRAM_STRIDE};
+    return MB_HDR + R * o[sec];
+}
+__host__ __device__ inline int64_t mb_len(const Prob& P) { return MB_HDR + (int64_t)P.nranks * pk_len(P); }
 
 // ---- launch modes
 enum FwdMode : int { FWD_ITER = 0, FWD_SETUP = 1, FWD_P = 2 };
@@ -180,6 +201,9 @@ void launch_kkt(const Prob& P, cudaStream_t st);
 void launch_dir_decide(const Prob& P, cudaStream_t st);
 void launch_gram_decide(const Prob& P, cudaStream_t st, int bwd_mode);
 void launch_kkt_decide(const Prob& P, cudaStream_t st);
+// p2p.cu: exchange over peer memory (the producers push from their tails)
+void launch_p2p_wait(const Prob& P, cudaStream_t st, int sec, int inc, int iter);
+void launch_p2p_put(const Prob& P, cudaStream_t st, int sec, int64_t off, int64_t cnt);
 void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K, int64_t ldk,
                   cudaStream_t st);
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
                  stash, res);
     if (P.sharded) {                                         // sharded: local pack
         if (threadIdx.x < 4) P.pk_loc[off_dir(P) + threadIdx.x] = res[threadIdx.x];
+        if (P.p2p) p2p_push(P, XS_DIR, off_dir(P), 4);
         return;
     }
     if (threadIdx.x != 0) return;
@@ -334,6 +335,24 @@ __global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec
     if (P.sharded) {                                         // sharded: local q partial
         if (r0ok) P.pk_loc[row] = q0;
         if (r1ok) P.pk_loc[row + 1] = q1;
+        if (P.p2p) {
+            // fused GEMV -> all-gather: this row block's final q rows go straight
+            // into slot [rank] of every rank's mailbox (row block 0 also carries
+            // the separable trial sums k_sep left at pk_loc + m), one signal each
+            const int64_t ql = qs_len(P);
+            for (int r = 0; r < P.nranks; ++r) {
+                double* dst = P.peer_mb[r] + mb_off(P, XS_QS) + (int64_t)P.rank_id * ql;
+                if (r0ok) dst[row] = q0;
+                if (r1ok) dst[row + 1] = q1;
+                if (blockIdx.x == 0)
+                    for (int64_t i = threadIdx.x; i < ql - m; i += blockDim.x) dst[m + i] = P.pk_loc[m + i];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence_system();
+                p2p_signal(P, XS_QS);
+            }
+        }
         return;
     }
     const int rsel = C->rsel;
@@ -593,6 +612,7 @@ __global__ void __launch_bounds__(NT) k_kkt(Prob P)
     reduce_parts(P.kkt_part, gridDim.x, 3, 3, [](int e) { return e < 2 ? 1 : 0; }, buf, 1024, stash, res);
     if (P.sharded) {
         if (threadIdx.x < 3) P.pk_loc[off_kkt(P) + threadIdx.x] = res[threadIdx.x];
+        if (P.p2p) p2p_push(P, XS_KKT, off_kkt(P), 4);
         return;
     }
     if (threadIdx.x != 0) return;

@@ -142,6 +142,16 @@ struct lbfgsb_t {
     int64_t n_global = 0;
     bool comm_owned = false;
     bool sharded = false;
+    // P2P exchange (p2p.cu): own mailbox (cudaMalloc, IPC-exportable), the mapped
+    // mailboxes of all ranks (own one at [rank]), consumed-count targets
+    bool p2p = false;
+    void* mb = nullptr;
+    int64_t mb_mmax = 0;
+    int mb_nranks = 0;
+    size_t mb_bytes = 0;
+    void* peer_mb[P2P_MAXR] = {};
+    bool peer_ipc[P2P_MAXR] = {};
+    DevBuf p2p_tgt;
 #ifdef LBFGSB_WITH_NCCL
     ncclComm_t comm = nullptr;
 #endif
@@ -298,6 +308,10 @@ extern "C" void lbfgsb_destroy(lbfgsb_t* h)
                       &h->og_d, &h->og_gn, &h->og_r, &h->og_q, &h->og_M, &h->og_part, &h->og_red,
                       &h->og_z, &h->og_out, &h->og_ticket};
     for (DevBuf* b : bufs) b->release();
+    for (int r = 0; r < P2P_MAXR; ++r)
+        if (h->peer_ipc[r] && h->peer_mb[r]) cudaIpcCloseMemHandle(h->peer_mb[r]);
+    if (h->mb) cudaFree(h->mb);
+    h->p2p_tgt.release();
     if (h->ctrl) cudaFree(h->ctrl);
     if (h->hc) cudaFreeHost(h->hc);
 #ifdef LBFGSB_WITH_NCCL
@@ -435,6 +449,25 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
             TRY(h->kkt_all.ensure(sizeof(double) * (size_t)R * 4));
             P.pk_loc = h->pk_loc.d(); P.qs_all = h->qs_all.d(); P.dir_all = h->dir_all.d();
             P.gram_all = h->gram_all.d(); P.kkt_all = h->kkt_all.d();
+            if (h->p2p) {                                     // gathered sections live in the mailbox
+                if (R != h->mb_nranks)
+                    return fail(LBFGSB_ERR_ARG, "P2P mailbox made for %d ranks, group has %d", h->mb_nranks, R);
+                if (P.m > h->mb_mmax)
+                    return fail(LBFGSB_ERR_DIM, "P2P mailbox sized for m <= %lld, objective has m = %lld",
+                                (long long)h->mb_mmax, (long long)P.m);
+                for (int r = 0; r < R; ++r)
+                    if (!h->peer_mb[r]) return fail(LBFGSB_ERR_ARG, "P2P exchange: rank %d not connected", r);
+                P.p2p = 1;
+                P.rank_id = h->rank;
+                for (int r = 0; r < R; ++r) P.peer_mb[r] = static_cast<double*>(h->peer_mb[r]);
+                double* mb = static_cast<double*>(h->mb);
+                P.mb_hdr = static_cast<unsigned long long*>(h->mb);
+                P.p2p_tgt = static_cast<unsigned long long*>(h->p2p_tgt.p);
+                P.qs_all = mb + mb_off(P, XS_QS);
+                P.dir_all = mb + mb_off(P, XS_DIR);
+                P.gram_all = mb + mb_off(P, XS_GRAM);
+                P.kkt_all = mb + mb_off(P, XS_KKT);
+            }
         }
     }
     if (ob && ob->kind == 2) {                                 // transport
@@ -487,6 +520,7 @@ static lbfgsb_err ctrl_to_host(lbfgsb_t* h, cudaStream_t st)
     return LBFGSB_OK;
 }
 
+#define FOR_RANKS_P for (size_t i_ = 0; i_ < g.Ps.size(); ++i_)
 // ------------------------------------------------------------------ groups
 // A Group is the set of handles that take part in one solve: one handle (a
 // single-GPU solve, or this rank of an NCCL-sharded solve), or nranks
@@ -515,10 +549,23 @@ static lbfgsb_err ctrl_to_host(Group& g)
     return LBFGSB_OK;
 }
 
-// All-gather one pack section across the ranks (rank order).
-static lbfgsb_err xchg(Group& g, Section sec)
+// All-gather one pack section across the ranks (rank order).  P2P handles:
+// the producing kernel already pushed its section (fused in its tail) unless
+// `put`; only the waits are launched here.  `iter`: the producer returns at
+// entry when the solve is halted, so the wait is skipped then too.  A fused
+// k_fwd push signals once per row block (`per_rb`).
+static lbfgsb_err xchg(Group& g, Section sec, bool iter = false, bool per_rb = false, bool put = false)
 {
     const Prob& P0 = g.Ps[0];
+    if (P0.p2p) {
+        const int R = (int)P0.nranks;
+        if (put) {
+            FOR_RANKS_P launch_p2p_put(g.Ps[i_], g.st, (int)sec, 0, qs_len(P0));
+        }
+        const int inc = per_rb ? R * P0.RB : R;
+        FOR_RANKS_P launch_p2p_wait(g.Ps[i_], g.st, (int)sec, inc, iter ? 1 : 0);
+        return LBFGSB_OK;
+    }
     int64_t off = 0, cnt = 0;
     switch (sec) {
         case SEC_QS: off = 0; cnt = qs_len(P0); break;
@@ -591,18 +638,18 @@ static lbfgsb_err launch_iteration(Group& g, int ev_base)
         rec_event(g, ev_base >= 0 ? ev_base + 3 : -1);
     } else {
         FOR_RANKS launch_dir(PR, st, 0);
-        TRY(xchg(g, SEC_DIR));
+        TRY(xchg(g, SEC_DIR, true));
         FOR_RANKS launch_dir_decide(PR, st);
         FOR_RANKS launch_sep(PR, st, SEP_ITER, nullptr);
         rec_event(g, ev_base >= 0 ? ev_base + 0 : -1);
         FOR_RANKS launch_fwd(PR, st, FWD_ITER, nullptr, nullptr);
         rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);
-        TRY(xchg(g, SEC_QS));
+        TRY(xchg(g, SEC_QS, true, true));
         FOR_RANKS launch_ls(PR, st, LS_SH_ITER, nullptr, nullptr, nullptr, 0);
         rec_event(g, ev_base >= 0 ? ev_base + 2 : -1);
         FOR_RANKS launch_bwd(PR, st, BWD_ITER, nullptr, nullptr);
         rec_event(g, ev_base >= 0 ? ev_base + 3 : -1);
-        TRY(xchg(g, SEC_GRAM));
+        TRY(xchg(g, SEC_GRAM, true));
         FOR_RANKS launch_gram_decide(PR, st, BWD_ITER);
     }
     g.h0()->launches += per_iteration_launches(g);
@@ -624,7 +671,7 @@ static lbfgsb_err launch_fval(Group& g, bool clip)
         launch_fwd(PR, st, FWD_SETUP, PR.x, nullptr);
     }
     if (g.sharded) {
-        TRY(xchg(g, SEC_QS));
+        TRY(xchg(g, SEC_QS, false, true));
         FOR_RANKS launch_ls(PR, st, LS_SH_SETUP, nullptr, nullptr, nullptr, 0);
     }
     return LBFGSB_OK;
@@ -670,11 +717,11 @@ static lbfgsb_err launch_ls_cont(Group& g)
         return LBFGSB_OK;
     }
     FOR_RANKS launch_sep(PR, g.st, SEP_NEXT, nullptr);
-    if (g.sharded && g.Ps[0].GS > 0) TRY(xchg(g, SEC_QS));
+    if (g.sharded && g.Ps[0].GS > 0) TRY(xchg(g, SEC_QS, false, false, true));
     FOR_RANKS launch_ls(PR, g.st, LS_NEXT, nullptr, nullptr, nullptr, 0);
     FOR_RANKS launch_bwd(PR, g.st, BWD_ITER, nullptr, nullptr);
     if (g.sharded) {
-        TRY(xchg(g, SEC_GRAM));
+        TRY(xchg(g, SEC_GRAM, true));
         FOR_RANKS launch_gram_decide(PR, g.st, BWD_ITER);
     }
     g.h0()->launches += 3;
@@ -810,6 +857,16 @@ static lbfgsb_err solve_group(Group& g, double* const* xs, double tol, lbfgsb_re
     TRY(launch_refresh(g));
     CK(cudaGetLastError());
     TRY(ctrl_to_host(g));
+    if (g.Ps[0].p2p) {
+        unsigned long long to = 0;
+        FOR_RANKS {
+            unsigned long long v = 0;
+            CK(cudaMemcpyAsync(&v, PR.mb_hdr + 4, sizeof v, cudaMemcpyDeviceToHost, g.st));
+            CK(cudaStreamSynchronize(g.st));
+            to |= v;
+        }
+        if (to) return fail(LBFGSB_ERR_NCCL, "P2P exchange timed out (a peer stopped signalling)");
+    }
     FOR_RANKS {
         if (xs[i_] != PR.x)
             CK(cudaMemcpyAsync(xs[i_], PR.x, sizeof(double) * g.hs[i_]->n, cudaMemcpyDeviceToDevice, g.st));
@@ -1486,6 +1543,99 @@ extern "C" lbfgsb_err lbfgsb_create_sharded(int64_t n_local, int64_t n_global, i
     (void)n_local; (void)m_hist; (void)lower_local; (void)upper_local; (void)opts; (void)cuda_stream;
     return fail(LBFGSB_ERR_UNSUPPORTED, "built without NCCL");
 #endif
+}
+
+// ------------------------------------------------------------------ sharded (P2P exchange)
+// Mailbox of one rank: header + the four gathered sections for m <= m_max
+// (layout in impl.cuh mb_off).  cudaMalloc (not the
+// stream-ordered allocator) so that it can be exported with CUDA IPC.
+static lbfgsb_err alloc_mailbox(lbfgsb_t* h, int nranks, int64_t m_max)
+{
+    if (nranks < 1 || nranks > P2P_MAXR) return fail(LBFGSB_ERR_ARG, "P2P exchange: 1 <= nranks <= %d", P2P_MAXR);
+    if (m_max < 1) return fail(LBFGSB_ERR_DIM, "m_max < 1");
+    const size_t per = (size_t)(m_max + (int64_t)KT * NSEP + 4 + GRAM_STRIDE + 4);
+    const size_t bytes = sizeof(double) * (MB_HDR + (size_t)nranks * per);
+    if (h->mb) { cudaFree(h->mb); h->mb = nullptr; }
+    cudaError_t e = cudaMalloc(&h->mb, bytes);
+    if (e == cudaSuccess) e = cudaMemset(h->mb, 0, bytes);
+    if (e != cudaSuccess) {
+        if (h->mb) cudaFree(h->mb);
+        h->mb = nullptr;
+        return fail(LBFGSB_ERR_OOM, "mailbox cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    }
+    TRY(h->p2p_tgt.ensure(sizeof(unsigned long long) * 4, true));
+    CK(cudaMemset(h->p2p_tgt.p, 0, sizeof(unsigned long long) * 4));
+    h->mb_mmax = m_max;
+    h->mb_nranks = nranks;
+    h->mb_bytes = bytes;
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_create_sharded_p2p(int64_t n_local, int64_t n_global, int32_t m_hist,
+                                                const double* lower_local, const double* upper_local,
+                                                const lbfgsb_opts* opts, void* cuda_stream, int32_t rank,
+                                                int32_t nranks, int64_t m_max, lbfgsb_t** out)
+{
+    if (!out) return fail(LBFGSB_ERR_ARG, "NULL out");
+    *out = nullptr;
+    if (nranks < 1 || nranks > P2P_MAXR || rank < 0 || rank >= nranks)
+        return fail(LBFGSB_ERR_ARG, "bad rank/nranks (P2P exchange: nranks <= %d)", P2P_MAXR);
+    if (n_global < n_local) return fail(LBFGSB_ERR_DIM, "n_global < n_local");
+    lbfgsb_t* h = nullptr;
+    TRY(create_common(n_local, m_hist, lower_local, upper_local, opts, cuda_stream, &h));
+    lbfgsb_err e = alloc_mailbox(h, nranks, m_max);
+    if (e != LBFGSB_OK) { lbfgsb_destroy(h); return e; }
+    h->p2p = true;
+    h->sharded = true;
+    h->nranks = nranks;
+    h->rank = rank;
+    h->n_global = n_global;
+    h->peer_mb[rank] = h->mb;
+    *out = h;
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_p2p_ipc_handle(lbfgsb_t* h, void* out)
+{
+    if (!h || !out || !h->p2p || !h->mb) return fail(LBFGSB_ERR_ARG, "not a P2P handle");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
+    cudaIpcMemHandle_t ih;
+    CK(cudaIpcGetMemHandle(&ih, h->mb));
+    std::memcpy(out, &ih, sizeof ih);
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_p2p_open(lbfgsb_t* h, const void* handles)
+{
+    if (!h || !handles || !h->p2p) return fail(LBFGSB_ERR_ARG, "not a P2P handle");
+    for (int r = 0; r < h->nranks; ++r) {
+        if (r == h->rank) { h->peer_mb[r] = h->mb; continue; }
+        if (h->peer_ipc[r] && h->peer_mb[r]) { cudaIpcCloseMemHandle(h->peer_mb[r]); h->peer_ipc[r] = false; }
+        cudaIpcMemHandle_t ih;
+        std::memcpy(&ih, static_cast<const char*>(handles) + 64 * (size_t)r, sizeof ih);
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", r,
+                                          cudaGetErrorString(e));
+        h->peer_mb[r] = p;
+        h->peer_ipc[r] = true;
+    }
+    return LBFGSB_OK;
+}
+
+extern "C" lbfgsb_err lbfgsb_p2p_connect_local(lbfgsb_t* const* hs, int32_t nranks, int64_t m_max)
+{
+    if (!hs || nranks < 1 || nranks > P2P_MAXR) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    for (int p = 0; p < nranks; ++p) {
+        if (!hs[p] || hs[p]->comm_owned || (hs[p]->p2p && hs[p]->peer_ipc[0]))
+            return fail(LBFGSB_ERR_ARG, "rank %d: not a plain single-GPU handle", p);
+        TRY(alloc_mailbox(hs[p], nranks, m_max));
+    }
+    for (int p = 0; p < nranks; ++p) {
+        hs[p]->p2p = true;
+        for (int r = 0; r < nranks; ++r) { hs[p]->peer_mb[r] = hs[r]->mb; hs[p]->peer_ipc[r] = false; }
+    }
+    return LBFGSB_OK;
 }
 
 // ------------------------------------------------------------------ ops

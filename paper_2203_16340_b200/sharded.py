@@ -7,9 +7,11 @@ matching variables, bounds and ring slice); per iteration the ranks
 all-gather the m-length partial of q = M~p and small packs (Alg. 2 sums,
 separable Armijo sums, the Gram of Alg. 3) and reduce them in rank order, so
 every rank takes bit-identical decisions.  torch.distributed is only the
-bootstrap (broadcast of the 128-byte ncclUniqueId) and the bench's barrier /
+bootstrap (broadcast of the 128-byte ncclUniqueId, or the all-gather of the
+64-byte CUDA IPC handles of the P2P mailboxes) and the bench's barrier /
 max-over-ranks timing; the per-iteration exchange is the library's own NCCL
-communicator.
+communicator (xchg="nccl") or its own kernels' stores into the peers'
+mailboxes over NVLink (xchg="p2p", lbfgsb_create_sharded_p2p).
 """
 from __future__ import annotations
 
@@ -43,11 +45,32 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
-def make_sharded_solver(n_local, n_global, m_hist, lower, opts, stream):
-    """lbfgsb_create_sharded on the current rank (rank 0 makes the NCCL id)."""
+def all_gather_bytes(payload: bytes) -> list[bytes]:
+    """All-gather one small byte string per rank (rank order) over the default group."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, payload)
+    return out
+
+
+def make_sharded_solver(n_local, n_global, m_hist, lower, opts, stream, xchg="nccl", m_max=None):
+    """Sharded handle on the current rank.  xchg="nccl": lbfgsb_create_sharded
+    (rank 0 makes the NCCL id).  xchg="p2p": lbfgsb_create_sharded_p2p with a
+    mailbox for residuals of length <= m_max, IPC handles all-gathered and
+    opened, then a barrier so that no rank signals an unmapped peer."""
     import torch.distributed as dist
     import paper_2203_16340_b200 as lb
     rank, world = dist.get_rank(), dist.get_world_size()
+    if xchg == "p2p":
+        if m_max is None:
+            raise ValueError("xchg='p2p' needs m_max")
+        s = lb.Solver(n_local, m_hist, lower=lower, opts=opts, stream=stream, rank=rank, nranks=world,
+                      n_global=n_global, p2p_m_max=int(m_max))
+        s.p2p_open(all_gather_bytes(s.ipc_handle()))
+        dist.barrier()
+        return s
+    if xchg != "nccl":
+        raise ValueError(f"unknown exchange {xchg!r}")
     nid = lb.nccl_unique_id() if rank == 0 else None
     nid = broadcast_bytes(nid, src=0)
     return lb.Solver(n_local, m_hist, lower=lower, opts=opts, stream=stream, nccl_id=nid,

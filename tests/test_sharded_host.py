@@ -46,6 +46,8 @@ def _worker(rank, world, port, out):
     got = sharded.broadcast_bytes(nid, src=0)
     # 2) max-over-ranks timing
     mx = sharded.max_over_ranks(1.5 + rank)
+    # 2b) the IPC-handle all-gather of the P2P exchange (64 bytes per rank, rank order)
+    hs = sharded.all_gather_bytes(bytes([rank]) * 64)
     # 3) the sharded decomposition on a small NNLS instance
     m, n = 60, 37
     rng = np.random.default_rng(0)
@@ -71,7 +73,7 @@ def _worker(rank, world, port, out):
         sums = sums + t.numpy()
     q_ref = oracle.matvec(A, d)
     pp_ref = np.maximum(x + d, 0.0) - x
-    res = dict(got=got, mx=mx, q_err=float(np.max(np.abs(q - q_ref) / (np.abs(A) @ np.abs(d) + 1e-300))),
+    res = dict(got=got, mx=mx, hs=hs, q_err=float(np.max(np.abs(q - q_ref) / (np.abs(A) @ np.abs(d) + 1e-300))),
                s_err=float(abs(sums[0] - pp_ref @ g) + abs(sums[1] - pp_ref @ pp_ref)),
                q_bits=q.tobytes())
     out[rank] = res
@@ -87,7 +89,24 @@ def test_gloo_world2_sharded_host_logic():
     for r in range(world):
         assert out[r]["got"] == bytes(range(128))
         assert out[r]["mx"] == 2.5
+        assert out[r]["hs"] == [bytes([k]) * 64 for k in range(world)]
         assert out[r]["q_err"] <= 1e-12
         assert out[r]["s_err"] <= 1e-12
     # every rank reduced the same gathered partials in the same order: identical bits
     assert out[0]["q_bits"] == out[1]["q_bits"]
+
+
+def test_make_sharded_solver_argument_checks():
+    from paper_2203_16340_b200 import sharded
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("default group already initialised")
+    port = _free_port()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        with pytest.raises(ValueError):
+            sharded.make_sharded_solver(10, 10, 5, None, None, None, xchg="p2p")          # no m_max
+        with pytest.raises(ValueError):
+            sharded.make_sharded_solver(10, 10, 5, None, None, None, xchg="mpi")
+    finally:
+        dist.destroy_process_group()
