@@ -1726,7 +1726,7 @@ static bool g_no_qepi_t = getenv("LBFGSB_NO_QEPI_T") != nullptr;   // register-G
 // k_bwd_t (register r', per-warp TMA pipelines) is opt-in (LBFGSB_BWD_T=1, ring depth
 // LBFGSB_TT_STAGES, default 3): on C2 it streams at 6.30 TB/s against k_bwd_s's 6.25 TB/s
 // as a plain GEMV^T but runs 275 vs 270 us inside the solve (tools/bwd_sweep.py,
-// profiles/r01_bwd_sweep.txt), so k_bwd_s stays the default.
+// profiles/r01_gemv_experiments.txt), so k_bwd_s stays the default.
 static bool g_no_bwd_t = getenv("LBFGSB_BWD_T") == nullptr;
 static int g_tt_stages = getenv("LBFGSB_TT_STAGES") ? atoi(getenv("LBFGSB_TT_STAGES")) : 3;
 static bool g_qepi_reg = getenv("LBFGSB_QEPI_REG") != nullptr;      // k_qepi_t (register Gram) instead of k_qepi_d (DMMA)
