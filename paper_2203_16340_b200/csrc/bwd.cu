@@ -390,11 +390,17 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
 // ---------------------------------------------------------------- k_bwd_w (short columns)
 // m < 2048 rows (C1, C4): a whole column is only a few KB, so a CTA-wide
 // reduction per column group would dominate.  Each WARP owns WCOL columns
-// at a time (lanes stride the rows, r' from shared memory), reduces with
-// shuffles only, and its lanes run the epilogue; the CTA syncs once per
-// round of 8 warp-groups to accumulate the Gram tile.
+// at a time (lanes stride the rows with WRS row steps = 4 x WCOL 16-byte loads
+// in flight per lane, r' from shared memory), reduces with shuffles only, and
+// its lanes run the epilogue into the warp's own tile rows.  The masked Gram
+// of the next basis is accumulated PER WARP (lane l owns entries l, l+32, ..;
+// warp-private smem partials, __syncwarp only), so no CTA barrier interrupts
+// the column stream; the CTA sums its warps' partials in warp order once.
 constexpr int WCOL = 4;
-constexpr int WTILE = (NT / 32) * WCOL * 2;     // tile rows per round (split: 2 vars per column)
+constexpr int WRS = 4;                          // row steps of 64 rows per trip
+constexpr int WROWS = WCOL * 2;                 // tile rows per warp (split: 2 vars per column)
+constexpr int WTILE = (NT / 32) * WROWS;        // tile rows per CTA
+constexpr int WG_STRIDE = MAXE + MAXH + 1;      // per-warp Gram partial slots (max; launch passes the m_hist size)
 
 template <int NC>
 __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int64_t ld, int64_t m,
@@ -402,21 +408,21 @@ __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int
 {
     const int lane = threadIdx.x & 31;
     int64_t i = 2 * lane;
-    for (; i + 64 + 1 < m; i += 128) {
-        double2 a0[NC], a1[NC];
+    for (; i + 64 * (WRS - 1) + 1 < m; i += 64 * WRS) {
+        double2 av[WRS][NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            a0[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i));
-            a1[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + 64));
-        }
-        const double2 r0 = *reinterpret_cast<const double2*>(rs + i);
-        const double2 r1 = *reinterpret_cast<const double2*>(rs + i + 64);
+        for (int u = 0; u < WRS; ++u)
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            acc[c] = fma(a0[c].x, r0.x, acc[c]);
-            acc[c] = fma(a0[c].y, r0.y, acc[c]);
-            acc[c] = fma(a1[c].x, r1.x, acc[c]);
-            acc[c] = fma(a1[c].y, r1.y, acc[c]);
+            for (int c = 0; c < NC; ++c)
+                av[u][c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + 64 * u));
+#pragma unroll
+        for (int u = 0; u < WRS; ++u) {
+            const double2 r = *reinterpret_cast<const double2*>(rs + i + 64 * u);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                acc[c] = fma(av[u][c].x, r.x, acc[c]);
+                acc[c] = fma(av[u][c].y, r.y, acc[c]);
+            }
         }
     }
     for (; i < m; i += 64) {
@@ -434,7 +440,8 @@ __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double* rvec, double* gout, int mpad)
+__global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double* rvec, double* gout, int mpad,
+                                                int wgs)
 {
     Ctrl* C = P.ctrl;
     if (mode == BWD_ITER && halted(C)) return;
@@ -442,9 +449,11 @@ __global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double*
     double* rs = smw;                               // r' [mpad]
     double* tile = smw + mpad;                      // [WTILE][MAXB]
     double* mk = tile + WTILE * MAXB;               // [WTILE]
+    double* wg = mk + WTILE;                        // [NT/32][wgs] per-warp Gram partials
     __shared__ double red[NT / 32 * BWD_NB];
     __shared__ double stash[NT];
     __shared__ double Gs[MAXE + MAXH + 2];
+    __shared__ unsigned char ea[MAXE + MAXH], eb[MAXE + MAXH];   // entry -> basis pair (eb = 255: full norm)
     const int G = gridDim.x, cta = blockIdx.x;
     const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
     const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
@@ -462,41 +471,50 @@ __global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double*
         }
         rs[i] = r;
     }
-    __syncthreads();
     const bool epi = mode != BWD_PLAIN;
     EpiCtx E;
     if (epi) epi_init(P, C, mode, E);
+    const bool gram = epi && E.gram;
     const int nb = epi ? E.nb : 1;
     const int ne = nb * (nb + 1) / 2;
-    GramEnt ent;
-    ent.init(nb, ne, ne + (epi && P.screen_full ? E.nh : 0), epi ? E.nh : 0);
-    double gacc[3] = {0.0, 0.0, 0.0};
+    const int ntot = gram ? ne + (P.screen_full ? E.nh : 0) : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = NT / 32;
+    double* wgw = wg + (int64_t)w * wgs;
+    if (gram) {
+        for (int e = threadIdx.x; e < ntot; e += NT) {          // upper triangle, row-major; then ||y_i||^2
+            if (e < ne) {
+                int aa = 0, rem = e;
+                while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
+                ea[e] = (unsigned char)aa; eb[e] = (unsigned char)(aa + rem);
+            } else {
+                ea[e] = (unsigned char)(E.nh + (e - ne)); eb[e] = 255;
+            }
+        }
+        for (int e = lane; e < ntot; e += 32) wgw[e] = 0.0;
+    }
+    __syncthreads();
     double gmax = 0.0, cnt = 0.0;
     const int nvg = P.split ? 2 : 1;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = NT / 32;
     const int64_t ncl = j1 - j0;
     const int64_t ngroups = (ncl + WCOL - 1) / WCOL;
-    const int64_t rounds = (ngroups + nw - 1) / nw;
     const int rows_per_warp = WCOL * nvg;
-    for (int64_t rd = 0; rd < rounds; ++rd) {
-        const int64_t grp = rd * nw + w;
+    const int trow0 = w * WROWS;
+    for (int64_t grp = w; grp < ngroups; grp += nw) {
         const int64_t jg = j0 + grp * WCOL;
-        const int nc = jg < j1 ? (int)(j1 - jg < WCOL ? j1 - jg : WCOL) : 0;
+        const int nc = (int)(j1 - jg < WCOL ? j1 - jg : WCOL);
         double acc[WCOL] = {0.0, 0.0, 0.0, 0.0};
         const double* M0 = P.M + jg * ld;
         switch (nc) {
             case 4: warp_col_dots<4>(M0, ld, m, rs, acc); break;
             case 3: warp_col_dots<3>(M0, ld, m, rs, acc); break;
             case 2: warp_col_dots<2>(M0, ld, m, rs, acc); break;
-            case 1: warp_col_dots<1>(M0, ld, m, rs, acc); break;
-            default: break;
+            default: warp_col_dots<1>(M0, ld, m, rs, acc); break;
         }
 #pragma unroll
         for (int c = 0; c < WCOL; ++c)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
         // all lanes now hold the column dots (xor butterfly: identical in every lane)
-        const int trow0 = w * rows_per_warp;
         if (lane < rows_per_warp) {
             const int t = trow0 + lane;
             if (lane < nc * nvg) {
@@ -510,19 +528,38 @@ __global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double*
                 if (P.colscale) dval = P.colscale[j] * dot;
                 if (!epi) gout[j + vv * ncols] = dval;
                 else epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)t * nb, mk + t, gmax, cnt);
-            } else if (epi) {
+            } else if (gram) {
                 for (int b = 0; b < nb; ++b) tile[(int64_t)t * nb + b] = 0.0;
                 mk[t] = 0.0;
             }
         }
-        if (epi && E.gram) {
-            __syncthreads();
-            ent.accumulate(tile, mk, nw * rows_per_warp, nb, gacc);
-            __syncthreads();
+        if (gram) {
+            __syncwarp();
+            const double* tw = tile + (int64_t)trow0 * nb;
+            const double* mw = mk + trow0;
+            for (int e = lane; e < ntot; e += 32) {
+                const int aa = ea[e], bb = eb[e];
+                double s = 0.0;
+                if (bb != 255) {
+                    for (int r = 0; r < rows_per_warp; ++r)
+                        if (mw[r] != 0.0) s = fma(tw[r * nb + aa], tw[r * nb + bb], s);
+                } else {
+                    for (int r = 0; r < rows_per_warp; ++r) s = fma(tw[r * nb + aa], tw[r * nb + aa], s);
+                }
+                wgw[e] += s;
+            }
+            __syncwarp();                                       // tile rows are rewritten next group
         }
     }
-    if (!epi || !E.gram) return;
-    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
+    if (!gram) return;
+    __syncthreads();
+    double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
+    for (int e = threadIdx.x; e < ntot; e += NT) {              // warp partials in warp order
+        double s = wg[e];
+        for (int k = 1; k < nw; ++k) s += wg[(int64_t)k * wgs + e];
+        out[e] = s;
+    }
+    gram_tail_after(P, C, E, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
 }
 
 // ---------------------------------------------------------------- k_bwd_c (TMA, CTA pairs)
@@ -1731,7 +1768,7 @@ static bool g_no_bwd_t = getenv("LBFGSB_BWD_T") == nullptr;
 static int g_tt_stages = getenv("LBFGSB_TT_STAGES") ? atoi(getenv("LBFGSB_TT_STAGES")) : 3;
 static bool g_qepi_reg = getenv("LBFGSB_QEPI_REG") != nullptr;      // k_qepi_t (register Gram) instead of k_qepi_d (DMMA)
 constexpr int BWD_W_MAXM = 2048;
-constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + 64);
+constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + (NT / 32) * WG_STRIDE + 64);
 static bool g_bwd_init = false;
 
 static void bwd_init()
@@ -1843,11 +1880,21 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
     const int Gs_ = (int)(P.ncols < sms ? P.ncols : sms);
     const size_t smem = aligned ? bwd_s_smem(P, Gs_) : 0;
     if (aligned && P.m < BWD_W_MAXM) {
-        const int G = (int)(P.ncols < (int64_t)sms * g_bwdw_occ ? P.ncols : (int64_t)sms * g_bwdw_occ);
         int mpad = (int)(P.m + (P.m & 1));
         if (mpad < 4096 / 2) mpad = 4096 / 2;     // tail reduce buffer reuses r' space
-        const size_t sm = sizeof(double) * ((size_t)mpad + WTILE * (MAXB + 1));
-        k_bwd_w<<<G, NT, sm, st>>>(P, mode, rvec, gout, mpad);
+        const int nbm = 2 * P.mh + 1;
+        const int wgs = nbm * (nbm + 1) / 2 + P.mh + 1;            // Gram entries + full norms for m_hist
+        const size_t sm = sizeof(double) * ((size_t)mpad + WTILE * (MAXB + 1) + (NT / 32) * (size_t)wgs);
+        static size_t occ_sm = 0;
+        static int occ_w = 1;
+        if (sm != occ_sm) {
+            int o = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_w, NT, sm);
+            occ_w = o > 0 ? o : 1;
+            occ_sm = sm;
+        }
+        const int Gw = (int)(P.ncols < (int64_t)sms * occ_w ? P.ncols : (int64_t)sms * occ_w);
+        k_bwd_w<<<Gw, NT, sm, st>>>(P, mode, rvec, gout, mpad, wgs);
         return;
     }
     if (aligned && !g_no_bwd_t && P.m % 2 == 0 && P.m >= BWD_W_MAXM &&
