@@ -622,8 +622,7 @@ static lbfgsb_err launch_iteration(Group& g, int ev_base)
         rec_event(g, ev_base >= 0 ? ev_base + 0 : -1);
         launch_tsum(P, st, TS_ITER);
         if (P.ent != 0.0) launch_tsum(P, st, TS_CONT);          // no-op unless trial 0 failed
-        rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);
-        rec_event(g, ev_base >= 0 ? ev_base + 2 : -1);
+        rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);     // also the start of k_bwd (no +2 node)
         launch_bwd(P, st, BWD_ITER, nullptr, nullptr);
         rec_event(g, ev_base >= 0 ? ev_base + 3 : -1);
     } else if (!g.sharded) {
@@ -632,8 +631,7 @@ static lbfgsb_err launch_iteration(Group& g, int ev_base)
         launch_sep(P, st, SEP_ITER, nullptr);
         rec_event(g, ev_base >= 0 ? ev_base + 0 : -1);
         launch_fwd(P, st, FWD_ITER, nullptr, nullptr);
-        rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);
-        rec_event(g, ev_base >= 0 ? ev_base + 2 : -1);
+        rec_event(g, ev_base >= 0 ? ev_base + 1 : -1);     // also the start of k_bwd (no +2 node)
         launch_bwd(P, st, BWD_ITER, nullptr, nullptr);
         rec_event(g, ev_base >= 0 ? ev_base + 3 : -1);
     } else {
@@ -782,7 +780,9 @@ static void collect_profile(lbfgsb_t* h, int64_t iters_done)
         if (cudaEventElapsedTime(&a, h->ev[4 * i + 0], h->ev[4 * i + 1]) == cudaSuccess) {
             h->prof_ms[0] += a; h->prof_n[0] += 1;
         }
-        if (cudaEventElapsedTime(&b, h->ev[4 * i + 2], h->ev[4 * i + 3]) == cudaSuccess) {
+        // single GPU: k_bwd follows k_fwd directly, so its start event is the fwd-end one
+        const int bs = h->sharded ? 2 : 1;
+        if (cudaEventElapsedTime(&b, h->ev[4 * i + bs], h->ev[4 * i + 3]) == cudaSuccess) {
             h->prof_ms[1] += b; h->prof_n[1] += 1;
         }
     }
