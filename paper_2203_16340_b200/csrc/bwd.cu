@@ -272,6 +272,10 @@ __global__ void __launch_bounds__(NT) k_gram_decide(Prob P, int mode)
     Ctrl* C = P.ctrl;
     if (mode == BWD_ITER && halted(C)) return;
     __shared__ double Gs[MAXE + MAXH + 2];
+    if (P.p2p) {                                             // P2P exchange: the Gram packs of all ranks
+        if (threadIdx.x == 0) p2p_wait_take(P, XS_GRAM, (unsigned long long)P.nranks);
+        __syncthreads();
+    }
     const int nh = C->nh, nb = 2 * nh + 1, ne = nb * (nb + 1) / 2;
     const int ntot = ne + (P.screen_full ? nh : 0), nent = ntot + 2;
     for (int e = threadIdx.x; e < nent; e += blockDim.x) {

@@ -95,6 +95,36 @@ __device__ __forceinline__ void p2p_signal(const Prob& P, int sec)
         atomicAdd_system(c, 1ULL);
     }
 }
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Consumer side (one thread): spin until section `sec` of the own mailbox has
+// received `tgt` signals in total.  A peer that never signals trips the
+// timeout flag in the header after 60 s instead of hanging the GPU.
+__device__ __forceinline__ void p2p_wait_for(const Prob& P, int sec, unsigned long long tgt)
+{
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(P.mb_hdr + sec) < tgt) {
+        __nanosleep(100);
+        if (globaltimer_ns() - t0 > 60000000000ULL) { atomicExch(P.mb_hdr + 4, 1ULL); break; }
+    }
+}
+// ... and account for them (single-CTA consumers: the *_decide kernels)
+__device__ __forceinline__ void p2p_wait_take(const Prob& P, int sec, unsigned long long inc)
+{
+    const unsigned long long tgt = P.p2p_tgt[sec] + inc;
+    p2p_wait_for(P, sec, tgt);
+    P.p2p_tgt[sec] = tgt;
+}
 __device__ __forceinline__ void p2p_push(const Prob& P, int sec, int64_t off, int64_t cnt)
 {
     __syncthreads();                                    // pk_loc section written by this CTA

@@ -202,7 +202,6 @@ void launch_dir_decide(const Prob& P, cudaStream_t st);
 void launch_gram_decide(const Prob& P, cudaStream_t st, int bwd_mode);
 void launch_kkt_decide(const Prob& P, cudaStream_t st);
 // p2p.cu: exchange over peer memory (the producers push from their tails)
-void launch_p2p_wait(const Prob& P, cudaStream_t st, int sec, int inc, int iter);
 void launch_p2p_put(const Prob& P, cudaStream_t st, int sec, int64_t off, int64_t cnt);
 void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K, int64_t ldk,
                   cudaStream_t st);

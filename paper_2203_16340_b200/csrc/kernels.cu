@@ -105,6 +105,7 @@ __global__ void k_dir_decide(Prob P)
 {
     Ctrl* C = P.ctrl;
     if (halted(C) || threadIdx.x != 0) return;
+    if (P.p2p) p2p_wait_take(P, XS_DIR, (unsigned long long)P.nranks);
     double res[4] = {0.0, 0.0, 0.0, INFINITY};
     for (int p = 0; p < P.nranks; ++p) {
         const double* o = P.dir_all + (int64_t)p * 4;
@@ -446,8 +447,20 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
                                            double* f_out, int ntr_op)
 {
     Ctrl* C = P.ctrl;
-    if (mode != LS_OP && halted(C)) return;
+    // LS_SH_SETUP (the sharded f(x) / residual refresh) runs even when the
+    // solve is done: the final refresh of reading R13 happens after `done`
+    if ((mode == LS_NEXT || mode == LS_SH_ITER) && halted(C)) return;
     __shared__ double buf[1024];
+    // P2P exchange: wait for the q section (pushed by every row block of every
+    // rank's k_fwd; by one k_p2p_put per rank on the Armijo continuation path)
+    const bool p2p_wait = P.p2p && (mode == LS_SH_ITER || mode == LS_SH_SETUP || (mode == LS_NEXT && P.GS > 0));
+    const unsigned long long p2p_tgt =
+        p2p_wait ? P.p2p_tgt[XS_QS] + (unsigned long long)P.nranks * (mode == LS_NEXT ? 1ULL : (unsigned long long)P.RB)
+                 : 0ULL;
+    if (p2p_wait) {
+        if (threadIdx.x == 0) p2p_wait_for(P, XS_QS, p2p_tgt);
+        __syncthreads();
+    }
     __shared__ double stash[NT];
     __shared__ double Ssum[KT];
     __shared__ double sepv[KT * NSEP];
@@ -493,6 +506,7 @@ __global__ void __launch_bounds__(NT) k_ls(Prob P, int mode, const double* rv, c
     block_sum_multi<KT>(acc, msh, Ssum);
     if ((int)threadIdx.x < ntr) P.lsp[(int64_t)blockIdx.x * KT + threadIdx.x] = Ssum[threadIdx.x];
     if (!last_cta(P.tickets + T_LS, gridDim.x)) return;
+    if (p2p_wait && threadIdx.x == 0) P.p2p_tgt[XS_QS] = p2p_tgt;   // every CTA has passed its wait
     reduce_parts(P.lsp, gridDim.x, KT, ntr, [](int) { return 0; }, buf, 1024, stash, Ssum);
     reduce_sep(P, ntr, buf, 1024, stash, sepv);
     if (threadIdx.x != 0) return;
@@ -624,6 +638,7 @@ __global__ void __launch_bounds__(NT) k_kkt(Prob P)
 __global__ void k_kkt_decide(Prob P)
 {
     if (threadIdx.x != 0) return;
+    if (P.p2p) p2p_wait_take(P, XS_KKT, (unsigned long long)P.nranks);
     double pg = 0.0, gm = 0.0, cnt = 0.0;
     for (int p = 0; p < P.nranks; ++p) {
         const double* o = P.kkt_all + (int64_t)p * 4;

@@ -562,8 +562,8 @@ static lbfgsb_err xchg(Group& g, Section sec, bool iter = false, bool per_rb = f
         if (put) {
             FOR_RANKS_P launch_p2p_put(g.Ps[i_], g.st, (int)sec, 0, qs_len(P0));
         }
-        const int inc = per_rb ? R * P0.RB : R;
-        FOR_RANKS_P launch_p2p_wait(g.Ps[i_], g.st, (int)sec, inc, iter ? 1 : 0);
+        // the consuming kernel waits in its prologue (k_dir_decide, k_ls, k_gram_decide, k_kkt_decide)
+        (void)R; (void)iter; (void)per_rb;
         return LBFGSB_OK;
     }
     int64_t off = 0, cnt = 0;
