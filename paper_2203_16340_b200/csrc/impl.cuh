@@ -187,7 +187,7 @@ constexpr int TNS = 3 + TT;                // k_tsum per-CTA sums
 void init_kernels();
 int sm_count();
 int bwd_ctas_per_sm();
-int fwd_ctas_per_sm();
+int fwd_ctas_per_sm(int64_t m);
 void launch_clip(const Prob& P, cudaStream_t st);
 void launch_dir(const Prob& P, cudaStream_t st, int op_mode);
 void launch_sep(const Prob& P, cudaStream_t st, int mode, const double* pvec);

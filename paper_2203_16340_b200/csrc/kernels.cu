@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace lb {
@@ -214,8 +215,8 @@ __device__ void reduce_sep(const Prob& P, int ntr, double* buf, int bufn, double
 // : p_j) * colscale_j.  p[S-bar] = 0 in both Alg. 2 branches, so fixed
 // variables cost no HBM traffic.  Row-block tail: q_i = sum_chunk (chunk
 // order), Armijo trial sums over the block's rows.  Global tail: decision.
-template <bool VEC>
-__global__ void __launch_bounds__(NT) k_fwd(Prob P, int mode, const double* pvec, double* qout)
+template <bool VEC, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double* pvec, double* qout)
 {
     Ctrl* C = P.ctrl;
     if (mode == FWD_ITER && halted(C)) return;
@@ -724,8 +725,18 @@ void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K
 }
 
 // ------------------------------------------------------------------ launchers
-static int g_sms = 0, g_fwd_occ = 0;
+static int g_sms = 0, g_fwd_occ[2] = {0, 0};
 static const size_t kGramSmem = sizeof(double) * (size_t)TILE * (MAXB + 1);
+// k_fwd register cap by shape (tools/_ab_cmd.sh, profiles/r01_gemv_experiments.txt): long columns
+// (m >= 2048, C2) stream best at 3 CTAs/SM (MINB = 3, 80 registers), short columns (C4) at 2 CTAs/SM
+// (MINB = 1, 88 registers: fewer column chunks, fewer split-K partials).  LBFGSB_FWD_MINB=1|3|4
+// forces one variant for A/B runs.
+static const int g_fwd_minb_env = getenv("LBFGSB_FWD_MINB") ? atoi(getenv("LBFGSB_FWD_MINB")) : 0;
+static int fwd_minb(int64_t m)
+{
+    if (g_fwd_minb_env == 1 || g_fwd_minb_env == 3 || g_fwd_minb_env == 4) return g_fwd_minb_env;
+    return m >= 2048 ? 3 : 1;
+}
 
 int sm_count()
 {
@@ -745,12 +756,16 @@ void init_kernels()
     cudaFuncSetAttribute(k_gram_recur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem);
     sm_count();
     int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fwd<true>, NT, 0);
-    g_fwd_occ = o > 0 ? o : 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fwd<true, 1>, NT, 0);
+    g_fwd_occ[0] = o > 0 ? o : 1;
+    o = 0;
+    if (g_fwd_minb_env == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fwd<true, 4>, NT, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fwd<true, 3>, NT, 0);
+    g_fwd_occ[1] = o > 0 ? o : 1;
     cudaGetLastError();
     done = true;
 }
-int fwd_ctas_per_sm() { init_kernels(); return g_fwd_occ; }
+int fwd_ctas_per_sm(int64_t m) { init_kernels(); return g_fwd_occ[fwd_minb(m) == 1 ? 0 : 1]; }
 
 static int grid_for(int64_t n, int per)
 {
@@ -775,8 +790,15 @@ void launch_sep(const Prob& P, cudaStream_t st, int mode, const double* pvec)
 void launch_fwd(const Prob& P, cudaStream_t st, int mode, const double* pvec, double* qout)
 {
     dim3 grid(P.RB, P.CC);
-    if (vec_ok(P)) k_fwd<true><<<grid, NT, 0, st>>>(P, mode, pvec, qout);
-    else k_fwd<false><<<grid, NT, 0, st>>>(P, mode, pvec, qout);
+    if (vec_ok(P)) {
+        const int mb = fwd_minb(P.m);
+        if (mb == 4) k_fwd<true, 4><<<grid, NT, 0, st>>>(P, mode, pvec, qout);
+        else if (mb == 3) k_fwd<true, 3><<<grid, NT, 0, st>>>(P, mode, pvec, qout);
+        else k_fwd<true, 1><<<grid, NT, 0, st>>>(P, mode, pvec, qout);
+    } else {
+        if (fwd_minb(P.m) == 1) k_fwd<false, 1><<<grid, NT, 0, st>>>(P, mode, pvec, qout);
+        else k_fwd<false, 3><<<grid, NT, 0, st>>>(P, mode, pvec, qout);
+    }
 }
 void launch_ls(const Prob& P, cudaStream_t st, int mode, const double* r, const double* q,
                double* f_out_dev, int ntr)

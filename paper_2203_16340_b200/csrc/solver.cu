@@ -394,7 +394,7 @@ static void gemv_geometry(Prob& P)
     const int sms = sm_count();
     P.RB = (int)cdiv(P.m, FWD_ROWS);
     static const int waves = getenv("LBFGSB_FWD_WAVES") ? atoi(getenv("LBFGSB_FWD_WAVES")) : 1;
-    const int64_t slots_f = (int64_t)sms * fwd_ctas_per_sm() * (waves > 0 ? waves : 1);
+    const int64_t slots_f = (int64_t)sms * fwd_ctas_per_sm(P.m) * (waves > 0 ? waves : 1);
     int64_t cc = clampi(slots_f / P.RB, 1, clampi(cdiv(P.ncols, 16), 1, 1 << 20));
     P.chunk = cdiv(P.ncols, cc);
     P.CC = (int)cdiv(P.ncols, P.chunk);

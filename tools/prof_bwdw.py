@@ -25,6 +25,9 @@ t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=T
 t0.record(); r = s.solve(obj, x); t1.record(); torch.cuda.synchronize()
 pr = s.profile(reset=True)
 bms, bn = pr["gemvT_epi (k_bwd)"]; fms, fn = pr["gemv_active (k_fwd)"]
+nact = pr.get("fwd_active_columns", (0, 0))[1] / max(fn, 1)
 print(json.dumps({"lib": lb._build.LIB, "config": name, "iters": r.iters, "f": r.f, "ms": t0.elapsed_time(t1),
                   "bwd_us": 1e3 * bms / max(bn, 1), "fwd_us": 1e3 * fms / max(fn, 1),
-                  "bwd_gbs": 8 * p.M.shape[0] * p.M.shape[1] / (bms / max(bn, 1) / 1e3) / 1e9}))
+                  "bwd_gbs": 8 * p.M.shape[0] * p.M.shape[1] / (bms / max(bn, 1) / 1e3) / 1e9,
+                  "fwd_active_cols": nact,
+                  "fwd_gbs": 8 * p.M.shape[0] * nact / (fms / max(fn, 1) / 1e3) / 1e9 if fn else None}))
