@@ -12,7 +12,8 @@ namespace lb {
 constexpr int T_DIR = 0, T_FWD_ALL = 1, T_LS = 2, T_KKT = 3, T_BWD_G2 = 4, T_GRAM = 5, T_SEP = 6;
 constexpr int T_FWD_RB = 64;            // + row block (<= 8192)
 constexpr int T_BWD_G1 = 64 + 8192;     // + group (<= 8000)
-static_assert(T_BWD_G1 + 8000 <= NTICKETS + 8192, "ticket space");
+constexpr int T_FWD_G = T_BWD_G1 + 8000; // + row block * FWD_MAXCG + chunk group (<= 4096)
+static_assert(T_FWD_G + 4096 <= NTICKETS + TICKETS_EXTRA, "ticket space");
 
 constexpr int BWD_BUF = 2048;           // smem doubles for the k_bwd tail reduction
 constexpr int BWD_TILE = 2 * BWD_NB;    // variables per epilogue group (split: 2 per column)

@@ -38,10 +38,13 @@ constexpr int NSEP = 2 + MAXC;                     // separable sums per trial
 constexpr int NT = 256;                            // threads per CTA
 constexpr int TILE = 256;                          // coordinates per Gram tile (k_gram)
 constexpr int FWD_ROWS = 2 * NT;                   // rows per k_fwd CTA (double2 per thread)
+constexpr int FWD_GRPC = 16;                      // k_fwd split-K partials reduced per chunk group
+constexpr int FWD_MAXCG = 64;                      // chunk groups per row block (CC <= 1024)
 constexpr int FWD_SUB = 1024;                      // columns per compaction sub-tile
 constexpr int BWD_NB = 8;                          // columns per register group in k_bwd
 constexpr int GRP = 32;                            // k_bwd CTAs per level-1 Gram group
 constexpr int NTICKETS = 8192;
+constexpr int TICKETS_EXTRA = 8192 + 4096;          // tickets[] holds NTICKETS + TICKETS_EXTRA counters
 constexpr int SEP_MAXG = 64;                       // max k_sep CTAs
 
 enum Stall : int { ST_NONE = 0, ST_FALLBACK = 1, ST_LS_CONT = 2 };

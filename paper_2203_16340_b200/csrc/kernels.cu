@@ -317,13 +317,39 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
     if (mode == FWD_ITER && blockIdx.x == 0 && threadIdx.x == 0)
         atomicAdd(reinterpret_cast<unsigned long long*>(&C->nact), (unsigned long long)nact_total);
 
-    // ---- row-block tail: finish q for rows [rb*FWD_ROWS, +FWD_ROWS)
-    if (!last_cta(P.tickets + T_FWD_RB + blockIdx.x, gridDim.y)) return;
+    // ---- row-block tail: finish q for rows [rb*FWD_ROWS, +FWD_ROWS).  Two levels
+    // when there are many column chunks (short columns, C4: 148): the last CTA
+    // of each group of FWD_GRPC chunks sums the group's partials (chunk order)
+    // into the group's first slot, the last group finisher sums the groups
+    // (group order) -- a serial pass over CC partials per row costs ~30 us.
     double q0 = 0.0, q1 = 0.0;
-    for (int c = 0; c < (int)gridDim.y; ++c) {
-        const double* src = P.qpart + (int64_t)c * m;
-        if (r0ok) q0 += __ldcg(src + row);
-        if (r1ok) q1 += __ldcg(src + row + 1);
+    const int CCn = (int)gridDim.y, ncg = (CCn + FWD_GRPC - 1) / FWD_GRPC;
+    if (ncg > 1) {
+        const int cg = (int)blockIdx.y / FWD_GRPC, c0g = cg * FWD_GRPC;
+        const int members = CCn - c0g < FWD_GRPC ? CCn - c0g : FWD_GRPC;
+        if (!last_cta(P.tickets + T_FWD_G + (int64_t)blockIdx.x * FWD_MAXCG + cg, members)) return;
+        for (int c = c0g; c < c0g + members; ++c) {
+            const double* src = P.qpart + (int64_t)c * m;
+            if (r0ok) q0 += __ldcg(src + row);
+            if (r1ok) q1 += __ldcg(src + row + 1);
+        }
+        double* dst = P.qpart + (int64_t)c0g * m;              // consumed: reuse as the group's slot
+        if (r0ok) dst[row] = q0;
+        if (r1ok) dst[row + 1] = q1;
+        if (!last_cta(P.tickets + T_FWD_RB + blockIdx.x, ncg)) return;
+        q0 = 0.0; q1 = 0.0;
+        for (int g = 0; g < ncg; ++g) {
+            const double* src = P.qpart + (int64_t)g * FWD_GRPC * m;
+            if (r0ok) q0 += __ldcg(src + row);
+            if (r1ok) q1 += __ldcg(src + row + 1);
+        }
+    } else {
+        if (!last_cta(P.tickets + T_FWD_RB + blockIdx.x, gridDim.y)) return;
+        for (int c = 0; c < CCn; ++c) {
+            const double* src = P.qpart + (int64_t)c * m;
+            if (r0ok) q0 += __ldcg(src + row);
+            if (r1ok) q1 += __ldcg(src + row + 1);
+        }
     }
     if (P.qp && P.colscale) {                                   // Q~ = D M D: row scaling
         if (r0ok) q0 = P.colscale[row] * q0;

@@ -219,7 +219,7 @@ static lbfgsb_err alloc_n(lbfgsb_t* h)
     TRY(h->dir_part.ensure(sizeof(double) * 4LL * sms * 4));
     TRY(h->kkt_part.ensure(sizeof(double) * 4LL * sms * 3));
     TRY(h->sep_part.ensure(sizeof(double) * (SEP_MAXG + 1) * KT * NSEP));
-    TRY(h->tickets.ensure(sizeof(unsigned) * (NTICKETS + 8192), true));
+    TRY(h->tickets.ensure(sizeof(unsigned) * (NTICKETS + TICKETS_EXTRA), true));
     TRY(h->fout.ensure(sizeof(double) * KT));
     CK(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
     CK(cudaMallocHost(&h->hc, sizeof(Ctrl)));
@@ -396,6 +396,9 @@ static void gemv_geometry(Prob& P)
     static const int waves = getenv("LBFGSB_FWD_WAVES") ? atoi(getenv("LBFGSB_FWD_WAVES")) : 1;
     const int64_t slots_f = (int64_t)sms * fwd_ctas_per_sm(P.m) * (waves > 0 ? waves : 1);
     int64_t cc = clampi(slots_f / P.RB, 1, clampi(cdiv(P.ncols, 16), 1, 1 << 20));
+    // the two-level q tail of k_fwd (> FWD_GRPC chunks) has FWD_MAXCG group tickets per row block
+    cc = clampi(cc, 1, (int64_t)FWD_GRPC * FWD_MAXCG);
+    if (cc > FWD_GRPC && (int64_t)P.RB * FWD_MAXCG > 4096) cc = FWD_GRPC;
     P.chunk = cdiv(P.ncols, cc);
     P.CC = (int)cdiv(P.ncols, P.chunk);
     P.GB = (int)clampi((int64_t)sms * bwd_ctas_per_sm(), 1, P.ncols);
@@ -1656,8 +1659,8 @@ extern "C" lbfgsb_err lbfgsb_op_gemv(const lbfgsb_objective* obj, const double* 
     double* qpart = nullptr;
     unsigned* tick = nullptr;
     CK(cudaMallocAsync(&qpart, sizeof(double) * (size_t)P.m * P.CC, st));
-    CK(cudaMallocAsync(&tick, sizeof(unsigned) * (NTICKETS + 8192), st));
-    CK(cudaMemsetAsync(tick, 0, sizeof(unsigned) * (NTICKETS + 8192), st));
+    CK(cudaMallocAsync(&tick, sizeof(unsigned) * (NTICKETS + TICKETS_EXTRA), st));
+    CK(cudaMemsetAsync(tick, 0, sizeof(unsigned) * (NTICKETS + TICKETS_EXTRA), st));
     P.qpart = qpart;
     P.tickets = tick;
     launch_fwd(P, st, FWD_P, p, q);
