@@ -84,7 +84,9 @@ struct DevBuf {
         bytes = 0;
         if (need == 0) need = 16;
         cudaError_t e = cudaMalloc(&p, need);
-        if (e == cudaSuccess && zero) e = cudaMemset(p, 0, need);
+        // always zeroed: recycled device memory must not leak a previous handle's state
+        (void)zero;
+        if (e == cudaSuccess) e = cudaMemset(p, 0, need);
         if (e != cudaSuccess) {
             if (p) cudaFree(p);
             p = nullptr;
