@@ -250,6 +250,20 @@ lbfgsb_err lbfgsb_solve_lsq_host(lbfgsb_t* h, const double* M_host, int64_t m, i
                                  const double* b_host, double* x_host, double tol,
                                  lbfgsb_result* res);
 
+/* `count` independent LSQ problems of one shape, all from HOST buffers
+ * (M_hosts[k]: m x ncols column-major, ld = m; b_hosts NULL or b_hosts[k]
+ * NULL = 0; x_hosts[k] in x^0 / out x*; res[k] (host) its outcome), solved
+ * one after the other on this handle.  The handle double-buffers the device
+ * copies: the host->device copy of problem k+1 runs on a copy stream while
+ * problem k is solved, so PCIe overlaps the solves; every problem's
+ * host->device and device->host copies happen inside the call (the bench's
+ * e2e number, pinned host memory recommended).  The handle keeps two device
+ * copies of the operator between calls and two captured graphs.  Errors:
+ * ARG, DIM, UNSUPPORTED (sharded handle), NONFINITE, CUDA, OOM. */
+lbfgsb_err lbfgsb_solve_lsq_host_batch(lbfgsb_t* h, int32_t count, const double* const* M_hosts, int64_t m,
+                                       int64_t ncols, const double* const* b_hosts, double* const* x_hosts,
+                                       double tol, lbfgsb_result* res);
+
 /* SURVEY 8(f) N4 "replicas": `batch` independent LSQ problems of one shape,
  *   min 1/2 ||A_k x - b_k||^2  s.t.  l_k <= x <= u_k,   k = 0..batch-1,
  * each solved by Alg. 1 in ONE CTA (A_k resident in shared

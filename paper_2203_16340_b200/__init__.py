@@ -109,6 +109,8 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_p2p_ipc_handle.argtypes = [vp, vp]
     L.lbfgsb_p2p_open.argtypes = [vp, vp]
     L.lbfgsb_p2p_connect_local.argtypes = [C.POINTER(vp), _c_i32, _c_i64]
+    L.lbfgsb_solve_lsq_host_batch.argtypes = [vp, _c_i32, C.POINTER(vp), _c_i64, _c_i64, C.POINTER(vp),
+                                              C.POINTER(vp), _c_d, C.POINTER(_Res)]
     L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
     L.lbfgsb_op_gaussian_kernel.argtypes = [vp, _c_i64, _c_i64, _c_d, vp, _c_i64, vp]
     L.lbfgsb_objective_transport.argtypes = [vp, _c_i64, _c_i64, _c_i32, _c_d, C.POINTER(vp)]
@@ -125,7 +127,8 @@ def load(build_if_needed: bool = True):
                  "lbfgsb_op_gemv", "lbfgsb_op_gemvt", "lbfgsb_op_direction", "lbfgsb_op_trials",
                  "lbfgsb_profile_get", "lbfgsb_solve_loopback", "lbfgsb_nccl_unique_id",
                  "lbfgsb_objective_qp", "lbfgsb_op_gaussian_kernel", "lbfgsb_create_sharded_p2p",
-                 "lbfgsb_p2p_ipc_handle", "lbfgsb_p2p_open", "lbfgsb_p2p_connect_local"):
+                 "lbfgsb_p2p_ipc_handle", "lbfgsb_p2p_open", "lbfgsb_p2p_connect_local",
+                 "lbfgsb_solve_lsq_host_batch"):
         getattr(L, name).restype = _c_i32
     _lib = L
     return L
@@ -417,6 +420,28 @@ class Solver:
                                           C.c_void_p(x_host.ctypes.data), float(tol), C.byref(r)))
         return Result(r.f, r.pg_inf, r.gfree_inf, r.seconds, r.iters, r.n_fg, r.n_backtracks,
                       r.n_free, r.n_fallbacks, r.status, r.last_branch)
+
+    def solve_lsq_host_batch(self, Ms, bs, xs, tol=0.0):
+        """lbfgsb_solve_lsq_host_batch: len(Ms) problems from host numpy buffers
+        (M: (m, n) Fortran-ordered float64, b: (m) or None, x: (n) in/out),
+        the next problem's H2D overlapping the current solve."""
+        import numpy as np
+        k = len(Ms)
+        if not (len(xs) == k and (bs is None or len(bs) == k)):
+            raise LbfgsbError("Ms, bs, xs lengths differ")
+        if k == 0:
+            return []
+        m, n = Ms[0].shape
+        for M_, x_ in zip(Ms, xs):
+            assert M_.flags.f_contiguous and M_.dtype == np.float64 and M_.shape == (m, n)
+            assert x_.flags.c_contiguous and x_.dtype == np.float64 and x_.shape == (n,)
+        Mp = (_c_vp * k)(*[M_.ctypes.data for M_ in Ms])
+        bp = (_c_vp * k)(*[(b_.ctypes.data if b_ is not None else None) for b_ in bs]) if bs is not None else None
+        xp = (_c_vp * k)(*[x_.ctypes.data for x_ in xs])
+        res = (_Res * k)()
+        _check(_lib.lbfgsb_solve_lsq_host_batch(self._h, k, Mp, m, n, bp, xp, float(tol), res))
+        return [Result(r.f, r.pg_inf, r.gfree_inf, r.seconds, r.iters, r.n_fg, r.n_backtracks,
+                       r.n_free, r.n_fallbacks, r.status, r.last_branch) for r in res]
 
     def al_solve(self, obj, x, E=None, e=None, G=None, hv=None,
                  al_opts: ALOptions | None = None) -> ALResult:

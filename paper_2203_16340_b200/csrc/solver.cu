@@ -129,10 +129,17 @@ struct lbfgsb_t {
     Ctrl* ctrl = nullptr;           // device
     Ctrl* hc = nullptr;             // pinned host mirror
     // graph cache
-    cudaGraphExec_t gexec = nullptr;
-    Prob gkey{};
-    int gchunk = 0;
-    cudaStream_t gstream = nullptr;
+    // two slots (the double-buffered host-batch solve alternates between two
+    // operator copies; any other use hits slot 0 again and again)
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    Prob gkey[2] = {};
+    int gchunk[2] = {0, 0};
+    cudaStream_t gstream[2] = {nullptr, nullptr};
+    int glast = 0;
+    // host-batch double buffering (lbfgsb_solve_lsq_host_batch)
+    DevBuf Mh2, bh2, xh2;
+    cudaStream_t cst = nullptr;
+    cudaEvent_t cev[4] = {nullptr, nullptr, nullptr, nullptr};   // [0,1] copied, [2,3] x* read back
     // profiling
     std::vector<cudaEvent_t> ev;    // 4 per iteration in a chunk: fwd0 fwd1 bwd0 bwd1
     double prof_ms[2] = {0, 0};
@@ -297,7 +304,12 @@ extern "C" void lbfgsb_destroy(lbfgsb_t* h)
 {
     if (!h) return;
     if (h->st) cudaStreamSynchronize(h->st);
-    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    for (int k = 0; k < 2; ++k)
+        if (h->gexec[k]) cudaGraphExecDestroy(h->gexec[k]);
+    for (int k = 0; k < 4; ++k)
+        if (h->cev[k]) cudaEventDestroy(h->cev[k]);
+    if (h->cst) cudaStreamDestroy(h->cst);
+    h->Mh2.release(); h->bh2.release(); h->xh2.release();
     for (auto e : h->ev) cudaEventDestroy(e);
     DevBuf* bufs[] = {&h->l, &h->u, &h->x, &h->g, &h->d, &h->pp, &h->pt, &h->S, &h->Y, &h->mask,
                       &h->xt, &h->gt, &h->gram_part, &h->gram_grp, &h->dir_part, &h->kkt_part,
@@ -748,9 +760,14 @@ static lbfgsb_err run_chunk(Group& g)
     const int chunk = h->o.check_every;
     const bool graph = h->o.use_graph && !g.loopback;
     if (graph) {
-        if (!h->gexec || std::memcmp(&h->gkey, &g.Ps[0], sizeof(Prob)) != 0 || h->gchunk != chunk ||
-            h->gstream != g.st) {
-            if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+        int sl = -1;
+        for (int k = 0; k < 2 && sl < 0; ++k)
+            if (h->gexec[k] && std::memcmp(&h->gkey[k], &g.Ps[0], sizeof(Prob)) == 0 && h->gchunk[k] == chunk &&
+                h->gstream[k] == g.st)
+                sl = k;
+        if (sl < 0) {
+            sl = h->gexec[0] == nullptr ? 0 : (h->gexec[1] == nullptr ? 1 : h->glast ^ 1);   // replace the LRU slot
+            if (h->gexec[sl]) { cudaGraphExecDestroy(h->gexec[sl]); h->gexec[sl] = nullptr; }
             cudaGraph_t gr = nullptr;
             CK(cudaStreamBeginCapture(g.st, cudaStreamCaptureModeThreadLocal));
             const int64_t l0 = h->launches;
@@ -760,14 +777,15 @@ static lbfgsb_err run_chunk(Group& g)
             cudaError_t e = cudaStreamEndCapture(g.st, &gr);
             if (e0 != LBFGSB_OK) { if (gr) cudaGraphDestroy(gr); return e0; }
             if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
-            e = cudaGraphInstantiate(&h->gexec, gr, 0);
+            e = cudaGraphInstantiate(&h->gexec[sl], gr, 0);
             cudaGraphDestroy(gr);
             if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-            h->gkey = g.Ps[0];
-            h->gchunk = chunk;
-            h->gstream = g.st;
+            h->gkey[sl] = g.Ps[0];
+            h->gchunk[sl] = chunk;
+            h->gstream[sl] = g.st;
         }
-        CK(cudaGraphLaunch(h->gexec, g.st));
+        h->glast = sl;
+        CK(cudaGraphLaunch(h->gexec[sl], g.st));
         h->launches += (int64_t)per_iteration_launches(g) * chunk;
     } else {
         for (int i = 0; i < chunk; ++i) TRY(launch_iteration(g, h->o.profile ? 4 * i : -1));
@@ -1068,6 +1086,60 @@ extern "C" lbfgsb_err lbfgsb_solve_lsq_host(lbfgsb_t* h, const double* M_host, i
     TRY(lbfgsb_solve(h, &ob, h->xh.d(), tol, res));
     CK(cudaMemcpyAsync(x_host, h->xh.p, sizeof(double) * ncols, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    return LBFGSB_OK;
+}
+
+// Many problems from host memory, double-buffered: the H2D copy of problem k+1
+// (copy stream) overlaps the solve of problem k; every problem's H2D of M, b,
+// x0 and D2H of x* happen inside the call.
+extern "C" lbfgsb_err lbfgsb_solve_lsq_host_batch(lbfgsb_t* h, int32_t count, const double* const* M_hosts,
+                                                  int64_t m, int64_t ncols, const double* const* b_hosts,
+                                                  double* const* x_hosts, double tol, lbfgsb_result* res)
+{
+    if (!h || count < 0 || (count > 0 && (!M_hosts || !x_hosts || !res))) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    if (m <= 0 || ncols != h->n) return fail(LBFGSB_ERR_DIM, "shape mismatch");
+    if (h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "single-GPU handles only");
+    if (count == 0) return LBFGSB_OK;
+    for (int k = 0; k < count; ++k)
+        if (!M_hosts[k] || !x_hosts[k]) return fail(LBFGSB_ERR_ARG, "NULL M or x of problem %d", k);
+    const size_t mb = sizeof(double) * (size_t)m * (size_t)ncols;
+    DevBuf* Mb[2] = {&h->Mh, &h->Mh2};
+    DevBuf* bb[2] = {&h->bh, &h->bh2};
+    DevBuf* xb[2] = {&h->xh, &h->xh2};
+    for (int k = 0; k < 2 && k < count; ++k) {
+        TRY(Mb[k]->ensure(mb));
+        TRY(bb[k]->ensure(sizeof(double) * (size_t)m));
+        TRY(xb[k]->ensure(sizeof(double) * (size_t)ncols));
+    }
+    if (!h->cst) CK(cudaStreamCreateWithFlags(&h->cst, cudaStreamNonBlocking));
+    for (int k = 0; k < 4; ++k)
+        if (!h->cev[k]) CK(cudaEventCreateWithFlags(&h->cev[k], cudaEventDisableTiming));
+    CK(cudaStreamSynchronize(h->st));                       // buffers free
+    auto issue = [&](int k) -> lbfgsb_err {
+        const int s2 = k & 1;
+        if (k >= 2) CK(cudaStreamWaitEvent(h->cst, h->cev[2 + s2], 0));   // x* of problem k-2 is read back
+        CK(cudaMemcpyAsync(Mb[s2]->p, M_hosts[k], mb, cudaMemcpyHostToDevice, h->cst));
+        if (b_hosts && b_hosts[k])
+            CK(cudaMemcpyAsync(bb[s2]->p, b_hosts[k], sizeof(double) * m, cudaMemcpyHostToDevice, h->cst));
+        CK(cudaMemcpyAsync(xb[s2]->p, x_hosts[k], sizeof(double) * ncols, cudaMemcpyHostToDevice, h->cst));
+        CK(cudaEventRecord(h->cev[s2], h->cst));
+        return LBFGSB_OK;
+    };
+    TRY(issue(0));
+    for (int k = 0; k < count; ++k) {
+        const int s2 = k & 1;
+        // buffer (k+1)&1 was last read by solve k-1, which has returned (lbfgsb_solve is host-synchronous)
+        if (k + 1 < count) TRY(issue(k + 1));
+        CK(cudaStreamWaitEvent(h->st, h->cev[s2], 0));
+        lbfgsb_objective ob{};
+        ob.kind = 0; ob.M = Mb[s2]->d(); ob.m = m; ob.ncols = ncols; ob.ld = m;
+        ob.b = (b_hosts && b_hosts[k]) ? bb[s2]->d() : nullptr;
+        TRY(lbfgsb_solve(h, &ob, xb[s2]->d(), tol, &res[k]));
+        CK(cudaMemcpyAsync(x_hosts[k], xb[s2]->p, sizeof(double) * ncols, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaEventRecord(h->cev[2 + s2], h->st));
+    }
+    CK(cudaStreamSynchronize(h->st));
+    CK(cudaStreamSynchronize(h->cst));
     return LBFGSB_OK;
 }
 
