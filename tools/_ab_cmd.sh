@@ -1,4 +1,7 @@
-# A/B of the working tree against _ab (a worktree at the previous commit), one GPU job
+# A/B of the working tree against _ab, one GPU job (gpurun -- 'bash tools/_ab_cmd.sh').
+# _ab is a worktree of the baseline commit with its own built library:
+#   git worktree add -f _ab <commit> && echo _ab/ >> .git/info/exclude
+#   (cd _ab && python -c "from paper_2203_16340_b200 import _build; _build.build()")
 mkdir -p gpurun_out/s20
 timeout 900 python -m pytest tests -m gpu -q -x --timeout=600 > gpurun_out/s20/tests.log 2>&1
 for i in 1 2; do
