@@ -127,7 +127,8 @@ lbfgsb_err lbfgsb_create(int64_t n, int32_t m_hist, const double* lower, const d
  * M~; for split objectives the u and v halves of those columns).  M, c,
  * bounds, x and the constraint columns passed later are this rank's block;
  * b is the full (replicated) m-vector.  Each iteration all-gathers, over
- * NCCL, the m-length partial of q = M~p and small packed reductions (Alg. 2
+ * NCCL (this entry point; lbfgsb_create_sharded_p2p below exchanges over
+ * peer memory instead), the m-length partial of q = M~p and small packed reductions (Alg. 2
  * sums, separable trial sums, the Gram of Alg. 3), and every rank reduces
  * them in rank order, so all ranks take bit-identical decisions.  The library
  * creates its own NCCL communicator from the 128-byte ncclUniqueId (host)

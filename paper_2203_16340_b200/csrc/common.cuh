@@ -88,7 +88,8 @@ __device__ __forceinline__ bool halted(const Ctrl* C) { return (C->done | C->sta
 // this rank's pack section pk_loc[off .. off + cnt) is stored into slot
 // [rank_id] of section `sec` of EVERY rank's mailbox (peer memory over
 // NVLink, or own memory), then one system-scope release per peer bumps that
-// peer's section counter.  k_p2p_wait on the peer waits for the count.
+// peer's section counter.  The consuming kernel on the peer waits for the count
+// in its prologue (p2p_wait_take / p2p_wait_for below).
 __device__ __forceinline__ void p2p_signal(const Prob& P, int sec)
 {
     for (int r = 0; r < P.nranks; ++r) {

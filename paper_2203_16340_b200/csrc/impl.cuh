@@ -134,7 +134,7 @@ struct Prob {
     // P2P exchange (p2p.cu): instead of an NCCL all-gather,
     // the producing kernel's tail stores this rank's pack straight into slot
     // [rank_id] of every peer's mailbox (NVLink / CUDA IPC mapped) and bumps
-    // the peer's section counter; k_p2p_wait spins on the local counter.
+    // the peer's section counter; the consuming kernel spins on the local counter.
     int p2p;
     int rank_id;
     double* peer_mb[P2P_MAXR];          // mailbox base of every rank (own one included)
