@@ -821,13 +821,16 @@ constexpr int TT_KPS = TT_WROWS / 64;         // row pairs per lane per segment 
 constexpr int TT_NSC_MAX = 5;                 // m <= 20480
 constexpr int TT_CMAX = 2048;                 // dots slots (columns per CTA + 1); 192 + 16 KB + 8 KB static <= 227 KB
 
-template <int NSC>
+// LOCK = true: the bulk-probe pipeline instead (profiles/r01_bw_probe.txt, "bulk 4x32KB 1CTA/SM":
+// 7.1 TB/s): thread 0 copies whole 32 KB segments, every thread waits on the segment's mbarrier, the CTA
+// syncs once per segment and thread 0 refills the slot just consumed; thread t owns rows 512 k + 2 t.
+template <int NSC, bool LOCK>
 __global__ void __launch_bounds__(TT_THREADS, 1) k_bwd_t(Prob P, int mode, const double* rvec, double* gout, int ns)
 {
     Ctrl* C = P.ctrl;
     if (mode == BWD_ITER && halted(C)) return;
     extern __shared__ __align__(1024) unsigned char smt[];
-    double* ring = reinterpret_cast<double*>(smt);                  // [ns][TT_WARPS][TT_WROWS]
+    double* ring = reinterpret_cast<double*>(smt);                  // [ns][TT_WARPS][TT_WROWS] | LOCK: [ns][TT_ROWS]
     double* dots = ring + (size_t)TT_STAGES * TT_ROWS;              // [cmax]
     __shared__ __align__(8) uint64_t full[TT_STAGES][TT_WARPS];
     __shared__ double red[TT_WARPS * BWD_NB];
@@ -848,32 +851,36 @@ __global__ void __launch_bounds__(TT_THREADS, 1) k_bwd_t(Prob P, int mode, const
     if (tid < TT_STAGES * TT_WARPS) mbar_init(&full[tid / TT_WARPS][tid % TT_WARPS], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    // this warp's issue cursor: column ic, segment is
+    // issue cursor (LOCK: thread 0 for the CTA; else lane 0 of each warp): column ic, segment is
     int64_t ic = 0;
     int is = 0, islot = 0;
-    const int64_t wrow0 = (int64_t)warp * TT_WROWS;
-    auto issue_next = [&]() {                                   // lane 0 only
+    const int64_t wrow0 = LOCK ? 0 : (int64_t)warp * TT_WROWS;
+    auto issue_next = [&]() {
         if (ic >= ccount) return;
         const int64_t r0 = (int64_t)is * TT_ROWS + wrow0;
-        const int64_t rows = m - r0 < TT_WROWS ? m - r0 : TT_WROWS;
-        uint64_t* bar = &full[islot][warp];
+        const int64_t span = LOCK ? TT_ROWS : TT_WROWS;
+        const int64_t rows = m - r0 < span ? m - r0 : span;
+        uint64_t* bar = LOCK ? &full[islot][0] : &full[islot][warp];
+        double* dst = LOCK ? ring + (size_t)islot * TT_ROWS : ring + ((size_t)islot * TT_WARPS + warp) * TT_WROWS;
         if (rows > 0) {
             mbar_arrive_tx(bar, 8u * (unsigned)rows);
-            bulk_g2s(ring + ((size_t)islot * TT_WARPS + warp) * TT_WROWS, P.M + (j0 + ic) * ld + r0,
-                     8u * (unsigned)rows, bar);
+            bulk_g2s(dst, P.M + (j0 + ic) * ld + r0, 8u * (unsigned)rows, bar);
         } else {
             mbar_arrive(bar);                                   // empty piece: complete the phase
         }
         if (++is == NSC) { is = 0; ++ic; }
         if (++islot == ns) islot = 0;
     };
-    if (lane == 0)
+    if (LOCK ? tid == 0 : lane == 0)
         for (int e = 0; e < ns; ++e) issue_next();
-    // r' rows (512 w + 64 k + 2 lane, +1) of every segment into registers
+    // r' in registers: rows 512 w + 64 k + 2 lane (+1) of every segment, or (LOCK) 512 k + 2 tid (+1)
+    auto row_of = [&](int s, int kk) -> int64_t {
+        return LOCK ? (int64_t)s * TT_ROWS + kk * 512 + 2 * tid : (int64_t)s * TT_ROWS + wrow0 + kk * 64 + 2 * lane;
+    };
     double2 rr[NSC * TT_KPS];
 #pragma unroll
     for (int k = 0; k < NSC * TT_KPS; ++k) {
-        const int64_t i = (int64_t)(k / TT_KPS) * TT_ROWS + wrow0 + (k % TT_KPS) * 64 + 2 * lane;
+        const int64_t i = row_of(k / TT_KPS, k % TT_KPS);
         double2 r = make_double2(0.0, 0.0);
         if (i < m) {                                            // m even: i + 1 < m
             r = *reinterpret_cast<const double2*>(rcur + i);
@@ -898,22 +905,31 @@ __global__ void __launch_bounds__(TT_THREADS, 1) k_bwd_t(Prob P, int mode, const
             if (c < nc) {
 #pragma unroll
                 for (int s = 0; s < NSC; ++s) {
-                    mbar_wait(&full[slot][warp], ph);
+                    mbar_wait(LOCK ? &full[slot][0] : &full[slot][warp], ph);
                     const double2* src =
-                        reinterpret_cast<const double2*>(ring + ((size_t)slot * TT_WARPS + warp) * TT_WROWS) + lane;
+                        LOCK ? reinterpret_cast<const double2*>(ring + (size_t)slot * TT_ROWS) + tid
+                             : reinterpret_cast<const double2*>(ring + ((size_t)slot * TT_WARPS + warp) * TT_WROWS) + lane;
 #pragma unroll
                     for (int kk = 0; kk < TT_KPS; ++kk) {
                         const int k = s * TT_KPS + kk;
-                        if ((int64_t)s * TT_ROWS + wrow0 + kk * 64 + 2 * lane < m) {
-                            const double2 a = src[kk * 32];
+                        if (row_of(s, kk) < m) {
+                            const double2 a = src[LOCK ? kk * 256 : kk * 32];
                             acc[c] = fma(a.x, rr[k].x, acc[c]);
                             acc[c] = fma(a.y, rr[k].y, acc[c]);
                         }
                     }
-                    __syncwarp();
-                    if (lane == 0) {                            // refill this warp's slot
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        issue_next();
+                    if (LOCK) {
+                        __syncthreads();                        // every thread is done with this slot
+                        if (tid == 0) {
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            issue_next();
+                        }
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) {                        // refill this warp's slot
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            issue_next();
+                        }
                     }
                     if (++slot == ns) { slot = 0; ph ^= 1u; }
                 }
@@ -1770,6 +1786,7 @@ static bool g_no_qepi_t = getenv("LBFGSB_NO_QEPI_T") != nullptr;   // register-G
 // profiles/r01_gemv_experiments.txt), so k_bwd_s stays the default.
 static bool g_no_bwd_t = getenv("LBFGSB_BWD_T") == nullptr;
 static int g_tt_stages = getenv("LBFGSB_TT_STAGES") ? atoi(getenv("LBFGSB_TT_STAGES")) : 3;
+static bool g_tt_lock = getenv("LBFGSB_TT_LOCK") != nullptr;     // k_bwd_t<.., true>: the bulk-probe pipeline
 static bool g_qepi_reg = getenv("LBFGSB_QEPI_REG") != nullptr;      // k_qepi_t (register Gram) instead of k_qepi_d (DMMA)
 constexpr int BWD_W_MAXM = 2048;
 constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + (NT / 32) * WG_STRIDE + 64);
@@ -1787,11 +1804,16 @@ static void bwd_init()
     cudaFuncSetAttribute(k_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
     {
         const int tsm = (int)(sizeof(double) * ((size_t)TT_STAGES * TT_ROWS + TT_CMAX));
-        cudaFuncSetAttribute(k_bwd_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<5, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        cudaFuncSetAttribute(k_bwd_t<5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
     }
     cudaFuncSetAttribute(k_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_W_SMEM_MAX);
     o = 0;
@@ -1904,13 +1926,18 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
     if (aligned && !g_no_bwd_t && P.m % 2 == 0 && P.m >= BWD_W_MAXM &&
         P.m <= (int64_t)TT_NSC_MAX * TT_ROWS && (P.ncols + Gs_ - 1) / Gs_ < TT_CMAX) {
         const size_t tsm = bwd_t_smem(P, Gs_);
-        const int ns = g_tt_stages >= 2 && g_tt_stages <= TT_STAGES ? g_tt_stages : 3;
+        const int ns = g_tt_stages >= 2 && g_tt_stages <= TT_STAGES ? g_tt_stages : (g_tt_lock ? 4 : 3);
         switch ((int)((P.m + TT_ROWS - 1) / TT_ROWS)) {
-            case 1: k_bwd_t<1><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            case 2: k_bwd_t<2><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            case 3: k_bwd_t<3><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            case 4: k_bwd_t<4><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            default: k_bwd_t<5><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            case 1: if (g_tt_lock) k_bwd_t<1, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
+                    else k_bwd_t<1, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            case 2: if (g_tt_lock) k_bwd_t<2, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
+                    else k_bwd_t<2, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            case 3: if (g_tt_lock) k_bwd_t<3, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
+                    else k_bwd_t<3, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            case 4: if (g_tt_lock) k_bwd_t<4, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
+                    else k_bwd_t<4, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
+            default: if (g_tt_lock) k_bwd_t<5, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
+                    else k_bwd_t<5, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
         }
         return;
     }

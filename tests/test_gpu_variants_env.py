@@ -1,7 +1,7 @@
 """The opt-in backward-GEMV variants, each selected by
 an environment variable read when the library loads, so every case runs in a
 fresh process: k_bwd_t (register r', per-warp TMA pipelines; LBFGSB_BWD_T=1,
-ring depths 2 and 3) and k_bwd_c (TMA + CTA pairs; LBFGSB_TMA=1).  Each must
+ring depths 2 and 3; and its lockstep whole-segment form, LBFGSB_TT_LOCK=1) and k_bwd_c (TMA + CTA pairs; LBFGSB_TMA=1).  Each must
 solve the NNLS instance to the oracle's optimum, like the default k_bwd_s."""
 import json
 import os
@@ -42,6 +42,7 @@ def oracle_f(orc):
 
 
 @pytest.mark.parametrize("env", [{}, {"LBFGSB_BWD_T": "1"}, {"LBFGSB_BWD_T": "1", "LBFGSB_TT_STAGES": "2"},
+                                 {"LBFGSB_BWD_T": "1", "LBFGSB_TT_LOCK": "1", "LBFGSB_TT_STAGES": "4"},
                                  {"LBFGSB_TMA": "1"}])
 def test_backward_variant_solves_to_the_oracle(env, oracle_f):
     e = dict(os.environ, **env)

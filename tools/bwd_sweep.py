@@ -37,7 +37,9 @@ if __name__ == "__main__":
         child()
         sys.exit(0)
     settings = [("k_bwd_s", {})] + \
-        [(f"k_bwd_t stages={s}", {"LBFGSB_BWD_T": "1", "LBFGSB_TT_STAGES": str(s)}) for s in (2, 3, 4, 5, 6)]
+        [(f"k_bwd_t stages={s}", {"LBFGSB_BWD_T": "1", "LBFGSB_TT_STAGES": str(s)}) for s in (3,)] + \
+        [(f"k_bwd_t lock stages={s}", {"LBFGSB_BWD_T": "1", "LBFGSB_TT_LOCK": "1", "LBFGSB_TT_STAGES": str(s)})
+         for s in (3, 4, 5, 6)]
     for name, env in settings:
         e = dict(os.environ, **env)
         out = subprocess.run([sys.executable, __file__, "--child"], env=e, capture_output=True, text=True)
