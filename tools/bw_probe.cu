@@ -153,13 +153,27 @@ float timeit(F f, int reps)
     return ms / reps;
 }
 
-int main()
+__global__ void fill_random(double* a, size_t n)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned long long z = (i + 1) * 0x9E3779B97F4A7C15ull;        // splitmix64
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        a[i] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+}
+
+int main(int argc, char** argv)
 {
     const size_t bytes = 1600000000ull;     // the C2 matrix
     const size_t n = bytes / 8;
     double* a; double* out;
     cudaMalloc(&a, bytes); cudaMalloc(&out, 8);
     cudaMemset(a, 0, bytes);
+    const bool rnd = argc > 1 && argv[1][0] == 'r';   // "r": fill with pseudo-random doubles (no zero pages)
+    if (rnd) { fill_random<<<1184, 256>>>(a, n); cudaDeviceSynchronize(); }
+    printf("# data: %s\n", rnd ? "pseudo-random doubles in [-1, 1)" : "zeros (cudaMemset)");
     int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const double2* a2 = reinterpret_cast<const double2*>(a);
     auto rep = [&](const char* name, float ms) { printf("%-36s %8.1f us  %7.1f GB/s\n", name, ms * 1e3, bytes / (ms * 1e-3) / 1e9); };
