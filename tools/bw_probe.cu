@@ -138,6 +138,61 @@ __global__ void __cluster_dims__(2, 1, 1) bulk_sum_cl(const double* __restrict__
     if (acc == 123.456) out[0] = acc;
 }
 
+
+// GEMV^T-shaped stream (C2: m = 20000 rows x 10000 columns, per-CTA balanced column ranges,
+// 4096-row segments per column (the last one 3616 rows), 4 x 32 KB TMA ring, thread 0 refills
+// after a CTA barrier).  FMA = 0: sum the segment (as bulk_sum); 1: FMA against r' held in
+// registers (thread t owns rows 512 k + 2 t), one accumulator per column.
+template <int FMA>
+__global__ void __launch_bounds__(256, 1) seg_stream(const double* __restrict__ a, int64_t m, int64_t ncols, double* out)
+{
+    constexpr int S = 4, R = 4096, NSC = 5;
+    extern __shared__ __align__(128) unsigned char sm[];
+    double* ring = reinterpret_cast<double*>(sm);
+    __shared__ __align__(8) uint64_t full[S];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
+    const int64_t total = (j1 - j0) * NSC;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    auto issue = [&](int64_t e) {
+        const int64_t c = e / NSC, r0 = (e - c * NSC) * (int64_t)R;
+        const int sl = (int)(e % S);
+        const unsigned bytes = 8u * (unsigned)(m - r0 < R ? m - r0 : R);
+        mbar_expect_tx(&full[sl], bytes);
+        bulk_g2s(ring + (size_t)sl * R, a + (j0 + c) * m + r0, bytes, &full[sl]);
+    };
+    if (tid == 0) for (int64_t e = 0; e < S && e < total; ++e) issue(e);
+    double2 rr[NSC * 8];
+#pragma unroll
+    for (int k = 0; k < NSC * 8; ++k) rr[k] = make_double2(1.0 + 1e-3 * k, 1.0 - 1e-3 * k);
+    double acc = 0.0, tot = 0.0;
+    int64_t it = 0;
+    for (int64_t c = 0; c < j1 - j0; ++c) {
+#pragma unroll
+        for (int s = 0; s < NSC; ++s, ++it) {
+            const int sl = (int)(it % S);
+            mbar_wait(&full[sl], (unsigned)((it / S) & 1));
+            const double2* src = reinterpret_cast<const double2*>(ring + (size_t)sl * R) + tid;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                if ((int64_t)s * R + kk * 512 + 2 * tid < m) {
+                    const double2 v = src[kk * 256];
+                    if (FMA) { acc = fma(v.x, rr[s * 8 + kk].x, acc); acc = fma(v.y, rr[s * 8 + kk].y, acc); }
+                    else acc += v.x + v.y;
+                }
+            }
+            __syncthreads();
+            if (tid == 0 && it + S < total) issue(it + S);
+        }
+        tot += acc; acc = 0.0;
+    }
+    if (tot == 123.456) out[0] = tot;
+}
+
 template <typename F>
 float timeit(F f, int reps)
 {
@@ -177,6 +232,14 @@ int main(int argc, char** argv)
     int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const double2* a2 = reinterpret_cast<const double2*>(a);
     auto rep = [&](const char* name, float ms) { printf("%-36s %8.1f us  %7.1f GB/s\n", name, ms * 1e3, bytes / (ms * 1e-3) / 1e9); };
+    {
+        const size_t smem = 4 * 32768;
+        cudaFuncSetAttribute(seg_stream<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(seg_stream<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        auto rep0 = [&](const char* name, float ms) { printf("%-36s %8.1f us  %7.1f GB/s\n", name, ms * 1e3, bytes / (ms * 1e-3) / 1e9); };
+        rep0("seg_stream sum 4x32KB (C2 columns)", timeit([&] { seg_stream<0><<<sms, 256, smem>>>(a, 20000, 10000, out); }, 10));
+        rep0("seg_stream fma 4x32KB (C2 columns)", timeit([&] { seg_stream<1><<<sms, 256, smem>>>(a, 20000, 10000, out); }, 10));
+    }
     for (int k : {1, 2, 4, 8}) {
         char nm[64];
         snprintf(nm, 64, "ldg_sum<4> grid=%dx%d tpb=256", sms, k);
