@@ -168,9 +168,47 @@ __global__ void __launch_bounds__(256, 1) seg_stream(const double* __restrict__ 
     if (tid == 0) for (int64_t e = 0; e < S && e < total; ++e) issue(e);
     double2 rr[NSC * 8];
 #pragma unroll
-    for (int k = 0; k < NSC * 8; ++k) rr[k] = make_double2(1.0 + 1e-3 * k, 1.0 - 1e-3 * k);
+    for (int k = 0; k < NSC * 8; ++k) {
+        if (FMA >= 2) {                                  // r' from global memory, as the kernels do
+            const int64_t i = (int64_t)k * 512 + 2 * tid;
+            rr[k] = i < m ? *reinterpret_cast<const double2*>(a + i) : make_double2(0.0, 0.0);
+        } else {
+            rr[k] = make_double2(1.0 + 1e-3 * k, 1.0 - 1e-3 * k);
+        }
+    }
     double acc = 0.0, tot = 0.0;
     int64_t it = 0;
+    if (FMA == 3) {                                      // 8-column groups, 8 accumulators (k_bwd_t's body)
+        for (int64_t jg = 0; jg < j1 - j0; jg += 8) {
+            const int nc = (int)(j1 - j0 - jg < 8 ? j1 - j0 - jg : 8);
+            double acc8[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                acc8[c] = 0.0;
+                if (c < nc) {
+#pragma unroll
+                    for (int s = 0; s < NSC; ++s, ++it) {
+                        const int sl = (int)(it % S);
+                        mbar_wait(&full[sl], (unsigned)((it / S) & 1));
+                        const double2* src = reinterpret_cast<const double2*>(ring + (size_t)sl * R) + tid;
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)
+                            if ((int64_t)s * R + kk * 512 + 2 * tid < m) {
+                                const double2 v = src[kk * 256];
+                                acc8[c] = fma(v.x, rr[s * 8 + kk].x, acc8[c]);
+                                acc8[c] = fma(v.y, rr[s * 8 + kk].y, acc8[c]);
+                            }
+                        __syncthreads();
+                        if (tid == 0 && it + S < total) issue(it + S);
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) tot += acc8[c];
+        }
+        if (tot == 123.456) out[0] = tot;
+        return;
+    }
     for (int64_t c = 0; c < j1 - j0; ++c) {
 #pragma unroll
         for (int s = 0; s < NSC; ++s, ++it) {
@@ -239,6 +277,10 @@ int main(int argc, char** argv)
         auto rep0 = [&](const char* name, float ms) { printf("%-36s %8.1f us  %7.1f GB/s\n", name, ms * 1e3, bytes / (ms * 1e-3) / 1e9); };
         rep0("seg_stream sum 4x32KB (C2 columns)", timeit([&] { seg_stream<0><<<sms, 256, smem>>>(a, 20000, 10000, out); }, 10));
         rep0("seg_stream fma 4x32KB (C2 columns)", timeit([&] { seg_stream<1><<<sms, 256, smem>>>(a, 20000, 10000, out); }, 10));
+        cudaFuncSetAttribute(seg_stream<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(seg_stream<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        rep0("seg_stream fma, r' from global", timeit([&] { seg_stream<2><<<sms, 256, smem>>>(a, 20000, 10000, out); }, 10));
+        rep0("seg_stream fma, r' global, 8 acc", timeit([&] { seg_stream<3><<<sms, 256, smem>>>(a, 20000, 10000, out); }, 10));
     }
     for (int k : {1, 2, 4, 8}) {
         char nm[64];
