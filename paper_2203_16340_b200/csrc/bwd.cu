@@ -576,24 +576,7 @@ __global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double*
     gram_tail_after(P, C, E, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
 }
 
-// ---------------------------------------------------------------- k_bwd_c (TMA, CTA pairs)
-// The B200 read ceiling for a per-CTA contiguous stream is reached with bulk
-// (TMA) copies and >= 128 KB in flight per SM (profiles/r01_bw_probe.txt:
-// 7.1 TB/s vs 6.0 TB/s for LDG from one 512-thread CTA).  With r' resident
-// in shared memory there is no room for that at m = 20000 (160 KB), so the
-// ROWS are split across a cluster of two CTAs: CTA h of cluster c keeps r'
-// for its half of the rows (80 KB) and streams its half of every column of
-// the cluster's column range through a 4 x 32 KB cp.async.bulk ring
-// (mbarrier full / empty pipeline, one producer warp, 16 consumer warps).
-// Half-row dots are combined over distributed shared memory (rank 0 + rank
-// 1, fixed order), then each CTA runs the epilogue for half of the columns.
-constexpr int TC_STAGES = 4;
-constexpr int TC_CHUNK = 4096;                                // rows per stage (one column segment)
-constexpr int TC_STAGE_BYTES = TC_CHUNK * 8;                  // 32 KB, one cp.async.bulk
-constexpr int TC_CONS = 512;                                  // consumer threads (16 warps)
-constexpr int TC_THREADS = TC_CONS;                           // all threads consume; thread 0 issues
-constexpr int TC_SMEM_MAX = 212 * 1024;   // + ~12.3 KB static <= 227 KB
-
+// ---------------------------------------------------------------- TMA / mbarrier helpers (k_qepi_t, k_qepi_d)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt)
 {
@@ -617,412 +600,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void cluster_sync_all()
-{
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ unsigned cluster_rank()
-{
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ double ld_dsmem(const double* local_ptr, unsigned rank)
-{
-    unsigned a = smem_u32(local_ptr), ra;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-    double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
-    return v;
-}
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(TC_CONS) : "memory"); }
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
-k_bwd_c(Prob P, int mode, const double* rvec, double* gout, int hmax, int cmax)
-{
-    Ctrl* C = P.ctrl;
-    if (mode == BWD_ITER && halted(C)) return;      // uniform across the cluster (same ctrl)
-    extern __shared__ __align__(1024) unsigned char smc[];
-    double* stage = reinterpret_cast<double*>(smc);                                    // [S][TC_CHUNK]
-    double* rs = reinterpret_cast<double*>(smc + (size_t)TC_STAGES * TC_STAGE_BYTES);   // [hmax]
-    double* dh = rs + hmax;                                                            // [cmax] half dots
-    double* dfull = dh + cmax;                                                         // [cmax] full dots
-    __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES];
-    __shared__ double wsh[2][TC_THREADS / 32][BWD_NB];
-    __shared__ double red[TC_THREADS / 32 * BWD_NB];
-    __shared__ double stash[TC_THREADS];
-    __shared__ double Gs[MAXE + MAXH + 2];
-
-    const unsigned h = cluster_rank();
-    const int ncl = gridDim.x / 2, cl = blockIdx.x / 2;
-    const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
-    const int64_t j0 = (int64_t)cl * ncols / ncl, j1 = (int64_t)(cl + 1) * ncols / ncl;
-    const int64_t mid = ((m / 2) + 1) & ~(int64_t)1;                 // even split row
-    const int64_t rlo = h ? mid : 0, rhi = h ? m : mid, H = rhi - rlo;
-    const bool iter = mode == BWD_ITER;
-    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
-    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
-    double* rnext = P.rbuf[rsel ^ 1];
-    const double alpha = iter ? C->alpha : 0.0;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-    if (tid == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TC_CONS / 32); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int64_t ngroups = (j1 - j0 + BWD_NB - 1) / BWD_NB;
-    // uniform row chunks of <= TC_CHUNK rows (even) per stage
-    const int64_t nchunks = (H + TC_CHUNK - 1) / TC_CHUNK;
-    const int64_t chunk = (((H + nchunks - 1) / nchunks) + 1) & ~(int64_t)1;
-    {
-        // r' for this CTA's rows; rnext slice: rows [rlo + cl*H/ncl, rlo + (cl+1)*H/ncl)
-        const int64_t w0 = rlo + (int64_t)cl * H / ncl, w1 = rlo + (int64_t)(cl + 1) * H / ncl;
-        for (int64_t i = rlo + tid; i < rhi; i += TC_THREADS) {
-            double r = rcur[i];
-            if (iter) {
-                r = fma(alpha, P.q[i], r);                      // carried residual (R13)
-                if (i >= w0 && i < w1) rnext[i] = r;
-            }
-            rs[i - rlo] = r;
-        }
-    }
-    // stage it <-> (group g, column c, row chunk ch), issued in this order by thread 0
-    int64_t total = 0;
-    for (int64_t g = 0; g < ngroups; ++g) {
-        const int64_t jg = j0 + g * BWD_NB;
-        total += (j1 - jg < BWD_NB ? j1 - jg : BWD_NB) * nchunks;
-    }
-    auto issue = [&](int64_t it) {
-        const int64_t per_col = nchunks;
-        const int64_t col = it / per_col, ch = it % per_col;      // column index within the range
-        const int s = (int)(it % TC_STAGES);
-        const int64_t r0 = rlo + ch * chunk;
-        const int rows = (int)(rhi - r0 < chunk ? rhi - r0 : chunk);
-        const unsigned bytes = (unsigned)rows * 8u;
-        mbar_arrive_tx(&full[s], bytes);
-        bulk_g2s(stage + (size_t)s * TC_CHUNK, P.M + (j0 + col) * ld + r0, bytes, &full[s]);
-    };
-    if (tid == 0)
-        for (int64_t it = 0; it < TC_STAGES && it < total; ++it) issue(it);
-    __syncthreads();                                            // r' complete
-    double acc[BWD_NB];
-#pragma unroll
-    for (int k = 0; k < BWD_NB; ++k) acc[k] = 0.0;
-    int64_t it = 0;
-    for (int64_t g = 0; g < ngroups; ++g) {
-        const int64_t jg = j0 + g * BWD_NB;
-        const int nc = (int)(j1 - jg < BWD_NB ? j1 - jg : BWD_NB);
-        for (int c = 0; c < nc; ++c) {
-            double sacc = 0.0;
-            for (int64_t ch = 0; ch < nchunks; ++ch, ++it) {
-                const int s = (int)(it % TC_STAGES);
-                const int64_t r0 = ch * chunk;                  // relative to rlo
-                const int rows = (int)(H - r0 < chunk ? H - r0 : chunk);
-                mbar_wait(&full[s], (unsigned)((it / TC_STAGES) & 1));
-                const double* src = stage + (size_t)s * TC_CHUNK;
-                for (int i = 2 * tid; i < rows; i += 2 * TC_THREADS) {   // consecutive 16 B per thread
-                    if (i + 1 < rows) {
-                        const double2 av = *reinterpret_cast<const double2*>(src + i);
-                        const double2 rv = *reinterpret_cast<const double2*>(rs + r0 + i);
-                        sacc = fma(av.x, rv.x, sacc);
-                        sacc = fma(av.y, rv.y, sacc);
-                    } else {
-                        sacc = fma(src[i], rs[r0 + i], sacc);
-                    }
-                }
-                __syncthreads();                                // stage s consumed
-                if (tid == 0 && it + TC_STAGES < total) issue(it + TC_STAGES);
-            }
-#pragma unroll
-            for (int k = 0; k < BWD_NB; ++k)
-                if (k == c) acc[k] = sacc;
-        }
-        // group complete: reduce the nc column dots
-        const int par = (int)(g & 1);
-#pragma unroll
-        for (int k = 0; k < BWD_NB; ++k) {
-            const double v = warp_red<0>(acc[k]);
-            if (lane == 0) wsh[par][warp][k] = v;
-            acc[k] = 0.0;
-        }
-        __syncthreads();
-        if (tid < nc) {
-            double v = wsh[par][0][tid];
-            for (int w = 1; w < TC_THREADS / 32; ++w) v += wsh[par][w][tid];
-            dh[g * BWD_NB + tid] = v;
-        }
-    }
-    __syncthreads();
-    // ---- combine the two half-row dots over DSMEM: rank 0 part + rank 1 part
-    const int64_t ccount = j1 - j0;
-    cluster_sync_all();
-    for (int64_t t = tid; t < ccount; t += TC_THREADS) {
-        const double a0 = h == 0 ? dh[t] : ld_dsmem(dh + t, 0);
-        const double a1 = h == 1 ? dh[t] : ld_dsmem(dh + t, 1);
-        dfull[t] = a0 + a1;
-    }
-    cluster_sync_all();                                         // partner done reading our dh
-    // ---- epilogue: CTA h owns columns [e0, e1) of the cluster range
-    const int64_t e0 = h ? ccount / 2 : 0, e1 = h ? ccount : ccount / 2;
-    const int nvg = P.split ? 2 : 1;
-    const int64_t ecols = e1 - e0, nvar = ecols * nvg;
-    if (mode == BWD_PLAIN) {
-        for (int64_t t = tid; t < nvar; t += TC_THREADS) {
-            const int64_t jj = e0 + t % ecols, vv = t / ecols;
-            const int64_t j = j0 + jj;
-            const double dot = dfull[jj];
-            double dval = vv ? -dot : dot;
-            if (P.colscale) dval = P.colscale[j] * dot;
-            gout[j + vv * ncols] = dval;
-        }
-        return;
-    }
-    EpiCtx E;
-    epi_init(P, C, mode, E);
-    GramEnt ent;
-    const int ne = E.nb * (E.nb + 1) / 2;
-    ent.init(E.nb, ne, ne + (P.screen_full ? E.nh : 0), E.nh);
-    double gacc[3] = {0.0, 0.0, 0.0};
-    double gmax = 0.0, cnt = 0.0;
-    constexpr int EPI_ROWS = 256;                               // tile fits the 128 KB stage ring
-    double* tile = stage;                                       // stages are free now
-    double* mk = stage + (size_t)EPI_ROWS * E.nb;
-    for (int64_t vb = 0; vb < nvar; vb += EPI_ROWS) {
-        const int rows = (int)(nvar - vb < EPI_ROWS ? nvar - vb : EPI_ROWS);
-        if (tid < rows) {
-            const int64_t idx = vb + tid;
-            const int64_t jj = e0 + idx % ecols, vv = idx / ecols;
-            const int64_t j = j0 + jj;
-            const double dot = dfull[jj];
-            double dval = vv ? -dot : dot;
-            if (P.colscale) dval = P.colscale[j] * dot;
-            epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)tid * E.nb, mk + tid, gmax, cnt);
-        }
-        if (E.gram) {
-            __syncthreads();
-            ent.accumulate(tile, mk, rows, E.nb, gacc);
-        }
-        __syncthreads();
-    }
-    if (!E.gram) return;
-    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, stage, 4096, stash, Gs);
-}
-
-// ---------------------------------------------------------------- k_bwd_t
-// TMA variant for 2048 <= m <= 20480 (C2, C3): r' lives in REGISTERS, so
-// shared memory is a ring of ns x 32 KB cp.async.bulk stages for the column
-// stream.  Every WARP is its own pipeline: the CTA's balanced column range is
-// walked in 4096-row segments (NSC per column) and warp w owns rows
-// [512 w, 512 w + 512) of every segment (lane l: rows 512 w + 64 k + 2 l, +1),
-// so it issues its own 4 KB bulk copy per segment into its own slot of each
-// stage and waits on its own mbarrier; a slot is refilled by the same warp as
-// soon as its lanes are done with it.  No warp waits on another inside the
-// stream (a shared producer thread measured 295-395 us on C2: its refills
-// trail the slowest warp).  8 warps of <= 255 registers (2 per SMSP).
-// Column dots are reduced per group of 8; the epilogue, Gram and Alg. 3 tail
-// are those of k_bwd_s, with the ring as the tile buffer.
-constexpr int TT_THREADS = 256;
-constexpr int TT_WARPS = TT_THREADS / 32;
-constexpr int TT_ROWS = 4096;                 // rows per segment (32 KB)
-constexpr int TT_WROWS = TT_ROWS / TT_WARPS;  // rows per warp piece (512, 4 KB)
-constexpr int TT_STAGES = 6;
-constexpr int TT_KPS = TT_WROWS / 64;         // row pairs per lane per segment (8)
-constexpr int TT_NSC_MAX = 5;                 // m <= 20480
-constexpr int TT_CMAX = 2048;                 // dots slots (columns per CTA + 1); 192 + 16 KB + 8 KB static <= 227 KB
-
-// LOCK = true: the bulk-probe pipeline instead (profiles/r01_bw_probe.txt, "bulk 4x32KB 1CTA/SM":
-// 7.1 TB/s): thread 0 copies whole 32 KB segments, every thread waits on the segment's mbarrier, the CTA
-// syncs once per segment and thread 0 refills the slot just consumed; thread t owns rows 512 k + 2 t.
-template <int NSC, bool LOCK>
-__global__ void __launch_bounds__(TT_THREADS, 1) k_bwd_t(Prob P, int mode, const double* rvec, double* gout, int ns)
-{
-    Ctrl* C = P.ctrl;
-    if (mode == BWD_ITER && halted(C)) return;
-    extern __shared__ __align__(1024) unsigned char smt[];
-    double* ring = reinterpret_cast<double*>(smt);                  // [ns][TT_WARPS][TT_WROWS] | LOCK: [ns][TT_ROWS]
-    double* dots = ring + (size_t)TT_STAGES * TT_ROWS;              // [cmax]
-    __shared__ __align__(8) uint64_t full[TT_STAGES][TT_WARPS];
-    __shared__ double red[TT_WARPS * BWD_NB];
-    __shared__ double stash[TT_THREADS];
-    __shared__ double Gs[MAXE + MAXH + 2];
-    const int G = gridDim.x, cta = blockIdx.x;
-    const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
-    const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
-    const int64_t i0 = (int64_t)cta * m / G, i1 = (int64_t)(cta + 1) * m / G;
-    const bool iter = mode == BWD_ITER;
-    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
-    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
-    double* rnext = P.rbuf[rsel ^ 1];
-    const double alpha = iter ? C->alpha : 0.0;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t ccount = j1 - j0;
-
-    if (tid < TT_STAGES * TT_WARPS) mbar_init(&full[tid / TT_WARPS][tid % TT_WARPS], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-    // issue cursor (LOCK: thread 0 for the CTA; else lane 0 of each warp): column ic, segment is
-    int64_t ic = 0;
-    int is = 0, islot = 0;
-    const int64_t wrow0 = LOCK ? 0 : (int64_t)warp * TT_WROWS;
-    auto issue_next = [&]() {
-        if (ic >= ccount) return;
-        const int64_t r0 = (int64_t)is * TT_ROWS + wrow0;
-        const int64_t span = LOCK ? TT_ROWS : TT_WROWS;
-        const int64_t rows = m - r0 < span ? m - r0 : span;
-        uint64_t* bar = LOCK ? &full[islot][0] : &full[islot][warp];
-        double* dst = LOCK ? ring + (size_t)islot * TT_ROWS : ring + ((size_t)islot * TT_WARPS + warp) * TT_WROWS;
-        if (rows > 0) {
-            mbar_arrive_tx(bar, 8u * (unsigned)rows);
-            bulk_g2s(dst, P.M + (j0 + ic) * ld + r0, 8u * (unsigned)rows, bar);
-        } else {
-            mbar_arrive(bar);                                   // empty piece: complete the phase
-        }
-        if (++is == NSC) { is = 0; ++ic; }
-        if (++islot == ns) islot = 0;
-    };
-    if (LOCK ? tid == 0 : lane == 0)
-        for (int e = 0; e < ns; ++e) issue_next();
-    // r' in registers: rows 512 w + 64 k + 2 lane (+1) of every segment, or (LOCK) 512 k + 2 tid (+1)
-    auto row_of = [&](int s, int kk) -> int64_t {
-        return LOCK ? (int64_t)s * TT_ROWS + kk * 512 + 2 * tid : (int64_t)s * TT_ROWS + wrow0 + kk * 64 + 2 * lane;
-    };
-    double2 rr[NSC * TT_KPS];
-#pragma unroll
-    for (int k = 0; k < NSC * TT_KPS; ++k) {
-        const int64_t i = row_of(k / TT_KPS, k % TT_KPS);
-        double2 r = make_double2(0.0, 0.0);
-        if (i < m) {                                            // m even: i + 1 < m
-            r = *reinterpret_cast<const double2*>(rcur + i);
-            if (iter) {
-                const double2 qq = *reinterpret_cast<const double2*>(P.q + i);
-                r.x = fma(alpha, qq.x, r.x);                    // carried residual (R13)
-                r.y = fma(alpha, qq.y, r.y);
-            }
-        }
-        rr[k] = r;
-    }
-    if (iter)
-        for (int64_t i = i0 + tid; i < i1; i += TT_THREADS) rnext[i] = fma(alpha, P.q[i], rcur[i]);
-    int slot = 0;
-    unsigned ph = 0;
-    for (int64_t jg = 0; jg < ccount; jg += BWD_NB) {
-        const int nc = (int)(ccount - jg < BWD_NB ? ccount - jg : BWD_NB);
-        double acc[BWD_NB];
-#pragma unroll
-        for (int c = 0; c < BWD_NB; ++c) {
-            acc[c] = 0.0;
-            if (c < nc) {
-#pragma unroll
-                for (int s = 0; s < NSC; ++s) {
-                    mbar_wait(LOCK ? &full[slot][0] : &full[slot][warp], ph);
-                    const double2* src =
-                        LOCK ? reinterpret_cast<const double2*>(ring + (size_t)slot * TT_ROWS) + tid
-                             : reinterpret_cast<const double2*>(ring + ((size_t)slot * TT_WARPS + warp) * TT_WROWS) + lane;
-#pragma unroll
-                    for (int kk = 0; kk < TT_KPS; ++kk) {
-                        const int k = s * TT_KPS + kk;
-                        if (row_of(s, kk) < m) {
-                            const double2 a = src[LOCK ? kk * 256 : kk * 32];
-                            acc[c] = fma(a.x, rr[k].x, acc[c]);
-                            acc[c] = fma(a.y, rr[k].y, acc[c]);
-                        }
-                    }
-                    if (LOCK) {
-                        __syncthreads();                        // every thread is done with this slot
-                        if (tid == 0) {
-                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                            issue_next();
-                        }
-                    } else {
-                        __syncwarp();
-                        if (lane == 0) {                        // refill this warp's slot
-                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                            issue_next();
-                        }
-                    }
-                    if (++slot == ns) { slot = 0; ph ^= 1u; }
-                }
-            }
-        }
-        // group complete: deterministic reduction of the nc column dots
-#pragma unroll
-        for (int c = 0; c < BWD_NB; ++c) {
-            const double v = warp_red<0>(acc[c]);
-            if (lane == 0) red[warp * BWD_NB + c] = v;
-        }
-        __syncthreads();
-        if (tid < nc) {
-            double v = red[tid];
-            for (int w = 1; w < TT_WARPS; ++w) v += red[w * BWD_NB + tid];
-            dots[jg + tid] = v;
-        }
-        __syncthreads();
-    }
-    __syncthreads();
-    const int nvg = P.split ? 2 : 1;
-    const int nvar = (int)ccount * nvg;
-    if (mode == BWD_PLAIN) {
-        for (int t = tid; t < nvar; t += TT_THREADS) {
-            const int jj = t % (int)ccount, vv = t / (int)ccount;
-            const int64_t j = j0 + jj;
-            const double dot = dots[jj];
-            double dval = vv ? -dot : dot;
-            if (P.colscale) dval = P.colscale[j] * dot;
-            gout[j + vv * ncols] = dval;
-        }
-        return;
-    }
-    EpiCtx E;
-    epi_init(P, C, mode, E);
-    GramEnt ent;
-    const int ne = E.nb * (E.nb + 1) / 2;
-    ent.init(E.nb, ne, ne + (P.screen_full ? E.nh : 0), E.nh);
-    double gacc[3] = {0.0, 0.0, 0.0};
-    double gmax = 0.0, cnt = 0.0;
-    double* tile = ring;                                        // the ring is free now
-    double* mk = ring + (int64_t)EPI_TILE * E.nb;
-    for (int vb = 0; vb < nvar; vb += EPI_TILE) {
-        const int rows = nvar - vb < EPI_TILE ? nvar - vb : EPI_TILE;
-        if (tid < rows) {
-            const int idx = vb + tid;
-            const int jj = idx % (int)ccount, vv = idx / (int)ccount;
-            const int64_t j = j0 + jj;
-            const double dot = dots[jj];
-            double dval = vv ? -dot : dot;
-            if (P.colscale) dval = P.colscale[j] * dot;
-            epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)tid * E.nb, mk + tid, gmax, cnt);
-        }
-        if (E.gram) {
-            __syncthreads();
-            ent.accumulate(tile, mk, rows, E.nb, gacc);
-        }
-        __syncthreads();
-    }
-    if (!E.gram) return;
-    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, ring, 4096, stash, Gs);
-}
-
-static size_t bwd_t_smem(const Prob& P, int G)
-{
-    const int64_t cmax = (P.ncols + G - 1) / G;
-    return sizeof(double) * ((size_t)TT_STAGES * TT_ROWS + (size_t)cmax + 1);
-}
-
-// smem k_bwd_c needs (0 = does not fit / not applicable)
-static size_t bwd_c_smem(const Prob& P, int ncl, int* hmax, int* cmax)
-{
-    if (P.m % 2 != 0 || P.m < 4096) return 0;
-    const int64_t mid = ((P.m / 2) + 1) & ~(int64_t)1;
-    const int64_t H = P.m - mid > mid ? P.m - mid : mid;
-    const int64_t cm = (P.ncols + ncl - 1) / ncl + 1;
-    const size_t bytes = (size_t)TC_STAGES * TC_STAGE_BYTES + sizeof(double) * (size_t)(H + 2 * cm + 8);
-    if (bytes > (size_t)TC_SMEM_MAX) return 0;
-    *hmax = (int)H;
-    *cmax = (int)cm;
-    return bytes;
-}
-
 // ---------------------------------------------------------------- k_qpu (QP objective)
 // QP objective (the kernel dual SVM): f = 1/2 x^T Q~ x + ..., the
 // gradient is carried as w = Q~ x (like the LSQ residual, R13): w' =
@@ -1783,20 +1360,10 @@ __global__ void __launch_bounds__(NT, 2) k_qepi_d(Prob P, int mode)
 
 // ---------------------------------------------------------------- launch
 static int g_bwd_occ = 0, g_bwdw_occ = 0;
-// k_bwd_c (TMA, CTA pairs) is opt-in: on C2 it measured 275-335 us vs 268 us for k_bwd_s
-// (DESIGN.md section 5); enable with LBFGSB_TMA=1 for experiments.
-static bool g_no_tma = getenv("LBFGSB_TMA") == nullptr;
 // k_qepi (register Gram) is the QP / transport epilogue for m_hist <= 5; LBFGSB_NO_QEPI=1
 // selects the shared-memory tile kernel k_qpu instead (A/B experiments)
 static bool g_no_qepi = getenv("LBFGSB_NO_QEPI") != nullptr;
 static bool g_no_qepi_t = getenv("LBFGSB_NO_QEPI_T") != nullptr;   // register-Gram kernel without TMA staging
-// k_bwd_t (register r', per-warp TMA pipelines) is opt-in (LBFGSB_BWD_T=1, ring depth
-// LBFGSB_TT_STAGES, default 3): on C2 it streams at 6.30 TB/s against k_bwd_s's 6.25 TB/s
-// as a plain GEMV^T but runs 275 vs 270 us inside the solve (tools/bwd_sweep.py,
-// profiles/r01_gemv_experiments.txt), so k_bwd_s stays the default.
-static bool g_no_bwd_t = getenv("LBFGSB_BWD_T") == nullptr;
-static int g_tt_stages = getenv("LBFGSB_TT_STAGES") ? atoi(getenv("LBFGSB_TT_STAGES")) : 3;
-static bool g_tt_lock = getenv("LBFGSB_TT_LOCK") != nullptr;     // k_bwd_t<.., true>: the bulk-probe pipeline
 static bool g_qepi_reg = getenv("LBFGSB_QEPI_REG") != nullptr;      // k_qepi_t (register Gram) instead of k_qepi_d (DMMA)
 constexpr int BWD_W_MAXM = 2048;
 constexpr int BWD_W_SMEM_MAX = (int)sizeof(double) * (BWD_W_MAXM + WTILE * (MAXB + 1) + (NT / 32) * WG_STRIDE + 64);
@@ -1811,20 +1378,6 @@ static void bwd_init()
     cudaFuncSetAttribute(k_bwd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_MAX);
     cudaFuncSetAttribute(k_qpu, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(double) * (NT * (MAXB + 1) > 4096 ? NT * (MAXB + 1) : 4096)));
-    cudaFuncSetAttribute(k_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
-    {
-        const int tsm = (int)(sizeof(double) * ((size_t)TT_STAGES * TT_ROWS + TT_CMAX));
-        cudaFuncSetAttribute(k_bwd_t<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<5, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-        cudaFuncSetAttribute(k_bwd_t<5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-    }
     cudaFuncSetAttribute(k_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_W_SMEM_MAX);
     o = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_w, NT, BWD_W_SMEM_MAX);
@@ -1932,33 +1485,6 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         const int Gw = (int)(P.ncols < (int64_t)sms * occ_w ? P.ncols : (int64_t)sms * occ_w);
         k_bwd_w<<<Gw, NT, sm, st>>>(P, mode, rvec, gout, mpad, wgs);
         return;
-    }
-    if (aligned && !g_no_bwd_t && P.m % 2 == 0 && P.m >= BWD_W_MAXM &&
-        P.m <= (int64_t)TT_NSC_MAX * TT_ROWS && (P.ncols + Gs_ - 1) / Gs_ < TT_CMAX) {
-        const size_t tsm = bwd_t_smem(P, Gs_);
-        const int ns = g_tt_stages >= 2 && g_tt_stages <= TT_STAGES ? g_tt_stages : (g_tt_lock ? 4 : 3);
-        switch ((int)((P.m + TT_ROWS - 1) / TT_ROWS)) {
-            case 1: if (g_tt_lock) k_bwd_t<1, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
-                    else k_bwd_t<1, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            case 2: if (g_tt_lock) k_bwd_t<2, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
-                    else k_bwd_t<2, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            case 3: if (g_tt_lock) k_bwd_t<3, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
-                    else k_bwd_t<3, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            case 4: if (g_tt_lock) k_bwd_t<4, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
-                    else k_bwd_t<4, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-            default: if (g_tt_lock) k_bwd_t<5, true><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns);
-                    else k_bwd_t<5, false><<<Gs_, TT_THREADS, tsm, st>>>(P, mode, rvec, gout, ns); break;
-        }
-        return;
-    }
-    if (aligned && !g_no_tma) {
-        const int ncl = (int)(P.ncols < sms / 2 ? P.ncols : sms / 2);
-        int hmax = 0, cmax = 0;
-        const size_t csm = bwd_c_smem(P, ncl, &hmax, &cmax);
-        if (csm && ncl >= 1) {
-            k_bwd_c<<<2 * ncl, TC_THREADS, csm, st>>>(P, mode, rvec, gout, hmax, cmax);
-            return;
-        }
     }
     if (smem && P.m >= 2048) {
         const int64_t cmax = (P.ncols + Gs_ - 1) / Gs_;
