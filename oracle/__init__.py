@@ -38,6 +38,44 @@ def build(force: bool = False) -> str:
 _lib = None
 
 
+class using_library:
+    """Context manager: route every call of this module through another build
+    of oracle.c (the mutation tests compile deliberately broken copies and
+    check that the pins reject them)."""
+
+    def __init__(self, path):
+        self.path = path
+
+    def __enter__(self):
+        global _lib
+        self._saved = _lib
+        lib = C.CDLL(self.path)
+        _setup(lib)
+        _lib = lib
+        return self
+
+    def __exit__(self, *exc):
+        global _lib
+        _lib = self._saved
+        return False
+
+
+def build_variant(out_path, replacements):
+    """Compile a copy of oracle.c with each (old, new) text replacement applied
+    (each ``old`` must occur exactly once).  Test infrastructure for the
+    mutation pins only."""
+    src = open(_SRC).read()
+    for old, new in replacements:
+        assert src.count(old) == 1, ("mutation anchor not unique", old)
+        src = src.replace(old, new)
+    cpath = out_path + ".c"
+    with open(cpath, "w") as f:
+        f.write(src)
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+                           cpath, "-o", out_path, "-lm"])
+    return out_path
+
+
 def _L():
     global _lib
     if _lib is None:
@@ -102,6 +140,16 @@ def _setup(L):
                                    C.POINTER(_Res)]
     L.orc_al_solve.argtypes = [C.POINTER(_Lsq), _dp, _dp, _dp, _dp, i32, C.POINTER(_Opts),
                                C.POINTER(_AlOpts), _dp, C.POINTER(_AlRes)]
+    L.orc_al_solve_ex.argtypes = [C.POINTER(_Lsq), _dp, _dp, _dp, _dp, i32, C.POINTER(_Opts),
+                                  C.POINTER(_AlOpts), _dp, i32, _dp, C.POINTER(_AlRes)]
+    L.orc_al_violation.argtypes = [i32, _dp, i32, _dp, _dp, d]
+    L.orc_al_violation.restype = d
+    L.orc_al_update_multipliers.argtypes = [i32, _dp, _dp, i32, _dp, _dp, d]
+    L.orc_al_update_rho.argtypes = [d, d, d, d, d]
+    L.orc_al_update_rho.restype = d
+    L.orc_armijo_lsq.argtypes = [C.POINTER(_Lsq), C.POINTER(_Opts), i64, _dp, _dp, _dp, _dp, _dp,
+                                 _dp, d, d, d, _dp, _dp, _dp, _dp, C.POINTER(i64)]
+    L.orc_armijo_lsq.restype = i32
     L.orc_check_convergence.argtypes = [i64, _dp, _u8p, d]
     L.orc_check_convergence.restype = i32
     L.orc_lsq_value.argtypes = [C.POINTER(_Lsq), _dp]
@@ -447,19 +495,91 @@ class ALResult:
 
 
 def al_solve(P: LSQ, l=None, u=None, m_hist=5, opts: Options | None = None,
-             al_opts: ALOptions | None = None):
-    """Alg. 4 for linear constraints."""
+             al_opts: ALOptions | None = None, x0=None, lam0=None, mu0=None, trace=False):
+    """Alg. 4 for linear constraints.
+
+    Cold start (default): x^0 = clip(0), lam = mu = 0 (R19).  Passing any of
+    x0 / lam0 / mu0 re-enters the method from that state (missing parts are
+    zero).  trace=True also returns, per outer iteration, a dict with the rho
+    the inner solve used, the violation v after the multiplier update, the rho
+    after the penalty rule, lam, mu and x."""
     o = opts or Options(); ao = al_opts or ALOptions()
-    x = np.zeros(P.nvars)
+    warm = x0 is not None or lam0 is not None or mu0 is not None
+    x = np.zeros(P.nvars) if x0 is None else _f64(x0).copy()
     l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
     u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
     lam = np.zeros(max(P.n_eq, 1)); mu = np.zeros(max(P.n_in, 1))
+    if lam0 is not None:
+        lam[:P.n_eq] = lam0
+    if mu0 is not None:
+        mu[:P.n_in] = mu0
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
                int(o.no_projection), int(o.armijo_diff), o.max_iters)
     sa = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer)
     s = P._struct()
     res = _AlRes()
-    _L().orc_al_solve(C.byref(s), _ptr(lam), _ptr(mu), _ptr(l), _ptr(u), m_hist, C.byref(so),
-                      C.byref(sa), _ptr(x), C.byref(res))
-    return ALResult(x, lam[:P.n_eq].copy(), mu[:P.n_in].copy(), res.f, res.violation_inf,
-                    res.rho, res.outer_iters, res.inner_iters_total, res.status)
+    rec = 3 + P.n_eq + P.n_in + P.nvars
+    tb = np.zeros(ao.max_outer * rec) if trace else None
+    _L().orc_al_solve_ex(C.byref(s), _ptr(lam), _ptr(mu), _ptr(l), _ptr(u), m_hist, C.byref(so),
+                         C.byref(sa), _ptr(x), int(warm), _ptr(tb), C.byref(res))
+    out = ALResult(x, lam[:P.n_eq].copy(), mu[:P.n_in].copy(), res.f, res.violation_inf,
+                   res.rho, res.outer_iters, res.inner_iters_total, res.status)
+    if trace:
+        recs = []
+        for it in range(res.outer_iters):
+            t = tb[it * rec:(it + 1) * rec]
+            recs.append({"rho_used": t[0], "v": t[1], "rho_next": t[2],
+                         "lam": t[3:3 + P.n_eq].copy(), "mu": t[3 + P.n_eq:3 + P.n_eq + P.n_in].copy(),
+                         "x": t[3 + P.n_eq + P.n_in:].copy()})
+        return out, recs
+    return out
+
+
+def al_violation(h=(), g=(), mu=None, rho=1.0):
+    """Violation measure of Alg. 4's penalty rule / stop test (R21)."""
+    h = _f64(np.atleast_1d(h)) if len(h) else np.zeros(1)
+    gg = _f64(np.atleast_1d(g)) if len(g) else np.zeros(1)
+    mu = np.zeros_like(gg) if mu is None else _f64(np.atleast_1d(mu))
+    return _L().orc_al_violation(len(np.atleast_1d(h)) if len(h) else 0, _ptr(h),
+                                 len(g), _ptr(gg), _ptr(mu), float(rho))
+
+
+def al_update_multipliers(lam, h, mu, g, rho):
+    """Alg. 4 lines 6-7.  Returns (lam', mu')."""
+    lam = _f64(np.atleast_1d(lam)).copy() if len(lam) else np.zeros(1)
+    mu = _f64(np.atleast_1d(mu)).copy() if len(mu) else np.zeros(1)
+    hh = _f64(np.atleast_1d(h)) if len(h) else np.zeros(1)
+    gg = _f64(np.atleast_1d(g)) if len(g) else np.zeros(1)
+    _L().orc_al_update_multipliers(len(h), _ptr(lam), _ptr(hh), len(g), _ptr(mu), _ptr(gg), float(rho))
+    return lam[:len(h)], mu[:len(g)]
+
+
+def al_update_rho(rho, vprev, v, factor=2.0, cap=1e12):
+    """Penalty rule of Alg. 4 (R20)."""
+    return _L().orc_al_update_rho(float(rho), float(vprev), float(v), float(factor), float(cap))
+
+
+def armijo_lsq(P: LSQ, x, p, amax, l=None, u=None, opts: Options | None = None):
+    """The oracle's Armijo backtracking on the carried residual (R10, R11, R13)
+    from the state (x, r = M~x - b, f, g) along p with upper bound amax.
+    Returns (accepted, alpha, f_t, number of rejected trials, x_t)."""
+    o = opts or Options()
+    x = _f64(x); p = _f64(p)
+    l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
+    u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
+    r = P.apply(x)
+    if not P.qp and P.b is not None:
+        r = _f64(r - P.b)
+    q = _f64(P.apply(p))
+    f = P.value(x)
+    g = P.grad(x)
+    gp = float(np.dot(g, p))
+    so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
+               int(o.no_projection), int(o.armijo_diff), o.max_iters)
+    xt = np.empty(P.nvars); rt = np.empty(max(P.m, 1))
+    fo = C.c_double(0.0); ao = C.c_double(0.0); nbt = C.c_int64(0)
+    s = P._struct()
+    ok = _L().orc_armijo_lsq(C.byref(s), C.byref(so), P.nvars, _ptr(x), _ptr(l), _ptr(u), _ptr(_f64(r)),
+                             _ptr(q), _ptr(p), f, gp, float(amax), _ptr(xt), _ptr(rt), C.byref(fo),
+                             C.byref(ao), C.byref(nbt))
+    return bool(ok), ao.value, fo.value, int(nbt.value), xt

@@ -519,6 +519,19 @@ static int armijo_lsq(const orc_lsq* P, const orc_opts* o, int64_t nv, const dou
     return 0;
 }
 
+/* armijo_lsq exposed for its pins (R10, R11): returns 1 on acceptance and
+ * the accepted alpha, f_t, and the number of rejected trials. */
+int32_t orc_armijo_lsq(const orc_lsq* P, const orc_opts* o, int64_t nv, const double* x,
+                       const double* l, const double* u, const double* r, const double* q,
+                       const double* p, double f, double gp, double amax,
+                       double* x_t, double* r_t, double* f_out, double* alpha_out, int64_t* n_bt)
+{
+    int64_t n_fg = 0;
+    *n_bt = 0;
+    return armijo_lsq(P, o, nv, x, l, u, r, q, p, f, gp, amax, x_t, r_t, f_out, alpha_out,
+                      &n_fg, n_bt);
+}
+
 /* Solve min f(x) s.t. l <= x <= u with Alg. 1.  x in: x0 (clipped),
  * out: x*.  m_hist pairs, newest last. */
 void orc_minimize_lsq(const orc_lsq* P, const double* l, const double* u, int32_t m_hist,
@@ -628,36 +641,77 @@ typedef struct {
  * -- the complementarity-aware measure of Birgin & Martinez (2014), the
  * reference PAPER.md:531 cites for the convergence of Alg. 4.  For equality
  * constraints it is ||h||_inf; for an inequality it is the violation g_+
- * when g > 0 and otherwise how far mu is from complementary slackness. */
-static double viol_inf(const orc_lsq* P, const double* x, const double* mu, double rho)
+ * when g > 0 and otherwise how far mu is from complementary slackness.
+ * h: n_eq values, g: n_in values (either may be NULL when its count is 0). */
+double orc_al_violation(int32_t n_eq, const double* h, int32_t n_in, const double* g,
+                        const double* mu, double rho)
 {
-    double* hval = cons_buf(P->n_eq);
-    double* gval = cons_buf(P->n_in);
     double v = 0.0;
-    lsq_cons(P, x, hval, gval);
-    for (int32_t k = 0; k < P->n_eq; ++k) if (fabs(hval[k]) > v) v = fabs(hval[k]);
-    for (int32_t k = 0; k < P->n_in; ++k) {
-        double t = -gval[k];
+    for (int32_t k = 0; k < n_eq; ++k) if (fabs(h[k]) > v) v = fabs(h[k]);
+    for (int32_t k = 0; k < n_in; ++k) {
+        double t = -g[k];
         const double mr = mu[k] / rho;
         if (mr < t) t = mr;
         if (fabs(t) > v) v = fabs(t);
     }
+    return v;
+}
+
+/* Alg. 4 lines 6-7: lam += rho h; mu = (mu + rho g)_+ */
+void orc_al_update_multipliers(int32_t n_eq, double* lam, const double* h, int32_t n_in,
+                               double* mu, const double* g, double rho)
+{
+    for (int32_t k = 0; k < n_eq; ++k) lam[k] = lam[k] + rho * h[k];
+    for (int32_t k = 0; k < n_in; ++k) {
+        const double t = mu[k] + rho * g[k];
+        mu[k] = t > 0.0 ? t : 0.0;
+    }
+}
+
+/* Penalty rule ("If the infinity norm of the constraint violation
+ * is not halved in an iteration, then rho is multiplied by a factor of 2";
+ * reading R20): rho * factor if v > v_prev / 2, else rho; capped at cap. */
+double orc_al_update_rho(double rho, double vprev, double v, double factor, double cap)
+{
+    if (v > 0.5 * vprev) {
+        rho = rho * factor;
+        if (rho > cap) rho = cap;
+    }
+    return rho;
+}
+
+static double viol_inf(const orc_lsq* P, const double* x, const double* mu, double rho)
+{
+    double* hval = cons_buf(P->n_eq);
+    double* gval = cons_buf(P->n_in);
+    lsq_cons(P, x, hval, gval);
+    const double v = orc_al_violation(P->n_eq, hval, P->n_in, gval, mu, rho);
     free(hval); free(gval);
     return v;
 }
 
-/* P->lam, P->mu are read AND updated in place (they must point at writable
+/* Alg. 4 with an optional warm start and an optional per-outer trace.
+ * warm = 0: x^0 = clip(0), lam = 0, mu = 0 (Alg. 4 line 3, R19);
+ * warm = 1: x, lam_io, mu_io are taken as given (x clipped) -- re-entering
+ *           the method with the multipliers of an earlier run.
+ * trace (NULL or max_outer records of 3 + n_eq + n_in + nvars doubles):
+ *   [rho used by the inner solve, v after the update, rho after the rule,
+ *    lam (n_eq), mu (n_in), x (nvars)].
+ * P->lam, P->mu are read AND updated in place (they must point at writable
  * arrays, cast away const by the caller-owned buffers lam_io / mu_io). */
-void orc_al_solve(orc_lsq* P, double* lam_io, double* mu_io, const double* l, const double* u,
-                  int32_t m_hist, const orc_opts* o, const orc_al_opts* ao, double* x,
-                  orc_al_result* res)
+void orc_al_solve_ex(orc_lsq* P, double* lam_io, double* mu_io, const double* l, const double* u,
+                     int32_t m_hist, const orc_opts* o, const orc_al_opts* ao, double* x,
+                     int32_t warm, double* trace, orc_al_result* res)
 {
     const int64_t nv = lsq_nvars(P);
+    const int64_t rec = 3 + P->n_eq + P->n_in + nv;
     memset(res, 0, sizeof(*res));
-    for (int64_t j = 0; j < nv; ++j) x[j] = 0.0;                   /* x^0 = 0 (R19) */
+    if (!warm) {
+        for (int64_t j = 0; j < nv; ++j) x[j] = 0.0;               /* x^0 = 0 (R19) */
+        for (int32_t k = 0; k < P->n_eq; ++k) lam_io[k] = 0.0;
+        for (int32_t k = 0; k < P->n_in; ++k) mu_io[k] = 0.0;
+    }
     orc_clip(nv, x, l, u, x);
-    for (int32_t k = 0; k < P->n_eq; ++k) lam_io[k] = 0.0;
-    for (int32_t k = 0; k < P->n_in; ++k) mu_io[k] = 0.0;
     P->lam = lam_io; P->mu = mu_io;
     double rho = ao->rho0;
     double vprev = viol_inf(P, x, mu_io, rho);
@@ -675,18 +729,19 @@ void orc_al_solve(orc_lsq* P, double* lam_io, double* mu_io, const double* l, co
         double* hval = cons_buf(P->n_eq);
         double* gval = cons_buf(P->n_in);
         lsq_cons(P, x, hval, gval);
-        for (int32_t k = 0; k < P->n_eq; ++k) lam_io[k] = lam_io[k] + rho * hval[k];  /* line 6 */
-        for (int32_t k = 0; k < P->n_in; ++k) {                                        /* line 7 */
-            const double t = mu_io[k] + rho * gval[k];
-            mu_io[k] = t > 0.0 ? t : 0.0;
-        }
+        orc_al_update_multipliers(P->n_eq, lam_io, hval, P->n_in, mu_io, gval, rho);  /* lines 6-7 */
         free(hval); free(gval);
         const double v = viol_inf(P, x, mu_io, rho);
-        if (v > 0.5 * vprev) {                                      /* line 8, R20 */
-            rho = rho * ao->rho_factor;
-            if (rho > ao->rho_cap) rho = ao->rho_cap;
-        }
+        const double rho_used = rho;
+        rho = orc_al_update_rho(rho, vprev, v, ao->rho_factor, ao->rho_cap);          /* line 8, R20 */
         vprev = v;
+        if (trace) {
+            double* t = trace + (int64_t)it * rec;
+            t[0] = rho_used; t[1] = v; t[2] = rho;
+            for (int32_t k = 0; k < P->n_eq; ++k) t[3 + k] = lam_io[k];
+            for (int32_t k = 0; k < P->n_in; ++k) t[3 + P->n_eq + k] = mu_io[k];
+            for (int64_t j = 0; j < nv; ++j) t[3 + P->n_eq + P->n_in + j] = x[j];
+        }
         if (ir.status == ORC_CONVERGED && v <= ao->feas_tol && oi.tol == o->tol) {
             res->status = ORC_CONVERGED;
             break;
@@ -702,6 +757,13 @@ void orc_al_solve(orc_lsq* P, double* lam_io, double* mu_io, const double* l, co
     }
     res->violation_inf = viol_inf(P, x, mu_io, rho);
     res->rho = rho;
+}
+
+void orc_al_solve(orc_lsq* P, double* lam_io, double* mu_io, const double* l, const double* u,
+                  int32_t m_hist, const orc_opts* o, const orc_al_opts* ao, double* x,
+                  orc_al_result* res)
+{
+    orc_al_solve_ex(P, lam_io, mu_io, l, u, m_hist, o, ao, x, 0, NULL, res);
 }
 
 /* Elementary helpers exposed for the pins (SPEC-style worked examples). */
