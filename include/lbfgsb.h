@@ -181,6 +181,32 @@ lbfgsb_err lbfgsb_p2p_open(lbfgsb_t* h, const void* handles);
  * device.  Errors: ARG, DIM, OOM. */
 lbfgsb_err lbfgsb_p2p_connect_local(lbfgsb_t* const* hs, int32_t nranks, int64_t m_max);
 
+/* SURVEY 8(e) bitwise P-invariance ("fixed C chunks, independent of P"):
+ * the n global variables are cut into C = nranks fixed column chunks, each a
+ * LOGICAL rank (an lbfgsb_create_sharded_p2p handle with rank = chunk index,
+ * nranks = C), and a process hosts any subset of them (C/P on each of P
+ * GPUs).  lbfgsb_p2p_open_group wires the n_local handles a process hosts
+ * to all C mailboxes: the local ones directly, the others through CUDA IPC
+ * (handles: host, C x 64 bytes in logical-rank order, e.g. all-gathered
+ * from lbfgsb_p2p_ipc_handle; each remote mailbox is mapped once per
+ * process and the mapping is owned by hs[0] -- destroy the group's handles
+ * together).  Errors: ARG (not P2P handles of one group, a logical rank
+ * hosted twice), CUDA. */
+lbfgsb_err lbfgsb_p2p_open_group(lbfgsb_t* const* hs, int32_t n_local, const void* handles);
+
+/* Solve one P2P-sharded problem over the n_local logical ranks this process
+ * hosts (Alg. 1; objs[p] = the LSQ objective of hs[p]'s
+ * chunk with the replicated b, xs[p] its DEVICE variable block, in x0 /
+ * out x*).  Each logical rank runs with the kernel geometry of its own
+ * chunk, and every decision reduces the C packs in logical-rank order, so x,
+ * f and the iteration count are BITWISE independent of how the C chunks are
+ * spread over processes and GPUs (P = 1, 2, 4, 8 for C = 8).  All launches
+ * go to hs[0]'s stream (one CUDA graph per check interval).  res (host)
+ * receives the global result.  Errors: ARG (handles not of one connected P2P
+ * group), DIM, CUDA, NCCL (a peer stopped signalling for 60 s). */
+lbfgsb_err lbfgsb_solve_group(lbfgsb_t* const* hs, const lbfgsb_objective* const* objs,
+                              double* const* xs, int32_t n_local, double tol, lbfgsb_result* res);
+
 void lbfgsb_destroy(lbfgsb_t* h);
 
 /* ---- objectives --------------------------------------------------------- */
@@ -276,7 +302,9 @@ lbfgsb_err lbfgsb_solve_lsq_host_batch(lbfgsb_t* h, int32_t count, const double*
  * results (seconds = the whole call).  opts as lbfgsb_create (NULL =
  * defaults; check_every / use_graph / profile / armijo_diff unused); tol
  * overrides opts.tol when > 0.  Synchronous on cuda_stream (NULL = legacy).
- * Errors: ARG, DIM (batch < 0, shape too large for one CTA), CUDA. */
+ * Errors: ARG (NULL pointer, option values outside the ranges lbfgsb_create
+ * accepts, tol < 0 or NaN), DIM (batch < 0, shape too large for one CTA),
+ * BOUNDS (some l_i > u_i or a NaN bound), CUDA. */
 lbfgsb_err lbfgsb_solve_batched_lsq(int32_t batch, int64_t m, int64_t n, const double* M, const double* b,
                                     const double* lower, const double* upper, double* x, int32_t m_hist,
                                     const lbfgsb_opts* opts, double tol, void* cuda_stream,

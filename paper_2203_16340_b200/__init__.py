@@ -20,7 +20,8 @@ from . import _build
 __all__ = ["Options", "ALOptions", "Result", "ALResult", "Solver", "LSQObjective",
            "CallbackObjective", "op_gemv", "op_gemvt", "load", "LbfgsbError", "colmajor",
            "solve_loopback", "nccl_unique_id", "QPObjective", "op_gaussian_kernel",
-           "TransportObjective", "solve_batched_lsq", "colmajor_batch", "p2p_connect_local"]
+           "TransportObjective", "solve_batched_lsq", "colmajor_batch", "p2p_connect_local",
+           "p2p_open_group", "solve_group"]
 
 _c_d, _c_i32, _c_i64, _c_vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
 
@@ -109,6 +110,9 @@ def load(build_if_needed: bool = True):
     L.lbfgsb_p2p_ipc_handle.argtypes = [vp, vp]
     L.lbfgsb_p2p_open.argtypes = [vp, vp]
     L.lbfgsb_p2p_connect_local.argtypes = [C.POINTER(vp), _c_i32, _c_i64]
+    L.lbfgsb_p2p_open_group.argtypes = [C.POINTER(vp), _c_i32, vp]
+    L.lbfgsb_solve_group.argtypes = [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), _c_i32, _c_d,
+                                     C.POINTER(_Res)]
     L.lbfgsb_solve_lsq_host_batch.argtypes = [vp, _c_i32, C.POINTER(vp), _c_i64, _c_i64, C.POINTER(vp),
                                               C.POINTER(vp), _c_d, C.POINTER(_Res)]
     L.lbfgsb_objective_qp.argtypes = [vp, _c_i64, _c_i64, vp, vp, _c_d, C.POINTER(vp)]
@@ -128,6 +132,7 @@ def load(build_if_needed: bool = True):
                  "lbfgsb_profile_get", "lbfgsb_solve_loopback", "lbfgsb_nccl_unique_id",
                  "lbfgsb_objective_qp", "lbfgsb_op_gaussian_kernel", "lbfgsb_create_sharded_p2p",
                  "lbfgsb_p2p_ipc_handle", "lbfgsb_p2p_open", "lbfgsb_p2p_connect_local",
+                 "lbfgsb_p2p_open_group", "lbfgsb_solve_group",
                  "lbfgsb_solve_lsq_host_batch"):
         getattr(L, name).restype = _c_i32
     _lib = L
@@ -544,6 +549,28 @@ def p2p_connect_local(solvers, m_max):
     R = len(solvers)
     hs = (_c_vp * R)(*[s._h.value for s in solvers])
     _check(load().lbfgsb_p2p_connect_local(hs, R, int(m_max)))
+
+
+def p2p_open_group(solvers, handles):
+    """lbfgsb_p2p_open_group: wire the logical ranks this process hosts
+    (P2P-sharded Solvers) to all C mailboxes (``handles``: the 64-byte IPC
+    handles of every logical rank, in logical-rank order)."""
+    R = len(solvers)
+    hs = (_c_vp * R)(*[s._h.value for s in solvers])
+    blob = b"".join(handles)
+    _check(load().lbfgsb_p2p_open_group(hs, R, C.cast(C.create_string_buffer(blob, len(blob)), C.c_void_p)))
+
+
+def solve_group(solvers, objs, xs, tol=0.0) -> Result:
+    """lbfgsb_solve_group: one P2P-sharded solve over the logical ranks this
+    process hosts (bitwise independent of the process / GPU count)."""
+    R = len(solvers)
+    hs = (_c_vp * R)(*[s._h.value for s in solvers])
+    os_ = (_c_vp * R)(*[o._h.value for o in objs])
+    xp = (_c_vp * R)(*[x.data_ptr() for x in xs])
+    r = _Res()
+    _check(load().lbfgsb_solve_group(hs, os_, xp, R, float(tol), C.byref(r)))
+    return Result.from_c(r)
 
 
 def solve_loopback(solvers, objs, xs, tol=0.0) -> Result:

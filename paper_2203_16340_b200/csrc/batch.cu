@@ -188,11 +188,17 @@ __global__ void __launch_bounds__(BT) k_batch(BatchArgs B)
             if (tid == 0) { res4[3] = a3; dir_decide(P, C, res4, 0); }
             __syncthreads();
         }
-        if (C->stall == ST_FALLBACK || C->done) {
-            if (C->done) break;
-            if (tid == 0) { C->stall = 0; C->fallback = 1; C->nh = 0; C->n_fallbacks += 1; C->coef[0] = -1.0; }
+        {
+            // every thread reads the flags BEFORE thread 0 may reset them (the barrier
+            // between the reads and the reset keeps all warps on the same path)
+            const int st = C->stall, dn = C->done;
             __syncthreads();
-            continue;
+            if (dn) break;
+            if (st == ST_FALLBACK) {
+                if (tid == 0) { C->stall = 0; C->fallback = 1; C->nh = 0; C->n_fallbacks += 1; C->coef[0] = -1.0; }
+                __syncthreads();
+                continue;
+            }
         }
         const double* pv = C->branch ? pp : pt;
         // ---- q = A p over the active columns
@@ -228,18 +234,24 @@ __global__ void __launch_bounds__(BT) k_batch(BatchArgs B)
                 armijo_decide(P, C, quad, nullptr);
             }
             __syncthreads();
-            if (C->stall == ST_LS_CONT) {
+            const int st = C->stall;
+            __syncthreads();                                     // all reads before the reset
+            if (st == ST_LS_CONT) {
                 if (tid == 0) C->stall = 0;
                 __syncthreads();
                 continue;
             }
             break;
         }
-        if (C->done) break;
-        if (C->stall == ST_FALLBACK) {
-            if (tid == 0) { C->stall = 0; C->fallback = 1; C->nh = 0; C->n_fallbacks += 1; C->coef[0] = -1.0; }
+        {
+            const int st = C->stall, dn = C->done;
             __syncthreads();
-            continue;
+            if (dn) break;
+            if (st == ST_FALLBACK) {
+                if (tid == 0) { C->stall = 0; C->fallback = 1; C->nh = 0; C->n_fallbacks += 1; C->coef[0] = -1.0; }
+                __syncthreads();
+                continue;
+            }
         }
         // ---- step (Alg. 1 line 7), r' = fma(alpha, q, r), g', s, y into the ring
         {

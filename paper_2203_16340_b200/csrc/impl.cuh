@@ -139,7 +139,7 @@ struct Prob {
     int rank_id;
     double* peer_mb[P2P_MAXR];          // mailbox base of every rank (own one included)
     unsigned long long* mb_hdr;         // own mailbox header: [4] section counters, [4] timeout flag
-    unsigned long long* p2p_tgt;        // [4] counts consumed so far (own device memory)
+    unsigned long long* p2p_tgt;        // [8] counts consumed so far per header slot (own device memory)
     // joint-probability / regularised OT objective (transport.cu):
     // x = vec(P), P tm x tn column-major; c = cost; delta (Gaussian) or ent
     // (entropy) weight; rbuf[rsel] holds the carried marginal residual
@@ -168,6 +168,7 @@ __host__ __device__ inline int64_t pk_len(const Prob& P) { return qs_len(P) + 4 
 // i.e. the four gathered sections in pack order; section sec starts at mb_off(P, sec)
 enum XSec : int { XS_QS = 0, XS_DIR = 1, XS_GRAM = 2, XS_KKT = 3 };
 constexpr int MB_HDR = 8;
+constexpr int MB_BARRIER = 5;              // header slot of the stall-path barrier counter (k_p2p_ack)
 __host__ __device__ inline int64_t mb_off(const Prob& P, int sec)
 {
     const int64_t R = P.nranks;
@@ -206,6 +207,7 @@ void launch_gram_decide(const Prob& P, cudaStream_t st, int bwd_mode);
 void launch_kkt_decide(const Prob& P, cudaStream_t st);
 // p2p.cu: exchange over peer memory (the producers push from their tails)
 void launch_p2p_put(const Prob& P, cudaStream_t st, int sec, int64_t off, int64_t cnt);
+void launch_p2p_barrier(const Prob* Ps, int n, cudaStream_t st);
 void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K, int64_t ldk,
                   cudaStream_t st);
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);

@@ -31,4 +31,31 @@ void launch_p2p_put(const Prob& P, cudaStream_t st, int sec, int64_t off, int64_
     k_p2p_put<<<1, NT, 0, st>>>(P, sec, off, cnt);
 }
 
+// Quiescence barrier of the host-driven stall paths (R14 fallback relaunch,
+// Armijo continuation).  Inside a replayed iteration a rank cannot push a
+// section again before every peer has read it (the next push follows a
+// consumption of a later section the peer sends only after reading), but a
+// relaunch decided on the host would re-push DIR / QS at once.  So before it
+// every rank first ACKs (its stream has finished every consumer kernel
+// launched so far) into every mailbox's barrier counter, then waits until
+// all ranks have ACKed: after the wait no rank still reads a slot the
+// relaunch overwrites.  Two kernels so that a loopback group on one stream
+// (all ranks' ACKs enqueued before any wait) cannot deadlock.
+__global__ void k_p2p_ack(Prob P)
+{
+    __threadfence_system();
+    p2p_signal(P, MB_BARRIER);
+}
+
+__global__ void k_p2p_wait_ack(Prob P)
+{
+    p2p_wait_take(P, MB_BARRIER, (unsigned long long)P.nranks);
+}
+
+void launch_p2p_barrier(const Prob* Ps, int n, cudaStream_t st)
+{
+    for (int i = 0; i < n; ++i) k_p2p_ack<<<1, 1, 0, st>>>(Ps[i]);
+    for (int i = 0; i < n; ++i) k_p2p_wait_ack<<<1, 1, 0, st>>>(Ps[i]);
+}
+
 }  // namespace lb

@@ -132,7 +132,7 @@ struct lbfgsb_t {
     // two slots (the double-buffered host-batch solve alternates between two
     // operator copies; any other use hits slot 0 again and again)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-    Prob gkey[2] = {};
+    std::vector<Prob> gkey[2];          // the Probs of every logical rank the graph launches
     int gchunk[2] = {0, 0};
     cudaStream_t gstream[2] = {nullptr, nullptr};
     int glast = 0;
@@ -208,7 +208,26 @@ __global__ void k_fill_bounds(double* l, double* u, const double* lin, const dou
         if (!(a <= b)) atomicExch(bad, 1);      // l > u or NaN
     }
 }
+
+// l <= u and no NaN, without copying (the batched entry point reads the caller's bounds)
+__global__ void k_check_bounds(const double* lin, const double* uin, int64_t n, int* bad)
+{
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double a = lin ? lin[j] : -INFINITY;
+        const double b = uin ? uin[j] : INFINITY;
+        if (!(a <= b)) atomicExch(bad, 1);
+    }
+}
 }  // namespace
+
+// option values every entry point accepts (eps > 0, 0 < c1 < 1, 0 < shrink < 1,
+// tol >= 0, max_backtracks >= 0, max_iters >= 0); NaN fails every test
+static bool opts_valid(const lbfgsb_opts& o)
+{
+    return (o.eps > 0) && (o.c1 > 0 && o.c1 < 1) && (o.shrink > 0 && o.shrink < 1) && (o.tol >= 0) &&
+           o.max_backtracks >= 0 && o.max_iters >= 0;
+}
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -247,9 +266,7 @@ static lbfgsb_err create_common(int64_t n, int32_t m_hist, const double* lower, 
     lbfgsb_opts o;
     lbfgsb_opts_default(&o);
     if (opts) o = *opts;
-    if (!(o.eps > 0) || !(o.c1 > 0 && o.c1 < 1) || !(o.shrink > 0 && o.shrink < 1) || !(o.tol >= 0) ||
-        o.max_backtracks < 0 || o.max_iters < 0)
-        return fail(LBFGSB_ERR_ARG, "invalid option value");
+    if (!opts_valid(o)) return fail(LBFGSB_ERR_ARG, "invalid option value");
     if (o.check_every < 1) o.check_every = 1;
     if (o.check_every > 64) o.check_every = 64;
     int ndev = 0;
@@ -762,8 +779,9 @@ static lbfgsb_err run_chunk(Group& g)
     if (graph) {
         int sl = -1;
         for (int k = 0; k < 2 && sl < 0; ++k)
-            if (h->gexec[k] && std::memcmp(&h->gkey[k], &g.Ps[0], sizeof(Prob)) == 0 && h->gchunk[k] == chunk &&
-                h->gstream[k] == g.st)
+            if (h->gexec[k] && h->gkey[k].size() == g.Ps.size() &&
+                std::memcmp(h->gkey[k].data(), g.Ps.data(), sizeof(Prob) * g.Ps.size()) == 0 &&
+                h->gchunk[k] == chunk && h->gstream[k] == g.st)
                 sl = k;
         if (sl < 0) {
             sl = h->gexec[0] == nullptr ? 0 : (h->gexec[1] == nullptr ? 1 : h->glast ^ 1);   // replace the LRU slot
@@ -780,7 +798,7 @@ static lbfgsb_err run_chunk(Group& g)
             e = cudaGraphInstantiate(&h->gexec[sl], gr, 0);
             cudaGraphDestroy(gr);
             if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-            h->gkey[sl] = g.Ps[0];
+            h->gkey[sl] = g.Ps;
             h->gchunk[sl] = chunk;
             h->gstream[sl] = g.st;
         }
@@ -869,6 +887,8 @@ static lbfgsb_err solve_group(Group& g, double* const* xs, double tol, lbfgsb_re
                 }
             }
             TRY(ctrl_to_dev(g));
+            // P2P: no rank may re-push DIR / QS while a peer still reads the previous pack
+            if (g.Ps[0].p2p) launch_p2p_barrier(g.Ps.data(), (int)g.Ps.size(), g.st);
             if (s == ST_FALLBACK) TRY(launch_iteration(g, -1));
             else TRY(launch_ls_cont(g));
             CK(cudaGetLastError());
@@ -1065,6 +1085,41 @@ extern "C" lbfgsb_err lbfgsb_solve_loopback(lbfgsb_t* const* hs, const lbfgsb_ob
         hs[p]->nranks = 1; hs[p]->sharded = false; hs[p]->rank = 0; hs[p]->n_global = hs[p]->n;
     }
     return e;
+}
+
+// SURVEY 8(e) bitwise P-invariance: a process hosts n_local LOGICAL ranks of a
+// P2P-sharded solve over C = nranks fixed column chunks (each handle made by
+// lbfgsb_create_sharded_p2p with its logical rank, mailboxes wired with
+// lbfgsb_p2p_open_group).  Every logical rank runs its kernels with the
+// geometry of its own chunk and every decision reduces the C packs in
+// logical-rank order, so the iterates do not depend on how the C chunks are
+// spread over processes / GPUs.  All launches go to hs[0]'s stream; the
+// iteration is captured as one CUDA graph over all local logical ranks.
+extern "C" lbfgsb_err lbfgsb_solve_group(lbfgsb_t* const* hs, const lbfgsb_objective* const* objs,
+                                         double* const* xs, int32_t n_local, double tol, lbfgsb_result* res)
+{
+    if (!hs || !objs || !xs || n_local < 1) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    Group g;
+    g.st = hs[0]->st;
+    g.sharded = true;
+    g.loopback = false;
+    g.Ps.resize(n_local);
+    for (int p = 0; p < n_local; ++p) {
+        if (!hs[p] || !objs[p] || !xs[p] || objs[p]->kind != 0) return fail(LBFGSB_ERR_ARG, "bad local rank %d", p);
+        if (!hs[p]->p2p || !hs[p]->sharded || hs[p]->nranks != hs[0]->nranks)
+            return fail(LBFGSB_ERR_ARG, "local rank %d: not a P2P-sharded handle of the same group", p);
+        for (int r = 0; r < hs[p]->nranks; ++r)
+            if (!hs[p]->peer_mb[r]) return fail(LBFGSB_ERR_ARG, "P2P exchange: rank %d not connected", r);
+        g.hs.push_back(hs[p]);
+        TRY(make_prob(hs[p], objs[p], g.Ps[p]));
+        if (objs[p]->m != objs[0]->m) return fail(LBFGSB_ERR_DIM, "ranks disagree on m");
+        set_sep(g.Ps[p]);
+        hs[p]->hc->rho = 1.0;
+        std::memset(hs[p]->hc->lam, 0, sizeof hs[p]->hc->lam);
+        std::memset(hs[p]->hc->rhs, 0, sizeof hs[p]->hc->rhs);
+    }
+    const double t = tol > 0 ? tol : hs[0]->o.tol;
+    return solve_group(g, xs, t, res);
 }
 
 extern "C" lbfgsb_err lbfgsb_solve_lsq_host(lbfgsb_t* h, const double* M_host, int64_t m, int64_t ncols,
@@ -1376,11 +1431,24 @@ extern "C" lbfgsb_err lbfgsb_solve_batched_lsq(int32_t batch, int64_t m, int64_t
     lbfgsb_opts o;
     lbfgsb_opts_default(&o);
     if (opts) o = *opts;
+    if (!opts_valid(o) || !(tol >= 0)) return fail(LBFGSB_ERR_ARG, "invalid option value");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(LBFGSB_ERR_CUDA, "no CUDA device available (the library has no CPU path)");
     init_kernels();
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (lower || upper) {                                   // l <= u, no NaN
+        int* bad = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), st));
+        CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+        k_check_bounds<<<256, 256, 0, st>>>(lower, upper, (int64_t)batch * n, bad);
+        CK(cudaGetLastError());
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(bad, st));
+        CK(cudaStreamSynchronize(st));
+        if (hbad) return fail(LBFGSB_ERR_BOUNDS, "l_i > u_i or NaN bound");
+    }
     lbfgsb_result* dres = nullptr;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&dres), sizeof(lbfgsb_result) * (size_t)batch, st));
     auto t0 = std::chrono::steady_clock::now();
@@ -1640,8 +1708,8 @@ static lbfgsb_err alloc_mailbox(lbfgsb_t* h, int nranks, int64_t m_max)
         h->mb = nullptr;
         return fail(LBFGSB_ERR_OOM, "mailbox cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
     }
-    TRY(h->p2p_tgt.ensure(sizeof(unsigned long long) * 4, true));
-    CK(cudaMemset(h->p2p_tgt.p, 0, sizeof(unsigned long long) * 4));
+    TRY(h->p2p_tgt.ensure(sizeof(unsigned long long) * MB_HDR, true));
+    CK(cudaMemset(h->p2p_tgt.p, 0, sizeof(unsigned long long) * MB_HDR));
     h->mb_mmax = m_max;
     h->mb_nranks = nranks;
     h->mb_bytes = bytes;
@@ -1696,6 +1764,47 @@ extern "C" lbfgsb_err lbfgsb_p2p_open(lbfgsb_t* h, const void* handles)
                                           cudaGetErrorString(e));
         h->peer_mb[r] = p;
         h->peer_ipc[r] = true;
+    }
+    return LBFGSB_OK;
+}
+
+// Wire the n_local handles a process hosts (logical ranks of one P2P group,
+// any subset of 0..nranks-1) to every mailbox: the local ones directly, the
+// others through CUDA IPC, each remote mailbox mapped ONCE per process (the
+// mapping is owned, and closed, by hs[0]; destroy the group's handles together).
+extern "C" lbfgsb_err lbfgsb_p2p_open_group(lbfgsb_t* const* hs, int32_t n_local, const void* handles)
+{
+    if (!hs || n_local < 1 || !handles) return fail(LBFGSB_ERR_ARG, "bad arguments");
+    const int R = hs[0]->nranks;
+    void* local[P2P_MAXR] = {};
+    for (int p = 0; p < n_local; ++p) {
+        if (!hs[p] || !hs[p]->p2p || !hs[p]->mb || hs[p]->nranks != R)
+            return fail(LBFGSB_ERR_ARG, "local rank %d: not a P2P handle of the group", p);
+        if (local[hs[p]->rank]) return fail(LBFGSB_ERR_ARG, "logical rank %d hosted twice", hs[p]->rank);
+        local[hs[p]->rank] = hs[p]->mb;
+    }
+    for (int p = 0; p < n_local; ++p)
+        for (int r = 0; r < R; ++r)
+            if (hs[p]->peer_ipc[r] && hs[p]->peer_mb[r]) {
+                cudaIpcCloseMemHandle(hs[p]->peer_mb[r]);
+                hs[p]->peer_ipc[r] = false;
+                hs[p]->peer_mb[r] = nullptr;
+            }
+    for (int r = 0; r < R; ++r) {
+        void* ptr = local[r];
+        bool ipc = false;
+        if (!ptr) {
+            cudaIpcMemHandle_t ih;
+            std::memcpy(&ih, static_cast<const char*>(handles) + 64 * (size_t)r, sizeof ih);
+            cudaError_t e = cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) return fail(LBFGSB_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", r,
+                                              cudaGetErrorString(e));
+            ipc = true;
+        }
+        for (int p = 0; p < n_local; ++p) {
+            hs[p]->peer_mb[r] = ptr;
+            hs[p]->peer_ipc[r] = ipc && p == 0;
+        }
     }
     return LBFGSB_OK;
 }

@@ -75,3 +75,63 @@ def make_sharded_solver(n_local, n_global, m_hist, lower, opts, stream, xchg="nc
     nid = broadcast_bytes(nid, src=0)
     return lb.Solver(n_local, m_hist, lower=lower, opts=opts, stream=stream, nccl_id=nid,
                      rank=rank, nranks=world, n_global=n_global)
+
+
+# --------------------------------------------------------------------------- P-invariant groups
+def local_chunks(nchunks: int, world: int, rank: int) -> list[int]:
+    """Logical ranks (fixed column chunks) hosted by process `rank` of `world`:
+    a contiguous block of nchunks // world (world must divide nchunks)."""
+    if nchunks % world:
+        raise ValueError(f"{world} processes cannot host {nchunks} chunks evenly")
+    k = nchunks // world
+    return list(range(rank * k, (rank + 1) * k))
+
+
+class ShardedGroup:
+    """SURVEY 8(e) bitwise P-invariance: the global problem is cut into
+    ``nchunks`` (C) fixed column chunks -- logical ranks, each a P2P-sharded
+    library handle -- independent of the number of processes; this process
+    hosts C / world of them (``local_chunks``).  The C mailboxes are wired
+    with lbfgsb_p2p_open_group (IPC handles all-gathered over
+    torch.distributed when world > 1) and one solve (lbfgsb_solve_group)
+    runs all local logical ranks on one stream.  x, f and the iteration count
+    do not depend on ``world``.
+
+    ``ranges[l]`` is the global column range [c0, c1) of logical rank l;
+    ``make_lower(l, c0, c1)`` returns its lower-bound tensor (or None)."""
+
+    def __init__(self, ncols: int, m_max: int, m_hist=5, nchunks=8, opts=None, stream=None,
+                 make_lower=None, make_upper=None, world=1, rank=0):
+        import paper_2203_16340_b200 as lb
+        self.ncols, self.nchunks, self.world, self.rank = ncols, nchunks, world, rank
+        self.ranges = [column_range(ncols, nchunks, l) for l in range(nchunks)]
+        self.local = local_chunks(nchunks, world, rank)
+        self.solvers = []
+        for l in self.local:
+            c0, c1 = self.ranges[l]
+            lo = make_lower(l, c0, c1) if make_lower else None
+            up = make_upper(l, c0, c1) if make_upper else None
+            self.solvers.append(lb.Solver(c1 - c0, m_hist, lower=lo, upper=up, opts=opts, stream=stream,
+                                          rank=l, nranks=nchunks, n_global=ncols, p2p_m_max=int(m_max)))
+        mine = {l: s.ipc_handle() for l, s in zip(self.local, self.solvers)}
+        if world > 1:
+            import pickle
+            import torch.distributed as dist
+            allh = {}
+            for blob in all_gather_bytes(pickle.dumps(mine)):
+                allh.update(pickle.loads(blob))
+        else:
+            allh = mine
+        handles = [allh.get(l, bytes(64)) for l in range(nchunks)]
+        lb.p2p_open_group(self.solvers, handles)
+        if world > 1:
+            dist.barrier()                 # every mailbox mapped before anyone signals
+
+    def solve(self, objs, xs, tol=0.0):
+        import paper_2203_16340_b200 as lb
+        return lb.solve_group(self.solvers, objs, xs, tol)
+
+    def close(self):
+        for s in reversed(self.solvers):   # hs[0] owns the IPC mappings: close it last
+            s.close()
+        self.solvers = []

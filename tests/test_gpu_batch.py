@@ -77,3 +77,74 @@ def test_batched_empty_and_stationary(lb):
                                lower=torch.zeros(3, 4, dtype=torch.float64, device="cuda"))
     assert all(r.status == lb.CONVERGED and r.iters == 0 for r in res)
     assert torch.all(x == 0)
+
+
+def _scaled(B, m, n, seed0, scale):
+    import synth
+    probs = [synth.nnls_gaussian(m, n, seed0 + k) for k in range(B)]
+    for p in probs:
+        p.M = p.M * scale
+        p.b = p.b * scale
+    return probs
+
+
+def test_batched_long_backtracking_vs_oracle(lb, orc):
+    """A badly scaled A (x1000) needs > 16 Armijo trials in its first
+    iteration, so the batched kernel goes through its LS_CONT continuation
+    (a second batch of trials) -- the stall path of ADVICE r1; results must
+    still match the oracle."""
+    probs = _scaled(6, 60, 30, 5, 1000.0)
+    A = np.stack([p.M for p in probs]); b = np.stack([p.b for p in probs])
+    x = torch.zeros(6, 30, dtype=torch.float64, device="cuda")
+    res = lb.solve_batched_lsq(lb.colmajor_batch(A), torch.from_numpy(b).cuda(), x,
+                               lower=torch.zeros(6, 30, dtype=torch.float64, device="cuda"))
+    for k, p in enumerate(probs):
+        first = orc.minimize_lsq(orc.LSQ(p.M, b=p.b), l=p.lower, opts=orc.Options(max_iters=1))
+        assert first.n_backtracks > 16                # the first search alone needs > 16 trials
+        ro = orc.minimize_lsq(orc.LSQ(p.M, b=p.b), l=p.lower)
+        r = res[k]
+        assert r.status == ro.status == lb.CONVERGED, (k, r)
+        assert r.n_backtracks > 16
+        assert abs(r.f - ro.f) <= 1e-8 * abs(ro.f), (k, r.f, ro.f)
+
+
+def test_batched_fallback_then_failure_vs_oracle(lb, orc):
+    """max_backtracks = 10 on a x30-scaled problem: the L-BFGS search fails,
+    the R14 fallback (empty ring, steepest descent) runs, and eventually the
+    search fails twice -> LINESEARCH_FAILURE, as in the oracle.  Exercises the
+    batched kernel's FALLBACK stall path."""
+    probs = _scaled(4, 60, 30, 5, 30.0)
+    A = np.stack([p.M for p in probs]); b = np.stack([p.b for p in probs])
+    x = torch.zeros(4, 30, dtype=torch.float64, device="cuda")
+    o = lb.Options(max_backtracks=10)
+    res = lb.solve_batched_lsq(lb.colmajor_batch(A), torch.from_numpy(b).cuda(), x,
+                               lower=torch.zeros(4, 30, dtype=torch.float64, device="cuda"), opts=o)
+    nfb = 0
+    for k, p in enumerate(probs):
+        ro = orc.minimize_lsq(orc.LSQ(p.M, b=p.b), l=p.lower, opts=orc.Options(max_backtracks=10))
+        r = res[k]
+        assert r.status == ro.status, (k, r, ro.status)
+        f0 = 0.5 * float(p.b @ p.b)
+        assert r.f <= f0                              # Theorem 1: monotone from x^0 = 0
+        nfb += r.n_fallbacks
+        if ro.n_fallbacks:
+            assert r.n_fallbacks >= 1
+    assert nfb >= 1
+
+
+def test_batched_rejects_bad_options_and_bounds(lb):
+    A = np.stack([np.eye(4)] * 2); b = np.ones((2, 4))
+    M = lb.colmajor_batch(A); bd = torch.from_numpy(b).cuda()
+    x = torch.zeros(2, 4, dtype=torch.float64, device="cuda")
+    with pytest.raises(lb.LbfgsbError):
+        lb.solve_batched_lsq(M, bd, x, opts=lb.Options(c1=1.5))
+    with pytest.raises(lb.LbfgsbError):
+        lb.solve_batched_lsq(M, bd, x, opts=lb.Options(eps=-1.0))
+    lo = torch.zeros(2, 4, dtype=torch.float64, device="cuda")
+    up = torch.zeros(2, 4, dtype=torch.float64, device="cuda")
+    up[1, 2] = -1.0                                   # l > u
+    with pytest.raises(lb.LbfgsbError):
+        lb.solve_batched_lsq(M, bd, x, lower=lo, upper=up)
+    up[1, 2] = float("nan")
+    with pytest.raises(lb.LbfgsbError):
+        lb.solve_batched_lsq(M, bd, x, lower=lo, upper=up)

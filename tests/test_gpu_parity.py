@@ -34,7 +34,8 @@ def _gemv_bound(A, p):
 
 
 # ------------------------------------------------------------------ a1 / a3 GEMVs
-@pytest.mark.parametrize("m,n", [(200, 100), (1037, 77), (2050, 1500), (513, 8), (1, 5), (7000, 333)])
+@pytest.mark.parametrize("m,n", [(200, 100), (1037, 77), (2050, 1500), (513, 8), (1, 5), (7000, 333),
+                                 (30000, 64), (100000, 40), (30001, 37)])
 def test_gemv_parity(lb, orc, m, n):
     rng = np.random.default_rng(m * 7 + n)
     A = rng.standard_normal((m, n))
@@ -47,7 +48,8 @@ def test_gemv_parity(lb, orc, m, n):
     assert np.all(np.abs(q.cpu().numpy() - ref) <= 1e-12 * _gemv_bound(A, p) + 1e-300)
 
 
-@pytest.mark.parametrize("m,n", [(200, 100), (1037, 77), (2050, 1500), (513, 8), (1, 5), (7000, 333)])
+@pytest.mark.parametrize("m,n", [(200, 100), (1037, 77), (2050, 1500), (513, 8), (1, 5), (7000, 333),
+                                 (30000, 64), (100000, 40), (30001, 37)])
 def test_gemvt_parity(lb, orc, m, n):
     rng = np.random.default_rng(m * 11 + n)
     A = rng.standard_normal((m, n))
@@ -215,6 +217,35 @@ def test_nnls_first_iterations_match_oracle(lb, orc):
                                oopts=orc.Options(max_iters=k, tol=1e-12))
         assert r.iters == ro.iters == k
         assert abs(r.f - ro.f) <= 1e-12 * abs(ro.f)
+
+
+def test_nnls_first_iterations_match_oracle_kbwd_s(lb, orc):
+    """Trajectory parity on the C2 kernels (m = 4000 >= 2048: k_bwd_s, the
+    long-column k_fwd): after k = 1..4 iterations f agrees to 1e-12 and x to
+    1e-10 of its magnitude (the same decisions step by step)."""
+    import synth
+    prob = synth.nnls_gaussian(4000, 2000, 22)
+    for k in range(1, 5):
+        r, ro, x = _solve_both(lb, orc, prob, opts=lb.Options(max_iters=k, tol=1e-12),
+                               oopts=orc.Options(max_iters=k, tol=1e-12))
+        assert r.iters == ro.iters == k
+        assert abs(r.f - ro.f) <= 1e-12 * abs(ro.f)
+        xo = orc.minimize_lsq(orc.LSQ(prob.M, b=prob.b), l=prob.lower,
+                              opts=orc.Options(max_iters=k, tol=1e-12)).x
+        assert np.max(np.abs(x - xo)) <= 1e-10 * max(np.max(np.abs(xo)), 1e-300)
+
+
+@pytest.mark.parametrize("m,n,seed", [(40000, 2000, 41), (30001, 1203, 42)])
+def test_nnls_end_to_end_tall(lb, orc, m, n, seed):
+    """C5-shaped columns (m >= 30000: the generic persistent k_bwd and the tall
+    k_fwd geometry) end to end against the oracle."""
+    import synth
+    prob = synth.nnls_gaussian(m, n, seed)
+    r, ro, x = _solve_both(lb, orc, prob)
+    assert r.status == lb.CONVERGED and ro.status == orc.CONVERGED
+    assert r.pg_inf <= 1e-6 and ro.pg_inf <= 1e-6
+    assert abs(r.f - ro.f) <= 1e-8 * abs(ro.f)
+    assert np.all(x >= 0.0)
 
 
 def test_determinism_graph_vs_eager(lb):
