@@ -28,7 +28,7 @@ CONVERGED, MAX_ITERS, LINESEARCH_FAILURE, AL_MAX_OUTER, AL_INNER_FAILURE = 0, 1,
 def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (no GPU needed)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
                _SRC, "-o", _LIB + ".tmp", "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)
@@ -71,7 +71,7 @@ def build_variant(out_path, replacements):
     cpath = out_path + ".c"
     with open(cpath, "w") as f:
         f.write(src)
-    subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
                            cpath, "-o", out_path, "-lm"])
     return out_path
 
@@ -131,6 +131,8 @@ def _setup(L):
     L.orc_masked_dot.restype = d
     L.orc_matvec.argtypes = [i64, i64, _dp, i64, _dp, _dp]
     L.orc_matvec_t.argtypes = [i64, i64, _dp, i64, _dp, _dp]
+    L.orc_set_threads.argtypes = [i32]
+    L.orc_get_threads.restype = i32
     L.orc_two_loop.argtypes = [i64, _dp, _u8p, i32, _dp, _dp, d, i32, _dp]
     L.orc_project_direction.argtypes = [i64, _dp, _dp, _dp, _dp, _dp, d, _dp]
     L.orc_project_direction.restype = i32
@@ -208,6 +210,16 @@ def masked_dot(u, v, free=None):
     fr = None if free is None else _u8(free)
     return _L().orc_masked_dot(u.size, _ptr(u), _ptr(v),
                                None if fr is None else fr.ctypes.data_as(_u8p))
+
+
+def set_threads(t: int):
+    """Threads of the oracle's matvecs (OpenMP over output elements only: the
+    results are bit-identical to 1 thread).  Default 1."""
+    _L().orc_set_threads(int(t))
+
+
+def get_threads() -> int:
+    return int(_L().orc_get_threads())
 
 
 def matvec(A, x):

@@ -73,20 +73,37 @@ double orc_masked_dot(int64_t n, const double* u, const double* v, const uint8_t
     return s;
 }
 
-/* out = A x   (A m x n column-major), loop order: for j, for i. */
+/* Thread count of the matvecs ("an OpenMP variant parallelizes
+ * over output elements only, with the same per-output summation order, so it
+ * is bit-identical to the 1-thread oracle").  Default 1: the oracle as it
+ * stands; bench.py's cpu_baseline also reports the all-cores figure. */
+static int g_threads = 1;
+void orc_set_threads(int32_t t) { g_threads = t > 0 ? t : 1; }
+int32_t orc_get_threads(void) { return g_threads; }
+
+/* out = A x   (A m x n column-major): out_i = sum_j A_ij x_j in increasing j
+ * (loop order: for j, for i).  With threads > 1 each thread owns a block of
+ * rows and runs the same j-then-i loops on it: every out_i sees the same
+ * additions in the same order. */
 void orc_matvec(int64_t m, int64_t n, const double* A, int64_t lda, const double* x, double* out)
 {
-    for (int64_t i = 0; i < m; ++i) out[i] = 0.0;
-    for (int64_t j = 0; j < n; ++j) {
-        const double xj = x[j];
-        const double* a = A + j * lda;
-        for (int64_t i = 0; i < m; ++i) out[i] += a[i] * xj;
+    const int64_t T = g_threads;
+#pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
+    for (int64_t t = 0; t < T; ++t) {
+        const int64_t i0 = t * m / T, i1 = (t + 1) * m / T;
+        for (int64_t i = i0; i < i1; ++i) out[i] = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            const double xj = x[j];
+            const double* a = A + j * lda;
+            for (int64_t i = i0; i < i1; ++i) out[i] += a[i] * xj;
+        }
     }
 }
 
-/* out = A^T r, out_j = sum_i A_ij r_i in increasing i. */
+/* out = A^T r, out_j = sum_i A_ij r_i in increasing i (threads: over j). */
 void orc_matvec_t(int64_t m, int64_t n, const double* A, int64_t lda, const double* r, double* out)
 {
+#pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1)
     for (int64_t j = 0; j < n; ++j) {
         const double* a = A + j * lda;
         double s = 0.0;

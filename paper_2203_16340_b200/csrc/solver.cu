@@ -896,7 +896,7 @@ static lbfgsb_err solve_group(Group& g, double* const* xs, double tol, lbfgsb_re
         }
     }
     const Ctrl fin = *h->hc;
-    h->nact_total += fin.nact;
+    for (auto* hh : g.hs) h->nact_total += hh->hc->nact;     // active columns read by every local k_fwd
     TRY(launch_refresh(g));
     CK(cudaGetLastError());
     TRY(ctrl_to_host(g));

@@ -203,6 +203,53 @@ def c5_device(m: int = 100000, n: int = 200000, seed: int = 5, col0: int = 0, nc
     return At.T, b, xp
 
 
+def c5_planted(m: int = 100000, n: int = 200000, seed: int = 5):
+    """The host-side draws of C5 (x_plant: 10% nonzeros |N(0,1)|, noise z), as in c5_device."""
+    rng = np.random.default_rng(seed)
+    xp = np.zeros(n)
+    nz = rng.random(n) < 0.1
+    xp[nz] = np.abs(rng.standard_normal(int(nz.sum())))
+    z = rng.standard_normal(m)
+    return xp, z
+
+
+def c5_block(m: int, col0: int, ncols: int, seed: int = 5, out=None, stream=None):
+    """Columns [col0, col0+ncols) of the C5 matrix, generated on the device
+    (Philox; bit-identical to synth.philox.centered_block) into a fresh or
+    given (ncols, m) row-major tensor = (m, ncols) column-major.  Returns the
+    (m, ncols) column-major view."""
+    import torch
+    L = _gen_lib()
+    scale = float(np.sqrt(12.0 / m))
+    At = torch.empty((ncols, m), dtype=torch.float64, device="cuda") if out is None else out
+    st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    rc = L.synth_fill_centered(At.data_ptr(), m, ncols, m, col0, seed, 0, scale, st)
+    if rc != 0:
+        raise RuntimeError(f"synth_fill_centered failed: {rc}")
+    return At.T
+
+
+def c5_rhs(m: int = 100000, n: int = 200000, seed: int = 5, b_chunk: int = 2048):
+    """b = A x_plant + 0.1 z of C5 over ALL n columns (the replicated right-hand
+    side; same arithmetic as c5_device, so the same bits)."""
+    import torch
+    L = _gen_lib()
+    xp, z = c5_planted(m, n, seed)
+    scale = float(np.sqrt(12.0 / m))
+    st = torch.cuda.current_stream().cuda_stream
+    bt = torch.zeros(m, dtype=torch.float64, device="cuda")
+    tmp = torch.empty((b_chunk, m), dtype=torch.float64, device="cuda")
+    for c0 in range(0, n, b_chunk):
+        k = min(b_chunk, n - c0)
+        xs = xp[c0:c0 + k]
+        if not np.any(xs):
+            continue
+        L.synth_fill_centered(tmp.data_ptr(), m, k, m, c0, seed, 0, scale, st)
+        bt += tmp[:k].T @ torch.from_numpy(xs).to("cuda")
+    del tmp
+    return bt.cpu().numpy() + 0.1 * z
+
+
 def blobs(N: int, d: int, seed: int, sep: float = 2.0, scale: float = 1.0):
     """Two Gaussian blobs, labels +-1 balanced: x_i ~ scale * N(y_i sep/sqrt(d) 1, I_d).
     scale = 1/sqrt(d) gives ||x_i - x_j||^2 ~ 2 (LibSVM-like feature scaling, so a

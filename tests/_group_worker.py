@@ -5,7 +5,7 @@ Runs standalone (world = 1) or under torch.distributed.run (gloo bootstrap;
 every process may sit on the same GPU).  Rank 0 writes the gathered x, f,
 iterations and status to argv[1] (.npz).
 
-argv: out m n seed kind(gauss|c5) nchunks use_graph scale max_backtracks"""
+argv: out m n seed kind(gauss|c5) nchunks use_graph scale max_backtracks tol"""
 import os
 import pickle
 import sys
@@ -17,7 +17,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 
-def main(out, m, n, seed, kind, nchunks, use_graph, scale, max_bt):
+def main(out, m, n, seed, kind, nchunks, use_graph, scale, max_bt, tol):
     import paper_2203_16340_b200 as lb
     import synth
     from paper_2203_16340_b200.sharded import ShardedGroup
@@ -28,7 +28,7 @@ def main(out, m, n, seed, kind, nchunks, use_graph, scale, max_bt):
         dist.init_process_group("gloo")
     ngpu = torch.cuda.device_count()
     torch.cuda.set_device(rank % ngpu)
-    opts = lb.Options(use_graph=bool(use_graph), max_backtracks=max_bt)
+    opts = lb.Options(use_graph=bool(use_graph), max_backtracks=max_bt, tol=tol)
     grp = ShardedGroup(n, m, nchunks=nchunks, opts=opts, world=world, rank=rank,
                        make_lower=lambda l, c0, c1: torch.zeros(c1 - c0, dtype=torch.float64, device="cuda"))
     objs, xs, keep = [], [], []
@@ -67,4 +67,4 @@ def main(out, m, n, seed, kind, nchunks, use_graph, scale, max_bt):
 
 if __name__ == "__main__":
     a = sys.argv[1:]
-    main(a[0], int(a[1]), int(a[2]), int(a[3]), a[4], int(a[5]), int(a[6]), float(a[7]), int(a[8]))
+    main(a[0], int(a[1]), int(a[2]), int(a[3]), a[4], int(a[5]), int(a[6]), float(a[7]), int(a[8]), float(a[9]))

@@ -276,3 +276,25 @@ def check_armijo_lsq_random(orc, n_cases=60):
 
 def test_armijo_lsq_random_exact(orc):
     check_armijo_lsq_random(orc)
+
+
+# ---------------------------------------------------------------- OpenMP variant
+def test_threaded_oracle_is_bit_identical(orc):
+    """the all-cores oracle (OpenMP over output elements, same
+    per-output summation order) gives the 1-thread oracle's bits: matvecs with
+    ragged row blocks, and a whole NNLS solve."""
+    import synth
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((1003, 357)); x = rng.standard_normal(357); r = rng.standard_normal(1003)
+    prob = synth.nnls_gaussian(700, 300, 12)
+    try:
+        orc.set_threads(1)
+        q1, g1 = orc.matvec(A, x), orc.matvec_t(A, r)
+        s1 = orc.minimize_lsq(orc.LSQ(prob.M, b=prob.b), l=prob.lower)
+        for t in (2, 3, 7):
+            orc.set_threads(t)
+            assert np.array_equal(orc.matvec(A, x), q1) and np.array_equal(orc.matvec_t(A, r), g1)
+            st = orc.minimize_lsq(orc.LSQ(prob.M, b=prob.b), l=prob.lower)
+            assert np.array_equal(st.x, s1.x) and st.f == s1.f and st.iters == s1.iters
+    finally:
+        orc.set_threads(1)

@@ -110,3 +110,18 @@ def test_make_sharded_solver_argument_checks():
             sharded.make_sharded_solver(10, 10, 5, None, None, None, xchg="mpi")
     finally:
         dist.destroy_process_group()
+
+
+def test_local_chunks_partition():
+    """P-invariant grouping (SURVEY 8(e)): C = 8 fixed chunks, world in {1, 2, 4, 8}
+    processes each host a contiguous block of 8 / world logical ranks; together
+    they cover every chunk exactly once; a world that does not divide C is refused."""
+    from paper_2203_16340_b200.sharded import column_range, local_chunks
+    for world in (1, 2, 4, 8):
+        got = [l for r in range(world) for l in local_chunks(8, world, r)]
+        assert got == list(range(8))
+    with pytest.raises(ValueError):
+        local_chunks(8, 3, 0)
+    # the chunk ranges do not depend on the process count
+    rng = [column_range(200000, 8, l) for l in range(8)]
+    assert rng[0] == (0, 25000) and rng[-1] == (175000, 200000)
