@@ -595,3 +595,139 @@ def armijo_lsq(P: LSQ, x, p, amax, l=None, u=None, opts: Options | None = None):
                              _ptr(q), _ptr(p), f, gp, float(amax), _ptr(xt), _ptr(rt), C.byref(fo),
                              C.byref(ao), C.byref(nbt))
     return bool(ok), ao.value, fo.value, int(nbt.value), xt
+
+
+# --------------------------------------------------------------------------
+# Generic objective (callback) + general Alg. 4 (linear and nonlinear constraints)
+# --------------------------------------------------------------------------
+_FG = C.CFUNCTYPE(C.c_int32, C.c_void_p, _dp, _dp, _dp)
+_HG = C.CFUNCTYPE(C.c_int32, C.c_void_p, _dp, _dp, _dp)
+_JTV = C.CFUNCTYPE(C.c_int32, C.c_void_p, _dp, _dp, _dp, _dp)
+
+
+class _GCons(C.Structure):
+    _fields_ = [("nv", C.c_int64), ("P", C.c_void_p), ("fg", _FG), ("fg_ctx", C.c_void_p),
+                ("m_eq", C.c_int32), ("p_in", C.c_int32), ("E", _dp), ("e", _dp), ("G", _dp), ("hv", _dp),
+                ("m_nl", C.c_int32), ("p_nl", C.c_int32), ("hg", _HG), ("jtv", _JTV), ("nl_ctx", C.c_void_p)]
+
+
+def _arr(ptr, n):
+    return np.ctypeslib.as_array(ptr, shape=(max(n, 1),))[:n]
+
+
+def _fg_cb(fun, n):
+    """ctypes trampoline for fun(x) -> (f, g) (numpy)."""
+    def cb(_ctx, xp, gp, fp):
+        try:
+            f, g = fun(_arr(xp, n).copy())
+            _arr(gp, n)[:] = g
+            fp[0] = float(f)
+            return 0
+        except Exception:          # noqa: BLE001 -- reported as a callback failure
+            return 1
+    return _FG(cb)
+
+
+def _setup_general(L):
+    L.orc_minimize_fg.argtypes = [C.c_int64, _FG, C.c_void_p, _dp, _dp, C.c_int32, C.POINTER(_Opts), _dp,
+                                  C.POINTER(_Res)]
+    L.orc_minimize_fg.restype = C.c_int32
+    L.orc_al_general.argtypes = [C.POINTER(_GCons), _dp, _dp, _dp, _dp, C.c_int32, C.POINTER(_Opts),
+                                 C.POINTER(_AlOpts), _dp, C.c_int32, C.POINTER(_AlRes)]
+    L.orc_al_general.restype = C.c_int32
+
+
+def _opts_c(o):
+    return _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
+                 int(o.no_projection), int(o.armijo_diff), o.max_iters)
+
+
+def minimize_fg(fun, n, l=None, u=None, x0=None, m_hist=5, opts: Options | None = None):
+    """Alg. 1 on a generic objective fun(x) -> (f, grad) with every
+    trial value evaluated (orc_minimize_fg)."""
+    L = _L(); _setup_general(L)
+    o = opts or Options()
+    x = np.zeros(n) if x0 is None else _f64(x0).copy()
+    l = None if l is None else _f64(np.broadcast_to(l, (n,)))
+    u = None if u is None else _f64(np.broadcast_to(u, (n,)))
+    cb = _fg_cb(fun, n)
+    res = _Res()
+    so = _opts_c(o)
+    rc = L.orc_minimize_fg(n, cb, None, _ptr(l), _ptr(u), m_hist, C.byref(so), _ptr(x), C.byref(res))
+    if rc:
+        raise RuntimeError(f"objective callback failed ({rc})")
+    return Result(x, res.f, res.pg_inf, res.gfree_inf, res.iters, res.n_fg, res.n_backtracks,
+                  res.n_free, res.status, res.last_branch, res.n_fallbacks)
+
+
+def al_general(n, base=None, fun=None, E=None, e=None, G=None, hv=None, m_nl=0, p_nl=0, hg=None, jtv=None,
+               l=None, u=None, m_hist=5, opts: Options | None = None, al_opts: ALOptions | None = None,
+               x0=None, lam0=None, mu0=None):
+    """Alg. 4 on min f(x) s.t. h(x) = 0, g(x) <= 0, l <= x <= u
+    with h = [E^T x - e; h_nl(x)], g = [G^T x - hv; g_nl(x)] (orc_al_general).
+    base: an LSQ (no constraints of its own) or None with fun(x) -> (f, grad);
+    hg(x) -> (h_nl (m_nl), g_nl (p_nl)); jtv(x, v_eq, v_in) -> J_h^T v_eq + J_g^T v_in.
+    Cold start unless x0 / lam0 / mu0 is given (warm re-entry)."""
+    L = _L(); _setup_general(L)
+    o = opts or Options(); ao = al_opts or ALOptions()
+    E = None if E is None else np.asfortranarray(np.reshape(E, (n, -1)), dtype=np.float64)
+    G = None if G is None else np.asfortranarray(np.reshape(G, (n, -1)), dtype=np.float64)
+    m_eq = 0 if E is None else E.shape[1]
+    p_in = 0 if G is None else G.shape[1]
+    e = None if e is None else _f64(np.atleast_1d(e))
+    hv = None if hv is None else _f64(np.atleast_1d(hv))
+    neq, nin = m_eq + m_nl, p_in + p_nl
+    keep = []
+    s = _GCons()
+    s.nv = n
+    if base is not None:
+        assert base.n_eq == 0 and base.n_in == 0
+        bs = base._struct(); keep.append(bs)
+        s.P = C.cast(C.pointer(bs), C.c_void_p)
+        s.fg = _FG(0)
+    else:
+        s.P = None
+        s.fg = _fg_cb(fun, n)
+    keep.append(s.fg)
+    s.m_eq, s.p_in, s.E, s.e, s.G, s.hv = m_eq, p_in, _ptr(E), _ptr(e), _ptr(G), _ptr(hv)
+    s.m_nl, s.p_nl = m_nl, p_nl
+    if m_nl + p_nl:
+        def hg_c(_ctx, xp, hp, gp):
+            try:
+                h_, g_ = hg(_arr(xp, n).copy())
+                if m_nl:
+                    _arr(hp, m_nl)[:] = h_
+                if p_nl:
+                    _arr(gp, p_nl)[:] = g_
+                return 0
+            except Exception:      # noqa: BLE001
+                return 1
+
+        def jtv_c(_ctx, xp, ve, vi, op):
+            try:
+                _arr(op, n)[:] = jtv(_arr(xp, n).copy(), _arr(ve, m_nl).copy(), _arr(vi, p_nl).copy())
+                return 0
+            except Exception:      # noqa: BLE001
+                return 1
+        s.hg, s.jtv = _HG(hg_c), _JTV(jtv_c)
+    else:
+        s.hg, s.jtv = _HG(0), _JTV(0)
+    keep += [s.hg, s.jtv]
+    warm = x0 is not None or lam0 is not None or mu0 is not None
+    x = np.zeros(n) if x0 is None else _f64(x0).copy()
+    lam = np.zeros(max(neq, 1)); mu = np.zeros(max(nin, 1))
+    if lam0 is not None:
+        lam[:neq] = lam0
+    if mu0 is not None:
+        mu[:nin] = mu0
+    l = None if l is None else _f64(np.broadcast_to(l, (n,)))
+    u = None if u is None else _f64(np.broadcast_to(u, (n,)))
+    so = _opts_c(o)
+    sa = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer)
+    res = _AlRes()
+    rc = L.orc_al_general(C.byref(s), _ptr(lam), _ptr(mu), _ptr(l), _ptr(u), m_hist, C.byref(so), C.byref(sa),
+                          _ptr(x), int(warm), C.byref(res))
+    if rc:
+        raise RuntimeError(f"callback failed ({rc})")
+    return ALResult(x, lam[:neq].copy(), mu[:nin].copy(), res.f, res.violation_inf, res.rho,
+                    res.outer_iters, res.inner_iters_total, res.status)

@@ -1137,3 +1137,248 @@ void orc_lbfgsb_original(const orc_lsq* P, const double* l, const double* u, int
     free(g); free(gn); free(xc); free(xb); free(d); free(xt); free(r); free(rt); free(q); free(rc);
     free(S); free(Y);
 }
+
+/* ------------------------------------------------------------------ */
+/* Alg. 1 on a GENERIC objective (f, grad f from a callback) and       */
+/* Alg. 4 with general constraints:*/
+/* min f(x) s.t. h(x) = 0, g(x) <= 0, l <= x <= u, with h = [E^T x - e; */
+/* h_nl(x)], g = [G^T x - hv; g_nl(x)]: linear blocks as E / G columns, */
+/* nonlinear blocks through callbacks for the values and for J^T v.     */
+/* Every objective value at a trial point is EVALUATED (no carried     */
+/* residual): the reading of the callback path (R14's fallback, R10,   */
+/* R11 as in orc_minimize_lsq).                                         */
+/* ------------------------------------------------------------------ */
+typedef int32_t (*orc_fg_fn)(void* ctx, const double* x, double* g, double* f);
+typedef int32_t (*orc_hg_fn)(void* ctx, const double* x, double* h, double* gc);
+typedef int32_t (*orc_jtv_fn)(void* ctx, const double* x, const double* veq, const double* vin,
+                              double* out);
+
+/* Alg. 1 with Alg. 2 / Alg. 3 and Armijo backtracking on
+ * f(clip(fma(alpha, p, x))) evaluated by fg.  Returns 0, or the nonzero
+ * callback code (res->status untouched then). */
+int32_t orc_minimize_fg(int64_t nv, orc_fg_fn fg, void* ctx, const double* l, const double* u,
+                        int32_t m_hist, const orc_opts* o, double* x, orc_result* res)
+{
+    const size_t nvb = sizeof(double) * (size_t)(nv > 0 ? nv : 1);
+    double *g = malloc(nvb), *gn = malloc(nvb), *d = malloc(nvb), *p = malloc(nvb), *xt = malloc(nvb);
+    double *Sr = malloc(nvb * (size_t)(m_hist > 0 ? m_hist : 1));
+    double *Yr = malloc(nvb * (size_t)(m_hist > 0 ? m_hist : 1));
+    uint8_t* fr = malloc((size_t)(nv > 0 ? nv : 1));
+    int32_t nh = 0, rc = 0;
+    memset(res, 0, sizeof(*res));
+    orc_clip(nv, x, l, u, x);                                       /* feasible x^0 */
+    double f = 0.0;
+    rc = fg(ctx, x, g, &f);
+    res->n_fg = 1;
+    int64_t k = 0;
+    int32_t status = ORC_MAX_ITERS;
+    while (rc == 0) {
+        orc_working_set(nv, x, g, l, u, o->eps, fr);                 /* Alg. 1 line 3 */
+        double gfree = 0.0; int64_t nfree = 0;
+        for (int64_t j = 0; j < nv; ++j)
+            if (fr[j]) { ++nfree; if (fabs(g[j]) > gfree) gfree = fabs(g[j]); }
+        if (nfree == 0 || gfree <= o->tol) { status = ORC_CONVERGED; break; }    /* R15 */
+        if (k >= o->max_iters) { status = ORC_MAX_ITERS; break; }
+        int accepted = 0;
+        double alpha = 0.0, ft = f;
+        for (int attempt = 0; attempt < 2 && !accepted && rc == 0; ++attempt) {
+            if (attempt == 1) { nh = 0; res->n_fallbacks += 1; }      /* R14 fallback */
+            orc_two_loop(nv, g, fr, nh, Sr, Yr, o->eps, o->screen_full_norm, d);
+            const int32_t br = o->no_projection ? orc_truncate_direction(nv, x, d, l, u, o->eps, p)
+                                                : orc_project_direction(nv, x, g, d, l, u, o->eps, p);
+            res->last_branch = br;
+            double gp = 0.0;
+            for (int64_t j = 0; j < nv; ++j) gp += g[j] * p[j];
+            if (!(gp < 0.0)) continue;                                 /* guard, R14 */
+            const double amax = br ? 1.0 : orc_max_step(nv, x, p, l, u);
+            alpha = amax < 1.0 ? amax : 1.0;                           /* R10 */
+            for (int32_t t = 0; t <= o->max_backtracks; ++t) {
+                if (t > 0) alpha = o->shrink * alpha;                  /* R11 */
+                for (int64_t j = 0; j < nv; ++j) xt[j] = clip1(fma(alpha, p[j], x[j]), l, u, j);
+                rc = fg(ctx, xt, gn, &ft);
+                res->n_fg += 1;
+                if (rc) break;
+                if (ft <= f + o->c1 * alpha * gp) { accepted = 1; break; }
+                res->n_backtracks += 1;
+            }
+        }
+        if (rc) break;
+        if (!accepted) { status = ORC_LINESEARCH_FAILURE; break; }
+        if (m_hist > 0) {                                              /* PAPER.md:77-80, R8 */
+            if (nh == m_hist) {
+                memmove(Sr, Sr + nv, nvb * (size_t)(m_hist - 1));
+                memmove(Yr, Yr + nv, nvb * (size_t)(m_hist - 1));
+                nh = m_hist - 1;
+            }
+            for (int64_t j = 0; j < nv; ++j) {
+                Sr[(int64_t)nh * nv + j] = xt[j] - x[j];
+                Yr[(int64_t)nh * nv + j] = gn[j] - g[j];
+            }
+            nh += 1;
+        }
+        memcpy(x, xt, nvb); memcpy(g, gn, nvb);
+        f = ft;
+        ++k;
+    }
+    if (rc == 0) {
+        orc_working_set(nv, x, g, l, u, o->eps, fr);
+        double pg = 0.0, gfree = 0.0; int64_t nfree = 0;
+        for (int64_t j = 0; j < nv; ++j) {
+            const double v = fabs(clip1(x[j] - g[j], l, u, j) - x[j]);
+            if (v > pg) pg = v;
+            if (fr[j]) { ++nfree; if (fabs(g[j]) > gfree) gfree = fabs(g[j]); }
+        }
+        res->f = f; res->pg_inf = pg; res->gfree_inf = gfree; res->n_free = nfree;
+        res->iters = k; res->status = status;
+    }
+    free(g); free(gn); free(d); free(p); free(xt); free(Sr); free(Yr); free(fr);
+    return rc;
+}
+
+/* The constrained problem of the general Alg. 4.  Base objective: the LSQ
+ * family P (its own constraint fields must be empty) or, when P is NULL, the
+ * callback fg.  Constraint stacking: equalities [linear m_eq; nonlinear
+ * m_nl], inequalities [linear p_in; nonlinear p_nl]; multipliers in the same
+ * order. */
+typedef struct {
+    int64_t nv;
+    const orc_lsq* P;
+    orc_fg_fn fg; void* fg_ctx;
+    int32_t m_eq, p_in;           /* linear: E (nv x m_eq col-major), e; G (nv x p_in), hv */
+    const double *E, *e, *G, *hv;
+    int32_t m_nl, p_nl;           /* nonlinear: values and J^T v through callbacks */
+    orc_hg_fn hg; orc_jtv_fn jtv; void* nl_ctx;
+} orc_gcons;
+
+typedef struct {
+    const orc_gcons* Q;
+    const double* lam; const double* mu; double rho;
+    double* hv; double* gv;       /* scratch: all equality / inequality values */
+    double* weq; double* win;     /* scratch: multiplier-weighted coefficients */
+    double* tmp;                  /* scratch nv */
+} orc_al_ctx;
+
+/* all constraint values at x: h (m_eq + m_nl), g (p_in + p_nl) */
+static int32_t gcons_values(const orc_gcons* Q, const double* x, double* h, double* gc)
+{
+    for (int32_t k = 0; k < Q->m_eq; ++k) {
+        double s = 0.0;
+        const double* col = Q->E + (int64_t)k * Q->nv;
+        for (int64_t j = 0; j < Q->nv; ++j) s += col[j] * x[j];
+        h[k] = s - Q->e[k];
+    }
+    for (int32_t k = 0; k < Q->p_in; ++k) {
+        double s = 0.0;
+        const double* col = Q->G + (int64_t)k * Q->nv;
+        for (int64_t j = 0; j < Q->nv; ++j) s += col[j] * x[j];
+        gc[k] = s - Q->hv[k];
+    }
+    if (Q->m_nl + Q->p_nl > 0)
+        return Q->hg(Q->nl_ctx, x, h + Q->m_eq, gc + Q->p_in);
+    return 0;
+}
+
+/* Eq. (3): L = f + rho/2 ||h + lam/rho||^2 + rho/2 ||(g + mu/rho)_+||^2,
+ * grad L = grad f + J_h^T (rho h + lam) + J_g^T (rho g + mu)_+ */
+static int32_t al_fg(void* vctx, const double* x, double* g, double* f)
+{
+    orc_al_ctx* A = (orc_al_ctx*)vctx;
+    const orc_gcons* Q = A->Q;
+    const int64_t nv = Q->nv;
+    int32_t rc = 0;
+    if (Q->P) {
+        *f = orc_lsq_value(Q->P, x);
+        orc_lsq_grad(Q->P, x, g);
+    } else {
+        rc = Q->fg(Q->fg_ctx, x, g, f);
+        if (rc) return rc;
+    }
+    rc = gcons_values(Q, x, A->hv, A->gv);
+    if (rc) return rc;
+    const int32_t neq = Q->m_eq + Q->m_nl, nin = Q->p_in + Q->p_nl;
+    double pen = 0.0;
+    for (int32_t k = 0; k < neq; ++k) {
+        const double t = A->hv[k] + A->lam[k] / A->rho;
+        pen += 0.5 * A->rho * t * t;
+        A->weq[k] = A->rho * A->hv[k] + A->lam[k];
+    }
+    for (int32_t k = 0; k < nin; ++k) {
+        double t = A->gv[k] + A->mu[k] / A->rho;
+        if (t < 0.0) t = 0.0;
+        pen += 0.5 * A->rho * t * t;
+        A->win[k] = A->rho * t;
+    }
+    *f = *f + pen;
+    for (int64_t j = 0; j < nv; ++j) {
+        double v = g[j];
+        for (int32_t k = 0; k < Q->m_eq; ++k) v = v + A->weq[k] * Q->E[(int64_t)k * nv + j];
+        for (int32_t k = 0; k < Q->p_in; ++k) v = v + A->win[k] * Q->G[(int64_t)k * nv + j];
+        g[j] = v;
+    }
+    if (Q->m_nl + Q->p_nl > 0) {
+        rc = Q->jtv(Q->nl_ctx, x, A->weq + Q->m_eq, A->win + Q->p_in, A->tmp);
+        if (rc) return rc;
+        for (int64_t j = 0; j < nv; ++j) g[j] = g[j] + A->tmp[j];
+    }
+    return 0;
+}
+
+/* Alg. 4 on the general problem, readings R19-R22 as in
+ * orc_al_solve_ex (warm = 1 re-enters from x, lam, mu as given).  Returns 0
+ * or a nonzero callback code. */
+int32_t orc_al_general(const orc_gcons* Q, double* lam, double* mu, const double* l, const double* u,
+                       int32_t m_hist, const orc_opts* o, const orc_al_opts* ao, double* x, int32_t warm,
+                       orc_al_result* res)
+{
+    const int64_t nv = Q->nv;
+    const int32_t neq = Q->m_eq + Q->m_nl, nin = Q->p_in + Q->p_nl;
+    memset(res, 0, sizeof(*res));
+    if (!warm) {
+        for (int64_t j = 0; j < nv; ++j) x[j] = 0.0;                  /* R19 */
+        for (int32_t k = 0; k < neq; ++k) lam[k] = 0.0;
+        for (int32_t k = 0; k < nin; ++k) mu[k] = 0.0;
+    }
+    orc_clip(nv, x, l, u, x);
+    orc_al_ctx A;
+    A.Q = Q; A.lam = lam; A.mu = mu;
+    A.hv = cons_buf(neq); A.gv = cons_buf(nin);
+    A.weq = cons_buf(neq); A.win = cons_buf(nin);
+    A.tmp = (double*)malloc(sizeof(double) * (size_t)(nv > 0 ? nv : 1));
+    double rho = ao->rho0;
+    int32_t rc = gcons_values(Q, x, A.hv, A.gv);
+    double vprev = rc ? 0.0 : orc_al_violation(neq, A.hv, nin, A.gv, mu, rho);
+    res->status = ORC_AL_MAX_OUTER;
+    for (int32_t it = 0; it < ao->max_outer && rc == 0; ++it) {
+        orc_opts oi = *o;
+        const double tin = 0.1 * vprev;
+        oi.tol = tin > o->tol ? tin : o->tol;                           /* R22 */
+        A.rho = rho;
+        orc_result ir;
+        rc = orc_minimize_fg(nv, al_fg, &A, l, u, m_hist, &oi, x, &ir); /* Alg. 4 line 5 */
+        if (rc) break;
+        res->inner_iters_total += ir.iters;
+        res->outer_iters = it + 1;
+        if (ir.status == ORC_LINESEARCH_FAILURE) { res->status = ORC_AL_INNER_FAILURE; break; }
+        rc = gcons_values(Q, x, A.hv, A.gv);
+        if (rc) break;
+        orc_al_update_multipliers(neq, lam, A.hv, nin, mu, A.gv, rho);  /* lines 6-7 */
+        const double v = orc_al_violation(neq, A.hv, nin, A.gv, mu, rho);
+        rho = orc_al_update_rho(rho, vprev, v, ao->rho_factor, ao->rho_cap);   /* line 8, R20 */
+        vprev = v;
+        if (ir.status == ORC_CONVERGED && v <= ao->feas_tol && oi.tol == o->tol) {
+            res->status = ORC_CONVERGED;
+            break;
+        }
+    }
+    if (rc == 0) {
+        double* gtmp = (double*)malloc(sizeof(double) * (size_t)(nv > 0 ? nv : 1));
+        if (Q->P) res->f = orc_lsq_value(Q->P, x);
+        else rc = Q->fg(Q->fg_ctx, x, gtmp, &res->f);
+        free(gtmp);
+        if (rc == 0) rc = gcons_values(Q, x, A.hv, A.gv);
+        res->violation_inf = orc_al_violation(neq, A.hv, nin, A.gv, mu, rho);
+        res->rho = rho;
+    }
+    free(A.hv); free(A.gv); free(A.weq); free(A.win); free(A.tmp);
+    return rc;
+}
