@@ -318,20 +318,39 @@ typedef struct {
     double rho_factor;          /* rho *= rho_factor if violation not halved; 2 */
     double rho_cap;             /* default 1e12                                          */
     int32_t max_outer;          /* default 100                                           */
-    int32_t pad_;
+    int32_t warm_start;         /* 0: x^0 = clip(0), lambda = mu = 0 (Alg. 4 line 3, R19);
+                                   1: re-enter from the given x, lambda, mu (x clipped)  */
 } al_opts;
 
 void al_opts_default(al_opts* o);                                    /* (host) */
 
-/* Linear constraints  E^T x = e  (m_eq of them) and  G^T x <= hv  (p_in),
- * m_eq + p_in <= LBFGSB_MAX_CONS.  E: n x m_eq column-major (DEVICE),
- * e: m_eq (host); G: n x p_in (DEVICE), hv: p_in (host). */
+/* Nonlinear constraint callbacks (h: R^n -> R^m, g: R^n -> R^p
+ * differentiable).  All pointers DEVICE, work enqueued on `stream` (or
+ * synchronous); return 0 on success, nonzero = failure (al_solve then returns
+ * LBFGSB_ERR_CALLBACK).
+ *   hg:  h_out (m_nl) = h_nl(x), g_out (p_nl) = g_nl(x);
+ *   jtv: out (n) = J_h(x)^T v_eq + J_g(x)^T v_in  (v_eq: m_nl, v_in: p_nl). */
+typedef int32_t (*al_hg_cb)(void* user, const double* x, double* h_out, double* g_out, void* stream);
+typedef int32_t (*al_jtv_cb)(void* user, const double* x, const double* v_eq, const double* v_in,
+                             double* out, void* stream);
+
+/* Constraints of Alg. 4: h(x) = [E^T x - e; h_nl(x)] = 0 and
+ * g(x) = [G^T x - hv; g_nl(x)] <= 0.
+ * Linear blocks: E n x m_eq, G n x p_in column-major (DEVICE, column k = the
+ * coefficients of constraint k, contiguous); e (m_eq), hv (p_in) HOST.
+ * Nonlinear blocks: m_nl equalities and p_nl inequalities through hg / jtv
+ * (NULL when m_nl = p_nl = 0).  Multipliers are stacked the same way:
+ * lambda = [linear m_eq; nonlinear m_nl], mu = [linear p_in; nonlinear p_nl]. */
 typedef struct {
     int64_t m_eq, p_in;
     const double* E;
     const double* e;
     const double* G;
     const double* hv;
+    int64_t m_nl, p_nl;
+    al_hg_cb hg;
+    al_jtv_cb jtv;
+    void* user;
 } al_constraints;
 
 typedef struct {
@@ -344,14 +363,25 @@ typedef struct {
     int32_t pad_;
 } al_result;
 
-/* Alg. 4: x^0 = clip(0) (R19), lambda^0 = 0, mu^0 = 0, rho = rho0; each
- * outer iteration minimises the augmented Lagrangian Eq. (3) over the box
- * with Alg. 1 (warm x, empty history, inner tol max(tol, 0.1 v), R22), then
- * lambda += rho h(x), mu = (mu + rho g(x))_+  and
- * rho *= rho_factor if the violation was not halved (R20).
- * obj must be an LSQ objective.  x (DEVICE, n) out; lambda (host, m_eq) and
- * mu (host, p_in) out.  Errors: ARG, DIM, UNSUPPORTED (callback objective or
- * too many constraints), CUDA. */
+/* Alg. 4: x^0 = clip(0) (R19), lambda^0 = 0, mu^0 = 0,
+ * rho = rho0 (or the given x, lambda, mu when opts->warm_start); each outer
+ * iteration minimises the augmented Lagrangian Eq. (3)
+ * over the box with Alg. 1 (warm x, empty history, inner tol
+ * max(tol, 0.1 v), R22), then lambda += rho h(x), mu = (mu + rho g(x))_+
+ * and rho *= rho_factor if the violation was not halved
+ * (R20).
+ * Two paths, the same method:
+ *  - fused: an LSQ objective with m_eq + p_in <= LBFGSB_MAX_CONS linear
+ *    constraints and no nonlinear ones -- the AL terms ride inside the
+ *    iteration kernels (carried constraint values, the trial sums of k_sep);
+ *  - general: any other case -- an LSQ or callback objective, any number of
+ *    linear constraints (E^T x and E w on the GEMV kernels, one pass over E
+ *    each), nonlinear constraints through hg / jtv.  The inner solve is the
+ *    callback-objective Alg. 1: every trial value is evaluated.
+ * x (DEVICE, n) in (warm start) / out; lambda (host, m_eq + m_nl) and mu
+ * (host, p_in + p_nl) in (warm start) / out.  Errors: ARG, DIM, UNSUPPORTED
+ * (QP or transport objective with constraints other than the fused path's),
+ * CALLBACK, NONFINITE, CUDA. */
 lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const al_constraints* cons,
                     const al_opts* opts, double* x, double* lambda, double* mu,
                     al_result* res);

@@ -46,12 +46,17 @@ class _Res(C.Structure):
 
 class _AlOpts(C.Structure):
     _fields_ = [("feas_tol", _c_d), ("rho0", _c_d), ("rho_factor", _c_d), ("rho_cap", _c_d),
-                ("max_outer", _c_i32), ("pad_", _c_i32)]
+                ("max_outer", _c_i32), ("warm_start", _c_i32)]
+
+
+HG_CB = C.CFUNCTYPE(_c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp)
+JTV_CB = C.CFUNCTYPE(_c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp)
 
 
 class _AlCons(C.Structure):
     _fields_ = [("m_eq", _c_i64), ("p_in", _c_i64), ("E", _c_vp), ("e", C.POINTER(_c_d)),
-                ("G", _c_vp), ("hv", C.POINTER(_c_d))]
+                ("G", _c_vp), ("hv", C.POINTER(_c_d)), ("m_nl", _c_i64), ("p_nl", _c_i64),
+                ("hg", HG_CB), ("jtv", JTV_CB), ("user", _c_vp)]
 
 
 class _AlRes(C.Structure):
@@ -449,26 +454,62 @@ class Solver:
                        r.n_free, r.n_fallbacks, r.status, r.last_branch) for r in res]
 
     def al_solve(self, obj, x, E=None, e=None, G=None, hv=None,
-                 al_opts: ALOptions | None = None) -> ALResult:
-        """Alg. 4 with linear constraints E^T x = e, G^T x <= hv; E (n, m_eq) and
-        G (n, p_in) CUDA fp64 column-major (column k contiguous)."""
+                 al_opts: ALOptions | None = None, hg=None, jtv=None, m_nl=0, p_nl=0,
+                 lam0=None, mu0=None, warm_start=False) -> ALResult:
+        """Alg. 4 (al_solve): linear constraints E^T x = e, G^T x <= hv (E (n, m_eq),
+        G (n, p_in) CUDA fp64; any number of them) and nonlinear ones through
+        hg(x, h_out, g_out) (h_out (m_nl), g_out (p_nl) CUDA views written in place)
+        and jtv(x, v_eq, v_in, out) (out (n) = J_h^T v_eq + J_g^T v_in).  obj: an
+        LSQObjective or a CallbackObjective.  warm_start: re-enter from x and
+        lam0 / mu0 (host sequences of m_eq + m_nl / p_in + p_nl) instead of
+        x = clip(0), lambda = mu = 0."""
         import torch
         ao = al_opts or ALOptions()
-        c_ao = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer, 0)
+        c_ao = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer, int(bool(warm_start)))
         m_eq = 0 if E is None else (E.shape[1] if E.dim() == 2 else 1)
         p_in = 0 if G is None else (G.shape[1] if G.dim() == 2 else 1)
         Ec = None if E is None else E.reshape(self.n, m_eq).T.contiguous()   # (m_eq, n) rows = columns
         Gc = None if G is None else G.reshape(self.n, p_in).T.contiguous()
         e_arr = (_c_d * max(m_eq, 1))(*([float(v) for v in torch.as_tensor(e).flatten()] if m_eq else [0.0]))
         h_arr = (_c_d * max(p_in, 1))(*([float(v) for v in torch.as_tensor(hv).flatten()] if p_in else [0.0]))
-        cons = _AlCons(m_eq, p_in, _ptr(Ec), e_arr, _ptr(Gc), h_arr)
-        lam = (_c_d * max(m_eq, 1))()
-        mu = (_c_d * max(p_in, 1))()
+        n = self.n
+        errs = []
+
+        def _hg(user, xp, hp, gp, stream):
+            try:
+                hg(_wrap(xp, n), _wrap(hp, m_nl) if m_nl else None, _wrap(gp, p_nl) if p_nl else None)
+                torch.cuda.current_stream().synchronize()
+                return 0
+            except Exception as ex:          # noqa: BLE001 -- surfaced after the call
+                errs.append(ex)
+                return 1
+
+        def _jtv(user, xp, vep, vip, op, stream):
+            try:
+                jtv(_wrap(xp, n), _wrap(vep, m_nl) if m_nl else None, _wrap(vip, p_nl) if p_nl else None,
+                    _wrap(op, n))
+                torch.cuda.current_stream().synchronize()
+                return 0
+            except Exception as ex:          # noqa: BLE001
+                errs.append(ex)
+                return 1
+        nl = (m_nl + p_nl) > 0
+        hg_c = HG_CB(_hg) if nl else HG_CB(0)
+        jtv_c = JTV_CB(_jtv) if nl else JTV_CB(0)
+        cons = _AlCons(m_eq, p_in, _ptr(Ec), e_arr, _ptr(Gc), h_arr, int(m_nl), int(p_nl), hg_c, jtv_c, None)
+        neq, nin = m_eq + m_nl, p_in + p_nl
+        lam = (_c_d * max(neq, 1))(*(list(map(float, lam0)) if lam0 is not None else []))
+        mu = (_c_d * max(nin, 1))(*(list(map(float, mu0)) if mu0 is not None else []))
         r = _AlRes()
-        _check(_lib.al_solve(self._h, obj._h, C.byref(cons), C.byref(c_ao), _ptr(x), lam, mu,
-                             C.byref(r)))
+        rc = _lib.al_solve(self._h, obj._h, C.byref(cons), C.byref(c_ao), _ptr(x), lam, mu, C.byref(r))
+        if isinstance(obj, CallbackObjective) and obj._err is not None:
+            e_, obj._err = obj._err, None
+            raise LbfgsbError(f"objective callback raised: {e_!r}") from e_
+        if errs:
+            raise LbfgsbError(f"constraint callback raised: {errs[0]!r}") from errs[0]
+        _check(rc)
         return ALResult(r.violation_inf, r.f, r.rho, r.pg_inf, r.outer_iters, r.inner_iters_total,
-                        r.status, list(lam)[:m_eq], list(mu)[:p_in])
+                        r.status, list(lam)[:neq], list(mu)[:nin])
 
     def al_solve_transport(self, obj, x, u, v, lam_out=None,
                            al_opts: ALOptions | None = None) -> ALResult:

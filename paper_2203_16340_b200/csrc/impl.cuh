@@ -208,6 +208,17 @@ void launch_kkt_decide(const Prob& P, cudaStream_t st);
 // p2p.cu: exchange over peer memory (the producers push from their tails)
 void launch_p2p_put(const Prob& P, cudaStream_t st, int sec, int64_t off, int64_t cnt);
 void launch_p2p_barrier(const Prob* Ps, int n, cudaStream_t st);
+// al.cu: the stacked-constraint pieces of the general Alg. 4
+void launch_al_terms(int64_t neq, const double* h, const double* lam, int64_t nin, const double* g,
+                     const double* mu, double rho, double* weq, double* win, double* out, cudaStream_t st);
+void launch_al_update(int64_t neq, const double* h, double* lam, int64_t nin, const double* g, double* mu,
+                      double rho, double* vout, cudaStream_t st);
+void launch_al_violation(int64_t neq, const double* h, int64_t nin, const double* g, const double* mu, double rho,
+                         double* vout, cudaStream_t st);
+void launch_lsq_value(int64_t m, const double* r, int64_t n, const double* x, const double* c, double delta,
+                      double* g, double* out, cudaStream_t st);
+void launch_sub(int64_t n, double* r, const double* b, cudaStream_t st);
+void launch_axpy(int64_t n, const double* x, double* y, cudaStream_t st);
 void launch_gauss(const double* X, int64_t N, int64_t d, double gamma, double* K, int64_t ldk,
                   cudaStream_t st);
 void launch_ring_load(const Prob& P, cudaStream_t st, int nh, const double* S, const double* Y);

@@ -76,6 +76,10 @@ namespace {
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
     lbfgsb_err ensure(size_t need, bool zero = false)
     {
         if (need <= bytes && p) return LBFGSB_OK;
@@ -1199,22 +1203,35 @@ extern "C" lbfgsb_err lbfgsb_solve_lsq_host_batch(lbfgsb_t* h, int32_t count, co
 }
 
 // ------------------------------------------------------------------ Alg. 4
+static lbfgsb_err al_solve_general(lbfgsb_t* h, const lbfgsb_objective* obj, const al_constraints* cons,
+                                   const al_opts& ao, double* x, double* lambda, double* mu, al_result* res);
+
 extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const al_constraints* cons,
                                const al_opts* opts, double* x, double* lambda, double* mu,
                                al_result* res)
 {
     if (!h || !obj || !x) return fail(LBFGSB_ERR_ARG, "NULL handle, objective or x");
-    if (obj->kind != 0) return fail(LBFGSB_ERR_UNSUPPORTED, "al_solve needs an LSQ objective");
     al_opts ao;
     al_opts_default(&ao);
     if (opts) ao = *opts;
-    const int neq = cons ? (int)cons->m_eq : 0, nin = cons ? (int)cons->p_in : 0;
-    if (neq < 0 || nin < 0) return fail(LBFGSB_ERR_DIM, "negative constraint count");
-    if (neq + nin > MAXC) return fail(LBFGSB_ERR_UNSUPPORTED, "at most %d linear constraints", MAXC);
-    if ((neq && (!cons->E || !cons->e)) || (nin && (!cons->G || !cons->hv)))
-        return fail(LBFGSB_ERR_ARG, "constraint data missing");
-    if (!(ao.rho0 > 0) || !(ao.rho_factor > 1) || ao.max_outer < 1)
+    if (!(ao.rho0 > 0) || !(ao.rho_factor > 1) || ao.max_outer < 1 || !(ao.rho_cap > 0))
         return fail(LBFGSB_ERR_ARG, "invalid al_opts");
+    const int64_t neq64 = cons ? cons->m_eq : 0, nin64 = cons ? cons->p_in : 0;
+    const int64_t mnl = cons ? cons->m_nl : 0, pnl = cons ? cons->p_nl : 0;
+    if (neq64 < 0 || nin64 < 0 || mnl < 0 || pnl < 0) return fail(LBFGSB_ERR_DIM, "negative constraint count");
+    if ((neq64 && (!cons->E || !cons->e)) || (nin64 && (!cons->G || !cons->hv)))
+        return fail(LBFGSB_ERR_ARG, "constraint data missing");
+    if ((mnl || pnl) && (!cons->hg || !cons->jtv)) return fail(LBFGSB_ERR_ARG, "nonlinear callbacks missing");
+    if (ao.warm_start && ((neq64 + mnl > 0 && !lambda) || (nin64 + pnl > 0 && !mu)))
+        return fail(LBFGSB_ERR_ARG, "warm start needs lambda / mu");
+    if (h->sharded) return fail(LBFGSB_ERR_UNSUPPORTED, "al_solve is single-GPU");
+    const bool fused = obj->kind == 0 && neq64 + nin64 <= MAXC && mnl + pnl == 0;
+    if (!fused) {
+        if (obj->kind == 2 || (obj->kind == 0 && obj->qp))
+            return fail(LBFGSB_ERR_UNSUPPORTED, "general al_solve takes an LSQ or callback objective");
+        return al_solve_general(h, obj, cons, ao, x, lambda, mu, res);
+    }
+    const int neq = (int)neq64, nin = (int)nin64;
     Group g;
     TRY(single_group(h, obj, g));
     Prob& P = g.Ps[0];
@@ -1223,9 +1240,13 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
     for (int k = 0; k < nin; ++k) P.Ecol[neq + k] = cons->G + (int64_t)k * h->n;
     set_sep(P);
     const double tol = h->o.tol;
-    // x^0 = clip(0) (R19), lambda = 0, mu = 0, rho = rho0
-    CK(cudaMemsetAsync(x, 0, sizeof(double) * h->n, h->st));
+    // x^0 = clip(0) (R19), lambda = 0, mu = 0, rho = rho0; warm start: as given
+    if (!ao.warm_start) CK(cudaMemsetAsync(x, 0, sizeof(double) * h->n, h->st));
     double lam[MAXC] = {0}, rhs[MAXC] = {0};
+    if (ao.warm_start) {
+        for (int k = 0; k < neq; ++k) lam[k] = lambda[k];
+        for (int k = 0; k < nin; ++k) lam[neq + k] = mu[k];
+    }
     for (int k = 0; k < neq; ++k) rhs[k] = cons->e[k];
     for (int k = 0; k < nin; ++k) rhs[neq + k] = cons->hv[k];
     double rho = ao.rho0;
@@ -1291,6 +1312,204 @@ extern "C" lbfgsb_err al_solve(lbfgsb_t* h, const lbfgsb_objective* obj, const a
     R.rho = rho;
     if (lambda) for (int k = 0; k < neq; ++k) lambda[k] = lam[k];
     if (mu) for (int k = 0; k < nin; ++k) mu[k] = lam[neq + k];
+    if (res) *res = R;
+    return LBFGSB_OK;
+}
+
+// ------------------------------------------------------------------ Alg. 4, general constraints
+// The general problem class through Eq. (3) as a callback
+// objective of the inner Alg. 1 (solve_cb): L(x) = f(x) + penalty terms with
+// f an LSQ objective (r = M~x - b by k_fwd, M~^T r by k_bwd) or the caller's
+// callback, the linear blocks E^T x / G^T x by k_bwd and E w / G w by k_fwd
+// (E as an n x K operator), the nonlinear blocks through hg / jtv, the
+// stacked-vector parts in al.cu.  Every trial value is evaluated.
+namespace {
+struct GOp {                                // one operator for plain GEMV / GEMV^T passes
+    Prob P{};
+    DevBuf qpart, tick;
+    lbfgsb_err init(const double* M, int64_t m, int64_t ncols, int64_t ld, const double* colscale, int split)
+    {
+        std::memset(&P, 0, sizeof P);
+        P.m = m; P.ncols = ncols; P.ld = ld; P.M = M;
+        P.colscale = colscale; P.split = split;
+        P.n = split ? 2 * ncols : ncols;
+        gemv_geometry(P);
+        TRY(qpart.ensure(sizeof(double) * (size_t)P.m * (size_t)P.CC));
+        TRY(tick.ensure(sizeof(unsigned) * (NTICKETS + TICKETS_EXTRA), true));
+        P.qpart = qpart.d();
+        P.tickets = static_cast<unsigned*>(tick.p);
+        return LBFGSB_OK;
+    }
+    void fwd(const double* p, double* q, cudaStream_t st) { launch_fwd(P, st, FWD_P, p, q); }   // q = M~ p
+    void bwd(const double* r, double* g, cudaStream_t st)                                       // g = M~^T r
+    {
+        P.rbuf[0] = const_cast<double*>(r);
+        P.rbuf[1] = const_cast<double*>(r);
+        launch_bwd(P, st, BWD_PLAIN, r, g);
+    }
+};
+
+struct ALGen {
+    lbfgsb_t* h = nullptr;
+    const lbfgsb_objective* base = nullptr;
+    const al_constraints* cons = nullptr;
+    cudaStream_t st = nullptr;
+    int64_t n = 0, m_eq = 0, p_in = 0, m_nl = 0, p_nl = 0, neq = 0, nin = 0;
+    GOp opM, opE, opG;
+    DevBuf r, lam, mu, hv, gv, weq, win, tmp, scal, erhs, hrhs;
+    double* sh = nullptr;                   // pinned host scalars [base f, penalty, violation]
+    double rho = 1.0;
+    bool cb_fail = false;
+
+    // stacked constraint values at x: hv = [E^T x - e; h_nl(x)], gv = [G^T x - hv; g_nl(x)]
+    int values(const double* x)
+    {
+        if (m_eq) { opE.bwd(x, hv.d(), st); launch_sub(m_eq, hv.d(), erhs.d(), st); }
+        if (p_in) { opG.bwd(x, gv.d(), st); launch_sub(p_in, gv.d(), hrhs.d(), st); }
+        if (m_nl + p_nl) return cons->hg(cons->user, x, hv.d() + m_eq, gv.d() + p_in, st);
+        return 0;
+    }
+    // base objective value (into sh[0] after a sync, or *fcb for a callback) and gradient g
+    int base_fg(const double* x, double* g, double* fcb)
+    {
+        if (base->kind == 1) return base->fg(base->user, x, g, fcb, st);
+        opM.fwd(x, r.d(), st);                                       // r = M~ x
+        if (base->b) launch_sub(base->m, r.d(), base->b, st);       // - b
+        opM.bwd(r.d(), g, st);                                       // g = M~^T r
+        launch_lsq_value(base->m, r.d(), n, x, base->c, base->delta, g, scal.d(), st);
+        return 0;
+    }
+};
+
+// callback of the inner solve: f = L(x), g = grad L(x)
+int32_t al_gen_fg(void* user, const double* x, double* g, double* f_host, void* /*stream*/)
+{
+    ALGen& A = *static_cast<ALGen*>(user);
+    double fcb = 0.0;
+    if (A.base_fg(x, g, &fcb) != 0 || A.values(x) != 0) { A.cb_fail = true; return 1; }
+    launch_al_terms(A.neq, A.hv.d(), A.lam.d(), A.nin, A.gv.d(), A.mu.d(), A.rho, A.weq.d(), A.win.d(),
+                    A.scal.d() + 1, A.st);
+    if (A.m_eq) { A.opE.fwd(A.weq.d(), A.tmp.d(), A.st); launch_axpy(A.n, A.tmp.d(), g, A.st); }
+    if (A.p_in) { A.opG.fwd(A.win.d(), A.tmp.d(), A.st); launch_axpy(A.n, A.tmp.d(), g, A.st); }
+    if (A.m_nl + A.p_nl) {
+        if (A.cons->jtv(A.cons->user, x, A.weq.d() + A.m_eq, A.win.d() + A.p_in, A.tmp.d(), A.st) != 0) {
+            A.cb_fail = true;
+            return 1;
+        }
+        launch_axpy(A.n, A.tmp.d(), g, A.st);
+    }
+    if (cudaMemcpyAsync(A.sh, A.scal.d(), sizeof(double) * 2, cudaMemcpyDeviceToHost, A.st) != cudaSuccess ||
+        cudaStreamSynchronize(A.st) != cudaSuccess)
+        return 1;
+    *f_host = (A.base->kind == 1 ? fcb : A.sh[0]) + A.sh[1];
+    return 0;
+}
+}  // namespace
+
+static lbfgsb_err al_solve_general(lbfgsb_t* h, const lbfgsb_objective* obj, const al_constraints* cons,
+                                   const al_opts& ao, double* x, double* lambda, double* mu, al_result* res)
+{
+    ALGen A;
+    A.h = h; A.base = obj; A.cons = cons; A.st = h->st; A.n = h->n;
+    A.m_eq = cons ? cons->m_eq : 0; A.p_in = cons ? cons->p_in : 0;
+    A.m_nl = cons ? cons->m_nl : 0; A.p_nl = cons ? cons->p_nl : 0;
+    A.neq = A.m_eq + A.m_nl; A.nin = A.p_in + A.p_nl;
+    const int64_t n = h->n;
+    cudaStream_t st = h->st;
+    if (obj->kind == 0) {
+        if ((obj->split ? 2 * obj->ncols : obj->ncols) != n) return fail(LBFGSB_ERR_DIM, "objective size != n");
+        TRY(A.opM.init(obj->M, obj->m, obj->ncols, obj->ld, obj->colscale, obj->split));
+        TRY(A.r.ensure(sizeof(double) * (size_t)obj->m));
+    }
+    if (A.m_eq) TRY(A.opE.init(cons->E, n, A.m_eq, n, nullptr, 0));
+    if (A.p_in) TRY(A.opG.init(cons->G, n, A.p_in, n, nullptr, 0));
+    const size_t be = sizeof(double) * (size_t)(A.neq > 0 ? A.neq : 1);
+    const size_t bi = sizeof(double) * (size_t)(A.nin > 0 ? A.nin : 1);
+    TRY(A.lam.ensure(be, true)); TRY(A.hv.ensure(be, true)); TRY(A.weq.ensure(be, true));
+    TRY(A.mu.ensure(bi, true)); TRY(A.gv.ensure(bi, true)); TRY(A.win.ensure(bi, true));
+    TRY(A.tmp.ensure(sizeof(double) * (size_t)n));
+    TRY(A.scal.ensure(sizeof(double) * 4, true));
+    if (A.m_eq) {
+        TRY(A.erhs.ensure(sizeof(double) * (size_t)A.m_eq));
+        CK(cudaMemcpyAsync(A.erhs.p, cons->e, sizeof(double) * A.m_eq, cudaMemcpyHostToDevice, st));
+    }
+    if (A.p_in) {
+        TRY(A.hrhs.ensure(sizeof(double) * (size_t)A.p_in));
+        CK(cudaMemcpyAsync(A.hrhs.p, cons->hv, sizeof(double) * A.p_in, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMallocHost(&A.sh, sizeof(double) * 4));
+    struct PinFree { double* p; ~PinFree() { if (p) cudaFreeHost(p); } } pin_guard{A.sh};
+    // x^0 = clip(0), lambda = mu = 0 (R19); warm start: the given x (clipped), lambda, mu
+    if (!ao.warm_start) {
+        CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+    } else {
+        if (A.neq) CK(cudaMemcpyAsync(A.lam.p, lambda, be, cudaMemcpyHostToDevice, st));
+        if (A.nin) CK(cudaMemcpyAsync(A.mu.p, mu, bi, cudaMemcpyHostToDevice, st));
+    }
+    lbfgsb_objective cbo{};
+    cbo.kind = 1;
+    cbo.fg = al_gen_fg;
+    cbo.user = &A;
+    {
+        Prob P;
+        TRY(make_prob(h, &cbo, P));
+        CK(cudaMemcpyAsync(P.x, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        launch_clip(P, st);
+        CK(cudaMemcpyAsync(x, P.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    }
+    double rho = ao.rho0;
+    auto violation = [&](double* v) -> lbfgsb_err {
+        launch_al_violation(A.neq, A.hv.d(), A.nin, A.gv.d(), A.mu.d(), rho, A.scal.d() + 2, st);
+        CK(cudaMemcpyAsync(A.sh + 2, A.scal.d() + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        *v = A.sh[2];
+        return LBFGSB_OK;
+    };
+    if (A.values(x) != 0) return fail(LBFGSB_ERR_CALLBACK, "constraint callback failed at x0");
+    double vprev = 0.0;
+    TRY(violation(&vprev));
+    const double tol = h->o.tol;
+    al_result R{};
+    R.status = AL_MAX_OUTER;
+    for (int it = 0; it < ao.max_outer; ++it) {
+        const double tin = 0.1 * vprev > tol ? 0.1 * vprev : tol;          // R22
+        A.rho = rho;
+        lbfgsb_result ir{};
+        lbfgsb_err e = solve_cb(h, &cbo, x, tin, &ir);                     // Alg. 4 line 5
+        if (e != LBFGSB_OK) return A.cb_fail ? fail(LBFGSB_ERR_CALLBACK, "objective / constraint callback failed") : e;
+        R.inner_iters_total += ir.iters;
+        R.outer_iters = it + 1;
+        R.pg_inf = ir.pg_inf;
+        if (ir.status == LBFGSB_LINESEARCH_FAILURE) { R.status = AL_INNER_FAILURE; break; }
+        if (A.values(x) != 0) return fail(LBFGSB_ERR_CALLBACK, "constraint callback failed");
+        launch_al_update(A.neq, A.hv.d(), A.lam.d(), A.nin, A.gv.d(), A.mu.d(), rho, A.scal.d() + 2, st);  // lines 6-7
+        CK(cudaMemcpyAsync(A.sh + 2, A.scal.d() + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double v = A.sh[2];
+        if (v > 0.5 * vprev) {                                             // line 8 (R20)
+            rho = rho * ao.rho_factor;
+            if (rho > ao.rho_cap) rho = ao.rho_cap;
+        }
+        vprev = v;
+        if (ir.status == LBFGSB_CONVERGED && v <= ao.feas_tol && tin == tol) {
+            R.status = LBFGSB_CONVERGED;
+            break;
+        }
+    }
+    // the original objective f(x) (no AL terms) and the final violation
+    {
+        double fcb = 0.0;
+        if (A.base_fg(x, A.tmp.d(), &fcb) != 0) return fail(LBFGSB_ERR_CALLBACK, "objective callback failed");
+        CK(cudaMemcpyAsync(A.sh, A.scal.d(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        R.f = obj->kind == 1 ? fcb : A.sh[0];
+        if (A.values(x) != 0) return fail(LBFGSB_ERR_CALLBACK, "constraint callback failed");
+        TRY(violation(&R.violation_inf));
+    }
+    R.rho = rho;
+    if (lambda && A.neq) CK(cudaMemcpyAsync(lambda, A.lam.p, sizeof(double) * A.neq, cudaMemcpyDeviceToHost, st));
+    if (mu && A.nin) CK(cudaMemcpyAsync(mu, A.mu.p, sizeof(double) * A.nin, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     if (res) *res = R;
     return LBFGSB_OK;
 }

@@ -54,7 +54,8 @@ MUTANTS = {
         [("    double alpha = amax < 1.0 ? amax : 1.0;\n    double xw", "    double alpha = amax;\n    double xw")],
         [pins.check_armijo_lsq_examples]),
     "armijo_simple_decrease": (
-        [("        if (ft <= f + o->c1 * alpha * gp) {", "        if (ft < f) {")],
+        [("        if (ft <= f + o->c1 * alpha * gp) {\n            *f_out = ft;",
+          "        if (ft < f) {\n            *f_out = ft;")],
         [pins.check_armijo_lsq_random]),
     "armijo_shrinks_before_first_trial": (
         [("    for (int32_t t = 0; t <= o->max_backtracks; ++t) {\n        if (t > 0) alpha = o->shrink * alpha;\n"
