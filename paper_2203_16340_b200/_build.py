@@ -60,5 +60,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(out: str, defines: list[str], verbose: bool = False) -> str:
+    """A/B experiments only: the same sources with extra -D flags into `out`."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    cmd = [nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-I", os.path.join(ROOT, "include"),
+           *cu, "-o", out]
+    nccl = _nccl_dirs()
+    if nccl:
+        inc, lib = nccl
+        cmd += ["-DLBFGSB_WITH_NCCL", "-I", inc, "-L", lib, "-l:libnccl.so.2",
+                "-Xlinker", "-rpath", "-Xlinker", lib]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

@@ -25,6 +25,12 @@ constexpr int NTB = 512;                // threads of k_bwd_s (one CTA per SM)
 constexpr int EPI_TILE = 256;           // epilogue tile rows
 constexpr int BWD_SMEM_MAX = 210 * 1024;   // dynamic; + ~10 KB static <= 227 KB per CTA
 
+#ifndef BWD_UNR
+#define BWD_UNR 1              // row pairs per trip of the generic k_bwd's column stream
+#endif
+#ifndef BWD_MINB
+#define BWD_MINB 4             // resident CTAs per SM of the generic k_bwd (register cap)
+#endif
 // ---------------------------------------------------------------- column dots
 // acc[c] += sum over this thread's rows of M[i, jg + c] * r'_i, rows
 // i = 2 tid + 2 blockDim k (row pairs), two row pairs per loop trip.
@@ -76,7 +82,44 @@ __device__ __forceinline__ void col_dots_glob(const double* __restrict__ M0, int
                                               bool iter, bool wr, double* rnext, int64_t i0, int64_t i1,
                                               double* acc)
 {
-    for (int64_t i = 2 * (int64_t)threadIdx.x; i < m; i += 2 * (int64_t)blockDim.x) {
+    int64_t i = 2 * (int64_t)threadIdx.x;
+#if BWD_UNR > 1
+    // two row pairs per trip (16 independent 16-byte loads in flight per thread); the
+    // per-column summation order is that of the one-pair loop below (rows ascending)
+    if (VEC) {
+        const int64_t step = 2 * (int64_t)blockDim.x;
+        for (; i + step + 1 < m; i += 2 * step) {
+            double2 rr0 = *reinterpret_cast<const double2*>(rcur + i);
+            double2 rr1 = *reinterpret_cast<const double2*>(rcur + i + step);
+            if (iter) {
+                const double2 q0 = *reinterpret_cast<const double2*>(qv + i);
+                const double2 q1 = *reinterpret_cast<const double2*>(qv + i + step);
+                rr0.x = fma(alpha, q0.x, rr0.x); rr0.y = fma(alpha, q0.y, rr0.y);
+                rr1.x = fma(alpha, q1.x, rr1.x); rr1.y = fma(alpha, q1.y, rr1.y);
+            }
+            if (wr) {
+                if (i >= i0 && i < i1) rnext[i] = rr0.x;
+                if (i + 1 >= i0 && i + 1 < i1) rnext[i + 1] = rr0.y;
+                if (i + step >= i0 && i + step < i1) rnext[i + step] = rr1.x;
+                if (i + step + 1 >= i0 && i + step + 1 < i1) rnext[i + step + 1] = rr1.y;
+            }
+            double2 a0[NC], a1[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                a0[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i));
+                a1[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + step));
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                acc[c] = fma(a0[c].x, rr0.x, acc[c]);
+                acc[c] = fma(a0[c].y, rr0.y, acc[c]);
+                acc[c] = fma(a1[c].x, rr1.x, acc[c]);
+                acc[c] = fma(a1[c].y, rr1.y, acc[c]);
+            }
+        }
+    }
+#endif
+    for (; i < m; i += 2 * (int64_t)blockDim.x) {
         const bool two = i + 1 < m;
         double r0, r1;
         if (VEC && two) {
@@ -837,7 +880,7 @@ __global__ void __launch_bounds__(NT, 1) k_qepi(Prob P, int mode)
 
 // ---------------------------------------------------------------- k_bwd (generic)
 template <bool VEC>
-__global__ void __launch_bounds__(NT, 4) k_bwd(Prob P, int mode, const double* rvec, double* gout)
+__global__ void __launch_bounds__(NT, BWD_MINB) k_bwd(Prob P, int mode, const double* rvec, double* gout)
 {
     Ctrl* C = P.ctrl;
     if (mode == BWD_ITER && halted(C)) return;
