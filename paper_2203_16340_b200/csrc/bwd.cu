@@ -26,7 +26,8 @@ constexpr int EPI_TILE = 256;           // epilogue tile rows
 constexpr int BWD_SMEM_MAX = 210 * 1024;   // dynamic; + ~10 KB static <= 227 KB per CTA
 
 #ifndef BWD_UNR
-#define BWD_UNR 1              // row pairs per trip of the generic k_bwd's column stream
+#define BWD_UNR 2              // row pairs per trip of the generic k_bwd's column stream (C5 chunk:
+                               // 3100 -> 2975 us per launch at 4 CTAs/SM, bitwise-identical sums)
 #endif
 #ifndef BWD_MINB
 #define BWD_MINB 4             // resident CTAs per SM of the generic k_bwd (register cap)
@@ -84,38 +85,45 @@ __device__ __forceinline__ void col_dots_glob(const double* __restrict__ M0, int
 {
     int64_t i = 2 * (int64_t)threadIdx.x;
 #if BWD_UNR > 1
-    // two row pairs per trip (16 independent 16-byte loads in flight per thread); the
-    // per-column summation order is that of the one-pair loop below (rows ascending)
+    // BWD_UNR row pairs per trip (BWD_UNR x NC independent 16-byte loads in flight per
+    // thread); the per-column summation order is that of the one-pair loop below (each
+    // thread's rows ascending), so the sums are bitwise those of BWD_UNR = 1
     if (VEC) {
+        constexpr int U = BWD_UNR;
         const int64_t step = 2 * (int64_t)blockDim.x;
-        for (; i + step + 1 < m; i += 2 * step) {
-            double2 rr0 = *reinterpret_cast<const double2*>(rcur + i);
-            double2 rr1 = *reinterpret_cast<const double2*>(rcur + i + step);
+        for (; i + (U - 1) * step + 1 < m; i += U * step) {
+            double2 rr[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) rr[u] = *reinterpret_cast<const double2*>(rcur + i + u * step);
             if (iter) {
-                const double2 q0 = *reinterpret_cast<const double2*>(qv + i);
-                const double2 q1 = *reinterpret_cast<const double2*>(qv + i + step);
-                rr0.x = fma(alpha, q0.x, rr0.x); rr0.y = fma(alpha, q0.y, rr0.y);
-                rr1.x = fma(alpha, q1.x, rr1.x); rr1.y = fma(alpha, q1.y, rr1.y);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const double2 qq = *reinterpret_cast<const double2*>(qv + i + u * step);
+                    rr[u].x = fma(alpha, qq.x, rr[u].x);
+                    rr[u].y = fma(alpha, qq.y, rr[u].y);
+                }
             }
             if (wr) {
-                if (i >= i0 && i < i1) rnext[i] = rr0.x;
-                if (i + 1 >= i0 && i + 1 < i1) rnext[i + 1] = rr0.y;
-                if (i + step >= i0 && i + step < i1) rnext[i + step] = rr1.x;
-                if (i + step + 1 >= i0 && i + step + 1 < i1) rnext[i + step + 1] = rr1.y;
-            }
-            double2 a0[NC], a1[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                a0[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i));
-                a1[c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + step));
+                for (int u = 0; u < U; ++u) {
+                    const int64_t k = i + u * step;
+                    if (k >= i0 && k < i1) rnext[k] = rr[u].x;
+                    if (k + 1 >= i0 && k + 1 < i1) rnext[k + 1] = rr[u].y;
+                }
             }
+            double2 av[U][NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                acc[c] = fma(a0[c].x, rr0.x, acc[c]);
-                acc[c] = fma(a0[c].y, rr0.y, acc[c]);
-                acc[c] = fma(a1[c].x, rr1.x, acc[c]);
-                acc[c] = fma(a1[c].y, rr1.y, acc[c]);
-            }
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    av[u][c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + u * step));
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    acc[c] = fma(av[u][c].x, rr[u].x, acc[c]);
+                    acc[c] = fma(av[u][c].y, rr[u].y, acc[c]);
+                }
         }
     }
 #endif

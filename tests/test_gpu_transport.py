@@ -90,33 +90,35 @@ def _sinkhorn_torch(M, u, v, lam, iters=5000):
     return a[:, None] * K * b[None, :]
 
 
-@pytest.mark.parametrize("n,tol", [(200, 1e-9), (1000, 2e-6)])
-def test_entropy_ds2_vs_sinkhorn(lb, n, tol):
+@pytest.mark.parametrize("n,tol,prel", [(200, 1e-9, 1e-6), (400, 1e-8, 2e-5), (1000, 2e-6, 3e-3)])
+def test_entropy_ds2_vs_sinkhorn(lb, n, tol, prel):
     """Full-scale invariants: the entropic optimum is the Sinkhorn scaling of
     exp(-M / lam) for any cost (stationarity with P > 0); DS2 n = 1000 is
     2 * 10^6 variables and 3000 constraints.  At n = 1000 the
     smallest marginals are ~1e-7, so the multiplier iteration of Alg. 4
-    contracts by ~1 / (1 + rho u_min / lam) per outer step and rho ~ 1e6 makes
+    contracts by ~1 / (1 + rho u_min / lam) per outer step and rho ~ 5e5 makes
     the inner problems stiff: the test runs at tol = feas_tol = 2e-6
     (N2 notes).  The epsilon of Eq. (1) must sit below the scale of
-    the entries (~1e-11 in the smallest rows): eps = 1e-20 (reading R30)."""
+    the entries (~1e-11 in the smallest rows): eps = 1e-20 (reading R30).
+    The optimum is strictly interior: every entry must end above the R30
+    lower bound 1e-300 with |gradient| <= 2 tol (no entry may sit on the
+    bound), and P agrees with Sinkhorn to `prel` of max P (measured on B200:
+    8.6e-11 / 3.0e-5 at n = 400, tol 1e-8; 5.3e-9 / 4.7e-6 at n = 1000, tol 2e-6)."""
     import synth
     t = synth.transport_ds2(n, 9)
     r, X, lamg = _gpu(lb, t.cost, t.u, t.v, "entropy", t.lam, tol, max_outer=60, eps=1e-20)
     assert r.status == lb.CONVERGED, r
     assert np.allclose(X.sum(1), t.u, atol=2 * tol) and np.allclose(X.sum(0), t.v, atol=2 * tol)
-    # KKT of the inner problem with the updated multipliers (Alg. 4 line 6):
-    # g = M + lam (log P + 1) + l_i + l_{m+j}; |g| <= tol where P is above its
-    # lower bound (R30), g >= 0 where an iterate sits on it
+    # stationarity of the inner problem with the updated multipliers (Alg. 4 line 6):
+    # |M + lam (log P + 1) + l_i + l_{m+j}| <= tol on EVERY entry (all entries are free)
     m = t.m
+    assert np.all(X > 1e-290)
     G = t.cost + t.lam * (np.log(X) + 1.0) + lamg[:m, None] + lamg[None, m:]
-    at_lb = X <= 1e-290
-    assert np.max(np.abs(G[~at_lb])) <= 2 * tol
-    assert np.all(G[at_lb] >= -2 * tol)
-    Ps = _sinkhorn_torch(_cuda(t.cost), _cuda(t.u), _cuda(t.v), t.lam).cpu().numpy()
-    assert np.max(np.abs(X - Ps)) <= (1e-6 if tol < 1e-8 else 2e-2) * Ps.max()
+    assert np.max(np.abs(G)) <= 2 * tol
+    Ps = _sinkhorn_torch(_cuda(t.cost), _cuda(t.u), _cuda(t.v), t.lam, iters=20000).cpu().numpy()
+    assert np.max(np.abs(X - Ps)) <= prel * Ps.max()
     fstar = float(np.sum(t.cost * Ps) + t.lam * np.sum(Ps * np.log(Ps)))
-    assert abs(r.f - fstar) <= (1e-8 if tol < 1e-8 else 1e-4) * abs(fstar)
+    assert abs(r.f - fstar) <= (1e-8 if tol < 1e-7 else 1e-5) * abs(fstar)
 
 
 def test_gaussian_ds1_kkt(lb):
