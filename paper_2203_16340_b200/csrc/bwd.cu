@@ -26,11 +26,12 @@ constexpr int EPI_TILE = 256;           // epilogue tile rows
 constexpr int BWD_SMEM_MAX = 210 * 1024;   // dynamic; + ~10 KB static <= 227 KB per CTA
 
 #ifndef BWD_UNR
-#define BWD_UNR 2              // row pairs per trip of the generic k_bwd's column stream (C5 chunk:
-                               // 3100 -> 2975 us per launch at 4 CTAs/SM, bitwise-identical sums)
+#define BWD_UNR 4              // row pairs per trip of the generic k_bwd's column stream: 32 x 16-byte
+                               // loads in flight per thread; C5 chunk 3070 -> 2845 us per launch
+                               // (6.5 -> 7.0 TB/s), bitwise-identical sums (profiles/r02_gemv_ab.txt)
 #endif
 #ifndef BWD_MINB
-#define BWD_MINB 4             // resident CTAs per SM of the generic k_bwd (register cap)
+#define BWD_MINB 2             // resident CTAs per SM of the generic k_bwd (128-register cap)
 #endif
 // ---------------------------------------------------------------- column dots
 // acc[c] += sum over this thread's rows of M[i, jg + c] * r'_i, rows
