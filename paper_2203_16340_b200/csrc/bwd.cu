@@ -462,8 +462,17 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
 // of the next basis is accumulated PER WARP (lane l owns entries l, l+32, ..;
 // warp-private smem partials, __syncwarp only), so no CTA barrier interrupts
 // the column stream; the CTA sums its warps' partials in warp order once.
+#ifndef BWDW_WRS
+#define BWDW_WRS 4             // row steps of 64 rows per trip of k_bwd_w's column stream
+#endif
+#ifndef BWDW_PRED
+#define BWDW_PRED 0            // 1: the last partial trip is one predicated batch (zeros beyond m)
+#endif
+#ifndef BWDW_MINB
+#define BWDW_MINB 3            // resident CTAs per SM of k_bwd_w (register cap)
+#endif
 constexpr int WCOL = 4;
-constexpr int WRS = 4;                          // row steps of 64 rows per trip
+constexpr int WRS = BWDW_WRS;                   // row steps of 64 rows per trip
 constexpr int WROWS = WCOL * 2;                 // tile rows per warp (split: 2 vars per column)
 constexpr int WTILE = (NT / 32) * WROWS;        // tile rows per CTA
 constexpr int WG_STRIDE = MAXE + MAXH + 1;      // per-warp Gram partial slots (max; launch passes the m_hist size)
@@ -491,6 +500,32 @@ __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int
             }
         }
     }
+#if BWDW_PRED
+    // the remaining (< WRS) row steps as ONE batch of loads: rows >= m contribute exact zeros,
+    // so every column sees the same additions in the same order as the one-step loop below
+    if (i < m) {
+        double2 av[WRS][NC];
+        double2 rv[WRS];
+#pragma unroll
+        for (int u = 0; u < WRS; ++u) {
+            const int64_t k = i + 64 * u;
+            const bool full = k + 1 < m, half = k < m;
+            rv[u] = full ? *reinterpret_cast<const double2*>(rs + k) : make_double2(half ? rs[k] : 0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                av[u][c] = full ? __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + k))
+                                : make_double2(half ? __ldcs(M0 + c * ld + k) : 0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < WRS; ++u)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                acc[c] = fma(av[u][c].x, rv[u].x, acc[c]);
+                acc[c] = fma(av[u][c].y, rv[u].y, acc[c]);
+            }
+        return;
+    }
+#endif
     for (; i < m; i += 64) {
         if (i + 1 < m) {
 #pragma unroll
@@ -506,7 +541,7 @@ __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) k_bwd_w(Prob P, int mode, const double* rvec, double* gout, int mpad,
+__global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const double* rvec, double* gout, int mpad,
                                                 int wgs)
 {
     Ctrl* C = P.ctrl;

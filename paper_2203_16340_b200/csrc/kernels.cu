@@ -215,6 +215,9 @@ __device__ void reduce_sep(const Prob& P, int ntr, double* buf, int bufn, double
 // : p_j) * colscale_j.  p[S-bar] = 0 in both Alg. 2 branches, so fixed
 // variables cost no HBM traffic.  Row-block tail: q_i = sum_chunk (chunk
 // order), Armijo trial sums over the block's rows.  Global tail: decision.
+#ifndef FWD_SHORT_B
+#define FWD_SHORT_B 8          // load batch (active columns) of the short-column (MINB = 1) k_fwd
+#endif
 template <bool VEC, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double* pvec, double* qout)
 {
@@ -273,11 +276,12 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         nact_total += nact;
         const double* Mc = P.M + c0 * ld + row;
         int a = 0;
-        for (; a + 8 <= nact; a += 8) {
-            double2 v2[8];
-            double s2[8];
+        constexpr int FB = MINB == 1 ? FWD_SHORT_B : 8;          // active columns per load batch
+        for (; a + FB <= nact; a += FB) {
+            double2 v2[FB];
+            double s2[FB];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < FB; ++e) {
                 const double* ptr = Mc + (int64_t)lidx[a + e] * ld;
                 if (VEC && r1ok) {
                     v2[e] = __ldcs(reinterpret_cast<const double2*>(ptr));
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
                 s2[e] = lval[a + e];
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < FB; ++e) {
                 acc0 = fma(v2[e].x, s2[e], acc0);
                 acc1 = fma(v2[e].y, s2[e], acc1);
             }
