@@ -488,6 +488,8 @@ def run_c5(args) -> int:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
     m, n, C = C5_M, C5_N, C5_CHUNKS
+    if args.c5_shape:                      # smoke tests of the N > 1 path on small boxes only
+        m, n = (int(v) for v in args.c5_shape.split(","))
     stream = torch.cuda.Stream(device=dev)
 
     def mx(v):
@@ -687,8 +689,9 @@ def run_c5(args) -> int:
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (C5: A_ij = (u_ij - 1/2) sqrt(12/m), u from Philox4x32-10 on the device; "
                         "x_plant 10% |N(0,1)|, b = A x_plant + 0.1 z; SURVEY 8(d))",
-                "config": {"workload": "C5: column-sharded NNLS m=100000 n=200000 fp64, x>=0, m_hist=5, "
-                                       "tol 1e-6 (BASELINE.json configs[4]), strong scaling",
+                "config": {"workload": (f"C5: column-sharded NNLS m={m} n={n} fp64, x>=0, m_hist=5, "
+                                        "tol 1e-6 (BASELINE.json configs[4]), strong scaling"
+                                        + ("" if (m, n) == (C5_M, C5_N) else " -- SHRUNKEN SMOKE SHAPE, not a bench")),
                            "m": m, "n_global": n, "chunks": C, "chunks_per_gpu": len(mine), "m_hist": M_HIST,
                            "tol": TOL, "seed": C5_SEED, "A_bytes": 8 * m * n,
                            "l2": "inputs larger than L2 (A = 160 GB); no flush",
@@ -732,6 +735,7 @@ def main():
     ap.add_argument("--config", choices=["C5", "C2"], default="C5",
                     help="C5 (default): BASELINE configs[4], strong scaling at every N; C2: configs[1], N=1")
     ap.add_argument("--no-c2", action="store_true", help="C5 at N=1 without the embedded C2 measurement")
+    ap.add_argument("--c5-shape", default=None, help=argparse.SUPPRESS)   # "m,n": shrunken C5, smoke tests only
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 5 if args.config == "C5" else 30

@@ -466,10 +466,12 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
 #define BWDW_WRS 4             // row steps of 64 rows per trip of k_bwd_w's column stream
 #endif
 #ifndef BWDW_PRED
-#define BWDW_PRED 0            // 1: the last partial trip is one predicated batch (zeros beyond m)
+#define BWDW_PRED 1            // the last partial trip is one predicated batch (zeros beyond m): C4
+                               // 1000 x 100000 k_bwd_w 177 -> 162 us with BWDW_MINB 2 (profiles/r02_gemv_ab_c4.txt)
 #endif
 #ifndef BWDW_MINB
-#define BWDW_MINB 3            // resident CTAs per SM of k_bwd_w (register cap)
+#define BWDW_MINB 2            // resident CTAs per SM of k_bwd_w (128-register cap: no spill in the
+                               // predicated trip; 3 CTAs/SM at 80 registers gained nothing)
 #endif
 constexpr int WCOL = 4;
 constexpr int WRS = BWDW_WRS;                   // row steps of 64 rows per trip
@@ -1573,7 +1575,10 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         k_bwd_w<<<Gw, NT, sm, st>>>(P, mode, rvec, gout, mpad, wgs);
         return;
     }
-    if (smem && P.m >= 2048) {
+#ifndef BWD_S_ENABLE
+#define BWD_S_ENABLE 1         // 0: the generic k_bwd also for 2048 <= m <= ~24K (A/B builds)
+#endif
+    if (BWD_S_ENABLE && smem && P.m >= 2048) {
         const int64_t cmax = (P.ncols + Gs_ - 1) / Gs_;
         const int64_t mpad = (int64_t)(smem / sizeof(double)) - cmax - 1;
         k_bwd_s<<<Gs_, NTB, smem, st>>>(P, mode, rvec, gout, mpad, (int)cmax);
