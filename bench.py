@@ -480,6 +480,7 @@ def run_c5(args) -> int:
     from paper_2203_16340_b200 import sharded
 
     ws, rank, local = _dist()
+    local = local % max(torch.cuda.device_count(), 1)      # (several ranks per GPU: smoke tests only)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -597,8 +598,14 @@ def run_c5(args) -> int:
     clocks = clk.summary()
     all_reasons = (sharded.all_gather_bytes(json.dumps(clocks.get("reasons", [])).encode())
                    if ws > 1 else [json.dumps(clocks.get("reasons", []))])
-    x_sum = float(sum(float(x.sum()) for x in xs))
-    x_sum = sum(float(v) for v in (sharded.all_gather_bytes(repr(x_sum).encode()) if ws > 1 else [repr(x_sum)]))
+    # checksum of x* summed chunk by chunk in logical-chunk order (the same grouping at every N)
+    csum = {l: float(x.sum()) for l, x in zip(mine, xs)} if xchg == "p2p" else {mine[0]: float(xs[0].sum())}
+    if ws > 1:
+        for blob in sharded.all_gather_bytes(json.dumps(csum).encode()):
+            csum.update({int(k): v for k, v in json.loads(blob).items()})
+    x_sum = 0.0
+    for l in sorted(csum):
+        x_sum += csum[l]
 
     # ---- e2e through the public API with host inputs: per step b and x0 from pinned host
     # memory, A regenerated on the device from the seed (the data set is the generator), the

@@ -35,6 +35,8 @@ def sources():
 
 
 def needs_build() -> bool:
+    if os.environ.get("LBFGSB_NO_AUTOBUILD"):        # A/B runs against a prebuilt variant library
+        return False
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
