@@ -57,7 +57,7 @@ def test_c3_full_size_lasso_en(lb, alpha):
     assert max(pgu.max(), pgv.max()) <= 2e-6
     if alpha == 1.0:
         # lasso optimality: |A_j^T res| <= lam off the support (subgradient), = lam on it
-        on = np.abs(w[idx]) > 0
+        on = np.abs(w[idx]) > 1e-8          # Eq. (1): entries within eps of the bound count as at it
         assert np.all(np.abs(at[~on]) <= lam + 2e-6)
         assert np.all(np.abs(np.abs(at[on]) - lam) <= 2e-6)
 
