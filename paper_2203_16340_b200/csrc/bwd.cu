@@ -36,12 +36,35 @@ constexpr int BWD_SMEM_MAX = 210 * 1024;   // dynamic; + ~10 KB static <= 227 KB
 // ---------------------------------------------------------------- column dots
 // acc[c] += sum over this thread's rows of M[i, jg + c] * r'_i, rows
 // i = 2 tid + 2 blockDim k (row pairs), two row pairs per loop trip.
+#ifndef BWDS_UNR
+#define BWDS_UNR 2             // row pairs per trip of k_bwd_s's column stream (2 or 4)
+#endif
 template <int NC, bool TWO = true>
 __device__ __forceinline__ void col_dots_smem(const double* __restrict__ M0, int64_t ld, int64_t m,
                                               const double* rs, double* acc)
 {
     const int64_t step = 2 * (int64_t)blockDim.x;
     int64_t i = 2 * (int64_t)threadIdx.x;
+#if BWDS_UNR > 2
+    // BWDS_UNR row pairs per trip (rows ascending per thread: the one-pair summation order)
+    for (; TWO && i + (BWDS_UNR - 1) * step + 1 < m; i += BWDS_UNR * step) {
+        double2 a[BWDS_UNR][NC];
+#pragma unroll
+        for (int u = 0; u < BWDS_UNR; ++u)
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                a[u][c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + u * step));
+#pragma unroll
+        for (int u = 0; u < BWDS_UNR; ++u) {
+            const double2 r = *reinterpret_cast<const double2*>(rs + i + u * step);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                acc[c] = fma(a[u][c].x, r.x, acc[c]);
+                acc[c] = fma(a[u][c].y, r.y, acc[c]);
+            }
+        }
+    }
+#endif
     for (; TWO && i + step + 1 < m; i += 2 * step) {
         double2 a0[NC], a1[NC];
 #pragma unroll
