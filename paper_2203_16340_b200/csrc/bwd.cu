@@ -37,7 +37,8 @@ constexpr int BWD_SMEM_MAX = 210 * 1024;   // dynamic; + ~10 KB static <= 227 KB
 // acc[c] += sum over this thread's rows of M[i, jg + c] * r'_i, rows
 // i = 2 tid + 2 blockDim k (row pairs), two row pairs per loop trip.
 #ifndef BWDS_UNR
-#define BWDS_UNR 2             // row pairs per trip of k_bwd_s's column stream (2 or 4)
+#define BWDS_UNR 3             // row pairs per trip of k_bwd_s's column stream: C2 263.7 -> 261.2 us
+                               // (4: 264.9 us); profiles/r02_gemv_ab_c2.txt
 #endif
 template <int NC, bool TWO = true>
 __device__ __forceinline__ void col_dots_smem(const double* __restrict__ M0, int64_t ld, int64_t m,
@@ -496,7 +497,10 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
 #define BWDW_MINB 2            // resident CTAs per SM of k_bwd_w (128-register cap: no spill in the
                                // predicated trip; 3 CTAs/SM at 80 registers gained nothing)
 #endif
-constexpr int WCOL = 4;
+#ifndef BWDW_WCOL
+#define BWDW_WCOL 4            // columns per warp group of k_bwd_w (4 or 8)
+#endif
+constexpr int WCOL = BWDW_WCOL;
 constexpr int WRS = BWDW_WRS;                   // row steps of 64 rows per trip
 constexpr int WROWS = WCOL * 2;                 // tile rows per warp (split: 2 vars per column)
 constexpr int WTILE = (NT / 32) * WROWS;        // tile rows per CTA
@@ -628,9 +632,17 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
     for (int64_t grp = w; grp < ngroups; grp += nw) {
         const int64_t jg = j0 + grp * WCOL;
         const int nc = (int)(j1 - jg < WCOL ? j1 - jg : WCOL);
-        double acc[WCOL] = {0.0, 0.0, 0.0, 0.0};
+        double acc[WCOL];
+#pragma unroll
+        for (int c = 0; c < WCOL; ++c) acc[c] = 0.0;
         const double* M0 = P.M + jg * ld;
         switch (nc) {
+#if BWDW_WCOL > 4
+            case 8: warp_col_dots<8>(M0, ld, m, rs, acc); break;
+            case 7: warp_col_dots<7>(M0, ld, m, rs, acc); break;
+            case 6: warp_col_dots<6>(M0, ld, m, rs, acc); break;
+            case 5: warp_col_dots<5>(M0, ld, m, rs, acc); break;
+#endif
             case 4: warp_col_dots<4>(M0, ld, m, rs, acc); break;
             case 3: warp_col_dots<3>(M0, ld, m, rs, acc); break;
             case 2: warp_col_dots<2>(M0, ld, m, rs, acc); break;
@@ -646,9 +658,9 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
             if (lane < nc * nvg) {
                 const int jj = lane % nc, vv = lane / nc;
                 double dot = acc[0];
-                if (jj == 1) dot = acc[1];
-                if (jj == 2) dot = acc[2];
-                if (jj == 3) dot = acc[3];
+#pragma unroll
+                for (int c = 1; c < WCOL; ++c)
+                    if (jj == c) dot = acc[c];
                 const int64_t j = jg + jj;
                 double dval = vv ? -dot : dot;
                 if (P.colscale) dval = P.colscale[j] * dot;

@@ -87,6 +87,31 @@ def local_chunks(nchunks: int, world: int, rank: int) -> list[int]:
     return list(range(rank * k, (rank + 1) * k))
 
 
+def merge_chunk_handles(parts: list, nchunks: int, complete: bool = True) -> list:
+    """Merge the {logical rank: IPC handle} dicts of all processes into the C
+    handles in logical-rank order; a chunk hosted twice (or, with `complete`,
+    a chunk hosted nowhere) is an error."""
+    allh = {}
+    for part in parts:
+        dup = set(part) & set(allh)
+        if dup:
+            raise ValueError(f"chunks {sorted(dup)} hosted twice")
+        allh.update(part)
+    if complete and sorted(allh) != list(range(nchunks)):
+        raise ValueError(f"chunks not covered: {sorted(set(range(nchunks)) - set(allh))}")
+    return [allh.get(l, bytes(64)) for l in range(nchunks)]
+
+
+def gather_chunk_handles(mine: dict, nchunks: int, world: int) -> list:
+    """Every process contributes {logical rank: 64-byte IPC handle} for the chunks
+    it hosts; returns the C handles in logical-rank order (all-gathered over the
+    default torch.distributed group when world > 1)."""
+    import pickle
+    if world == 1:
+        return merge_chunk_handles([mine], nchunks, complete=False)
+    return merge_chunk_handles([pickle.loads(b) for b in all_gather_bytes(pickle.dumps(mine))], nchunks)
+
+
 class ShardedGroup:
     """SURVEY 8(e) bitwise P-invariance: the global problem is cut into
     ``nchunks`` (C) fixed column chunks -- logical ranks, each a P2P-sharded
@@ -114,17 +139,10 @@ class ShardedGroup:
             self.solvers.append(lb.Solver(c1 - c0, m_hist, lower=lo, upper=up, opts=opts, stream=stream,
                                           rank=l, nranks=nchunks, n_global=ncols, p2p_m_max=int(m_max)))
         mine = {l: s.ipc_handle() for l, s in zip(self.local, self.solvers)}
-        if world > 1:
-            import pickle
-            import torch.distributed as dist
-            allh = {}
-            for blob in all_gather_bytes(pickle.dumps(mine)):
-                allh.update(pickle.loads(blob))
-        else:
-            allh = mine
-        handles = [allh.get(l, bytes(64)) for l in range(nchunks)]
+        handles = gather_chunk_handles(mine, nchunks, world)
         lb.p2p_open_group(self.solvers, handles)
         if world > 1:
+            import torch.distributed as dist
             dist.barrier()                 # every mailbox mapped before anyone signals
 
     def solve(self, objs, xs, tol=0.0):

@@ -125,3 +125,65 @@ def test_local_chunks_partition():
     # the chunk ranges do not depend on the process count
     rng = [column_range(200000, 8, l) for l in range(8)]
     assert rng[0] == (0, 25000) and rng[-1] == (175000, 200000)
+
+
+def _group_worker(rank, world, port, out):
+    import pickle
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2203_16340_b200 import sharded
+    import oracle
+    C = 8
+    mine = sharded.local_chunks(C, world, rank)
+    # 1) the IPC-handle exchange of ShardedGroup: every process gets all C handles in chunk order
+    hs = sharded.gather_chunk_handles({l: bytes([l]) * 64 for l in mine}, C, world)
+    # 2) the chunk-ordered reduction that makes the solve P-invariant (R36): q = sum over the C fixed
+    #    chunks, in chunk order, of the chunk's partial A_l p_l
+    m, n = 50, 83
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((m, n))
+    p = rng.standard_normal(n)
+    parts = {}
+    for l in mine:
+        c0, c1 = sharded.column_range(n, C, l)
+        parts[l] = oracle.matvec(A[:, c0:c1], p[c0:c1])
+    allp = {}
+    for blob in sharded.all_gather_bytes(pickle.dumps(parts)):
+        allp.update(pickle.loads(blob))
+    q = np.zeros(m)
+    for l in range(C):
+        q = q + allp[l]
+    out[rank] = dict(hs=hs, q_bits=q.tobytes())
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_group_host_logic():
+    """world_size 2 (gloo): the P-invariant group's handle exchange and its
+    chunk-ordered reduction give every process the same handles and the same
+    bits, equal to the single-process (world 1) result."""
+    from paper_2203_16340_b200 import sharded
+    import oracle
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_group_worker, args=(world, port, out), nprocs=world, join=True)
+    ref_h = [bytes([l]) * 64 for l in range(8)]
+    assert out[0]["hs"] == ref_h and out[1]["hs"] == ref_h
+    # world 1: the same chunks, the same order
+    m, n = 50, 83
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((m, n))
+    p = rng.standard_normal(n)
+    q = np.zeros(m)
+    for l in range(8):
+        c0, c1 = sharded.column_range(n, 8, l)
+        q = q + oracle.matvec(A[:, c0:c1], p[c0:c1])
+    assert out[0]["q_bits"] == out[1]["q_bits"] == q.tobytes()
+    # a chunk hosted twice, or a chunk hosted nowhere, is refused
+    with pytest.raises(ValueError):
+        sharded.merge_chunk_handles([{3: bytes(64)}, {3: bytes(64)}], 8)
+    with pytest.raises(ValueError):
+        sharded.merge_chunk_handles([{l: bytes(64) for l in range(7)}], 8)
