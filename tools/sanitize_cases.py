@@ -57,6 +57,27 @@ def al():
     print("al", r.status, r.outer_iters)
 
 
+def algen():
+    """general Alg. 4: 24 linear equalities (GEMV kernels on E) + a nonlinear ball through callbacks"""
+    rng = np.random.default_rng(12)
+    m, n = 300, 150
+    A = rng.standard_normal((m, n)) / np.sqrt(m)
+    E = rng.standard_normal((n, 24)) / np.sqrt(n)
+    e = E.T @ np.abs(rng.standard_normal(n))
+    obj = lb.LSQObjective(lb.colmajor(A), b=torch.from_numpy(rng.standard_normal(m)).cuda())
+    s = lb.Solver(n, 5, lower=torch.zeros(n, dtype=torch.float64, device="cuda"))
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    R = 4.0 * float(np.abs(rng.standard_normal(n)) @ np.abs(rng.standard_normal(n)))
+
+    def hg(x, h, g):
+        g[0] = torch.dot(x, x) - R
+
+    def jtv(x, ve, vi, out):
+        out.copy_(2.0 * vi[0] * x)
+    r = s.al_solve(obj, x, E=torch.from_numpy(E).cuda(), e=e, hg=hg, jtv=jtv, p_nl=1)
+    print("algen", r.status, r.outer_iters)
+
+
 def loop3():
     from paper_2203_16340_b200.sharded import column_range
     p = synth.nnls_gaussian(900, 600, 7)
@@ -124,7 +145,7 @@ def transport():
         print("transport", reg, r.status, r.outer_iters)
 
 
-CASES = {f.__name__: f for f in (c1, c2s, c4s, lasso, al, loop3, group, batch, qp, transport)}
+CASES = {f.__name__: f for f in (c1, c2s, c4s, lasso, al, algen, loop3, group, batch, qp, transport)}
 
 if __name__ == "__main__":
     torch.cuda.init()
