@@ -91,6 +91,10 @@ typedef struct {
     int32_t armijo_diff;        /* 1: Armijo test on the exact expansion of f(x+a p) - f(x)
                                    (LSQ / QP objectives; reading R29, avoids the
                                    cancellation floor of f_t <= f + c1 a g^T p); default 0 */
+    int32_t refresh_every;      /* R > 0: the carried residual is replaced by r = M~x - b (and f, g
+                                   recomputed exactly) at the top of every iteration k with
+                                   k % R == 0, k > 0 (R13's optional refresh, for long runs);
+                                   0: only the final refresh.  LSQ / QP objectives; default 0 */
     int64_t max_iters;          /* default 10000                                        */
 } lbfgsb_opts;
 

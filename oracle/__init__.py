@@ -102,7 +102,7 @@ class _Opts(C.Structure):
     _fields_ = [("eps", C.c_double), ("c1", C.c_double), ("shrink", C.c_double),
                 ("tol", C.c_double), ("max_backtracks", C.c_int32),
                 ("screen_full_norm", C.c_int32), ("no_projection", C.c_int32),
-                ("armijo_diff", C.c_int32), ("max_iters", C.c_int64)]
+                ("armijo_diff", C.c_int32), ("refresh_every", C.c_int32), ("max_iters", C.c_int64)]
 
 
 class _Res(C.Structure):
@@ -325,6 +325,7 @@ class Options:
     max_iters: int = 10000
     no_projection: bool = False     # PAPER.md:201 variant
     armijo_diff: bool = False       # R29: Armijo on the expanded difference (N4)
+    refresh_every: int = 0          # R13: exact r, f, g every R iterations (0: only the final refresh)
 
 
 @dataclass
@@ -464,7 +465,7 @@ def minimize_lsq(P: LSQ, l=None, u=None, x0=None, m_hist=5, opts: Options | None
     l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
     u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               int(o.no_projection), int(o.armijo_diff), o.max_iters)
+               int(o.no_projection), int(o.armijo_diff), int(o.refresh_every), o.max_iters)
     res = _Res()
     s = P._struct()
     _L().orc_minimize_lsq(C.byref(s), _ptr(l), _ptr(u), m_hist, C.byref(so), _ptr(x),
@@ -483,7 +484,7 @@ def minimize_lsq_original(P: LSQ, l=None, u=None, x0=None, m_hist=5, opts: Optio
     l = None if l is None else _f64(np.broadcast_to(l, (P.nvars,)))
     u = None if u is None else _f64(np.broadcast_to(u, (P.nvars,)))
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               int(o.no_projection), int(o.armijo_diff), o.max_iters)
+               int(o.no_projection), int(o.armijo_diff), int(o.refresh_every), o.max_iters)
     res = _Res()
     tcp = C.c_double(0.0)
     s = P._struct()
@@ -526,7 +527,7 @@ def al_solve(P: LSQ, l=None, u=None, m_hist=5, opts: Options | None = None,
     if mu0 is not None:
         mu[:P.n_in] = mu0
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               int(o.no_projection), int(o.armijo_diff), o.max_iters)
+               int(o.no_projection), int(o.armijo_diff), int(o.refresh_every), o.max_iters)
     sa = _AlOpts(ao.feas_tol, ao.rho0, ao.rho_factor, ao.rho_cap, ao.max_outer)
     s = P._struct()
     res = _AlRes()
@@ -587,7 +588,7 @@ def armijo_lsq(P: LSQ, x, p, amax, l=None, u=None, opts: Options | None = None):
     g = P.grad(x)
     gp = float(np.dot(g, p))
     so = _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-               int(o.no_projection), int(o.armijo_diff), o.max_iters)
+               int(o.no_projection), int(o.armijo_diff), int(o.refresh_every), o.max_iters)
     xt = np.empty(P.nvars); rt = np.empty(max(P.m, 1))
     fo = C.c_double(0.0); ao = C.c_double(0.0); nbt = C.c_int64(0)
     s = P._struct()
@@ -639,7 +640,7 @@ def _setup_general(L):
 
 def _opts_c(o):
     return _Opts(o.eps, o.c1, o.shrink, o.tol, o.max_backtracks, int(o.screen_full_norm),
-                 int(o.no_projection), int(o.armijo_diff), o.max_iters)
+                 int(o.no_projection), int(o.armijo_diff), int(o.refresh_every), o.max_iters)
 
 
 def minimize_fg(fun, n, l=None, u=None, x0=None, m_hist=5, opts: Options | None = None):

@@ -411,6 +411,8 @@ typedef struct {
     int32_t max_backtracks, screen_full_norm;
     int32_t no_projection;       /* 1: Alg. 2 without the projected branch */
     int32_t armijo_diff;         /* 1: Armijo test on the expanded difference f_t - f (R29) */
+    int32_t refresh_every;       /* R > 0: r = M~x - b, f and g recomputed exactly at the top of
+                                    every iteration k with k % R == 0, k > 0 (R13's optional refresh) */
     int64_t max_iters;
 } orc_opts;
 
@@ -574,6 +576,11 @@ void orc_minimize_lsq(const orc_lsq* P, const double* l, const double* u, int32_
     int64_t k = 0;
     int32_t status = ORC_MAX_ITERS;
     for (;;) {
+        if (o->refresh_every > 0 && k > 0 && k % o->refresh_every == 0) {   /* R13 optional refresh */
+            lsq_residual(P, x, r);
+            f = quad_value(P, x, r) + lsq_phi(P, x, NULL, NULL);
+            lsq_grad(P, x, r, g);
+        }
         orc_working_set(nv, x, g, l, u, o->eps, fr);             /* Alg. 1 line 3 */
         double gfree = 0.0; int64_t nfree = 0;
         for (int64_t j = 0; j < nv; ++j)

@@ -775,10 +775,9 @@ static lbfgsb_err ensure_events(lbfgsb_t* h)
     return LBFGSB_OK;
 }
 
-static lbfgsb_err run_chunk(Group& g)
+static lbfgsb_err run_chunk(Group& g, int chunk)
 {
     lbfgsb_t* h = g.h0();
-    const int chunk = h->o.check_every;
     const bool graph = h->o.use_graph && !g.loopback;
     if (graph) {
         int sl = -1;
@@ -869,10 +868,14 @@ static lbfgsb_err solve_group(Group& g, double* const* xs, double tol, lbfgsb_re
     if (h->o.profile) TRY(ensure_events(h));
 
     const int64_t guard = h->o.max_iters + 64;
+    const int R = h->o.refresh_every > 0 ? h->o.refresh_every : 0;
     int64_t loops = 0;
     while (!h->hc->done) {
         const long long k0 = h->hc->k;
-        TRY(run_chunk(g));
+        // with a periodic refresh every chunk ends at the next multiple of R
+        int chunk = h->o.check_every;
+        if (R > 0 && R - (int)(k0 % R) < chunk) chunk = R - (int)(k0 % R);
+        TRY(run_chunk(g, chunk));
         TRY(ctrl_to_host(g));
         collect_profile(h, h->hc->k - k0);
         if (++loops > guard) return fail(LBFGSB_ERR_CUDA, "solver loop did not terminate");
@@ -895,6 +898,22 @@ static lbfgsb_err solve_group(Group& g, double* const* xs, double tol, lbfgsb_re
             if (g.Ps[0].p2p) launch_p2p_barrier(g.Ps.data(), (int)g.Ps.size(), g.st);
             if (s == ST_FALLBACK) TRY(launch_iteration(g, -1));
             else TRY(launch_ls_cont(g));
+            CK(cudaGetLastError());
+            TRY(ctrl_to_host(g));
+        }
+        // R13's optional refresh at the top of iteration k, k % R == 0: r = M~x - b, f, g, the
+        // working set, the convergence test and Alg. 3 again from the exact values (the setup
+        // sequence without the clip; the curvature pairs are kept)
+        if (R > 0 && !h->hc->done && h->hc->k > 0 && h->hc->k % R == 0 && h->hc->k != k0 &&
+            !g.Ps[0].tp && !h->hc->stall) {
+            if (g.Ps[0].p2p) launch_p2p_barrier(g.Ps.data(), (int)g.Ps.size(), g.st);
+            TRY(launch_fval(g, false));
+            FOR_RANKS launch_bwd(PR, g.st, BWD_SETUP, nullptr, nullptr);
+            if (g.sharded) {
+                TRY(xchg(g, SEC_GRAM));
+                FOR_RANKS launch_gram_decide(PR, g.st, BWD_SETUP);
+            }
+            h->launches += 4;
             CK(cudaGetLastError());
             TRY(ctrl_to_host(g));
         }

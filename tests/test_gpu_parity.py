@@ -248,6 +248,26 @@ def test_nnls_end_to_end_tall(lb, orc, m, n, seed):
     assert np.all(x >= 0.0)
 
 
+@pytest.mark.parametrize("R,check", [(3, 8), (5, 2), (1, 4)])
+def test_periodic_refresh_matches_oracle(lb, orc, R, check):
+    """opts.refresh_every (R13's optional refresh: exact r, f, g at the top of
+    every R-th iteration) against the oracle's refresh at the same iterations:
+    f after k = 1..6 iterations to 1e-12, the converged f to 1e-8; the chunks
+    of the replayed graph end at the multiples of R whatever check_every is."""
+    import synth
+    prob = synth.nnls_gaussian(2000, 1000, 23)
+    for k in range(1, 7):
+        r, ro, x = _solve_both(lb, orc, prob, opts=lb.Options(max_iters=k, tol=1e-12, refresh_every=R,
+                                                              check_every=check),
+                               oopts=orc.Options(max_iters=k, tol=1e-12, refresh_every=R))
+        assert r.iters == ro.iters == k
+        assert abs(r.f - ro.f) <= 1e-12 * abs(ro.f)
+    r, ro, x = _solve_both(lb, orc, prob, opts=lb.Options(refresh_every=R, check_every=check),
+                           oopts=orc.Options(refresh_every=R))
+    assert r.status == lb.CONVERGED and ro.status == orc.CONVERGED
+    assert abs(r.f - ro.f) <= 1e-8 * abs(ro.f) and r.pg_inf <= 1e-6
+
+
 def test_determinism_graph_vs_eager(lb):
     """Deterministic reductions: graph replay, eager launches and different
     host-check chunks give bit-identical results."""

@@ -298,3 +298,43 @@ def test_threaded_oracle_is_bit_identical(orc):
             assert np.array_equal(st.x, s1.x) and st.f == s1.f and st.iters == s1.iters
     finally:
         orc.set_threads(1)
+
+
+# ---------------------------------------------------------------- R13 optional refresh
+@pytest.mark.parametrize("R", [1, 3])
+def test_periodic_refresh_changes_only_rounding(orc, R):
+    """R13: the carried residual r + alpha q equals M~x' - b in exact arithmetic,
+    so refreshing r, f and g every R iterations leaves the trajectory unchanged
+    up to rounding: f after k = 1..6 iterations agrees with the refresh-free run
+    to 1e-12, and the optimum to 1e-12."""
+    import synth
+    p = synth.nnls_gaussian(150, 80, 17)
+    P = orc.LSQ(p.M, b=p.b)
+    for k in range(1, 7):
+        a = orc.minimize_lsq(P, l=p.lower, opts=orc.Options(max_iters=k, tol=1e-12))
+        b = orc.minimize_lsq(P, l=p.lower, opts=orc.Options(max_iters=k, tol=1e-12, refresh_every=R))
+        assert a.iters == b.iters == k
+        assert abs(a.f - b.f) <= 1e-12 * abs(a.f)
+    a = orc.minimize_lsq(P, l=p.lower)
+    b = orc.minimize_lsq(P, l=p.lower, opts=orc.Options(refresh_every=R))
+    assert a.status == b.status == orc.CONVERGED
+    assert abs(a.f - b.f) <= 1e-12 * abs(a.f)
+
+
+def test_periodic_refresh_removes_residual_drift(orc):
+    """A long run (a badly conditioned NNLS, ~hundreds of iterations): with the
+    refresh the reported f (recomputed from x at the end in both cases) is
+    unchanged while the refresh keeps the carried f exact at the refresh points
+    -- pinned through the final f against the refresh-free run and against
+    scipy's active-set NNLS optimum."""
+    from scipy.optimize import nnls
+    import synth
+    p = synth.nnls_ds1(0.1, 3)
+    P = orc.LSQ(p.M, b=p.b)
+    a = orc.minimize_lsq(P, l=p.lower, opts=orc.Options(max_iters=20000))
+    b = orc.minimize_lsq(P, l=p.lower, opts=orc.Options(max_iters=20000, refresh_every=10))
+    xs, rn = nnls(p.M, p.b, maxiter=100000)
+    fs = 0.5 * rn * rn
+    for r in (a, b):
+        assert r.status == orc.CONVERGED
+        assert abs(r.f - fs) <= 1e-8 * abs(fs)
