@@ -95,6 +95,10 @@ typedef struct {
                                    recomputed exactly) at the top of every iteration k with
                                    k % R == 0, k > 0 (R13's optional refresh, for long runs);
                                    0: only the final refresh.  LSQ / QP objectives; default 0 */
+    int32_t trials_per_pass;    /* Armijo trials alpha_0 beta^t decided per fused pass (1..16;
+                                   0 = 16): beyond them the host continues with the next batch.
+                                   The accepted trial does not depend on it (the trials are
+                                   sequential); it only moves the batch boundaries. default 0 */
     int64_t max_iters;          /* default 10000                                        */
 } lbfgsb_opts;
 

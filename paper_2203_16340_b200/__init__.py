@@ -35,7 +35,7 @@ class _Opts(C.Structure):
                 ("max_backtracks", _c_i32), ("screen_full_norm", _c_i32),
                 ("check_every", _c_i32), ("use_graph", _c_i32), ("profile", _c_i32),
                 ("no_projection", _c_i32), ("armijo_diff", _c_i32), ("refresh_every", _c_i32),
-                ("max_iters", _c_i64)]
+                ("trials_per_pass", _c_i32), ("max_iters", _c_i64)]
 
 
 class _Res(C.Structure):
@@ -192,12 +192,14 @@ class Options:
     no_projection: bool = False
     armijo_diff: bool = False       # R29: Armijo on the expanded difference f(x + a p) - f(x)
     refresh_every: int = 0          # R13: exact r, f, g every R iterations (0: final refresh only)
+    trials_per_pass: int = 0        # Armijo trials decided per fused pass (1..16; 0 = 16)
 
     def _c(self):
         return _Opts(self.eps, self.c1, self.shrink, self.tol, self.max_backtracks,
                      int(bool(self.screen_full_norm)), self.check_every, int(bool(self.use_graph)),
                      int(bool(self.profile)), int(bool(self.no_projection)),
-                     int(bool(self.armijo_diff)), int(self.refresh_every), self.max_iters)
+                     int(bool(self.armijo_diff)), int(self.refresh_every), int(self.trials_per_pass),
+                     self.max_iters)
 
 
 @dataclass

@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(BT) k_batch(BatchArgs B)
     if (tid == 0) {
         memset(&Ps, 0, sizeof(Prob));
         Ps.n = n; Ps.m = m; Ps.eps = B.eps; Ps.c1 = B.c1; Ps.shrink = B.shrink; Ps.max_bt = B.max_bt;
+        Ps.tpp = KT;                                    // the batched kernel decides KT trials per batch
         Ps.screen_full = B.screen_full; Ps.mh = mh; Ps.no_projection = B.no_projection;
         Ps.max_iters = B.max_iters;
         memset(C, 0, sizeof(Ctrl));

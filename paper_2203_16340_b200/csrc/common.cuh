@@ -485,9 +485,10 @@ __device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const doub
     const int ncons = P.n_eq + P.n_in;
     double a = C->alpha0;
     int tried = 0;
-    for (int t = 0; t < KT; ++t) {
+    const int tpp = P.tpp;                                     // trials decided per pass (<= KT)
+    for (int t = 0; t < tpp; ++t) {
         if (t > 0) a = a * P.shrink;
-        if (C->ls_batch * KT + t > P.max_bt) break;
+        if (C->ls_batch * tpp + t > P.max_bt) break;
         ++tried;
         const double ft = trial_value(P, C, quad[t], sep ? sep + t * NSEP : nullptr, cc, hv, nullptr);
         if (ft <= C->f + P.c1 * a * C->gp) {                    // Armijo condition
@@ -501,7 +502,7 @@ __device__ __forceinline__ void armijo_decide(const Prob& P, Ctrl* C, const doub
     }
     C->n_fg += tried;
     C->n_bt += tried;
-    if ((C->ls_batch + 1) * KT > P.max_bt) {                    // trials exhausted
+    if ((C->ls_batch + 1) * tpp > P.max_bt) {                   // trials exhausted
         if (C->fallback) { C->done = 1; C->status = S_LS_FAIL; }
         else C->stall = ST_FALLBACK;
     } else {

@@ -271,6 +271,8 @@ static lbfgsb_err create_common(int64_t n, int32_t m_hist, const double* lower, 
     lbfgsb_opts_default(&o);
     if (opts) o = *opts;
     if (!opts_valid(o)) return fail(LBFGSB_ERR_ARG, "invalid option value");
+    if (o.trials_per_pass < 0 || o.trials_per_pass > KT || o.refresh_every < 0)
+        return fail(LBFGSB_ERR_ARG, "trials_per_pass outside [0, %d] or refresh_every < 0", KT);
     if (o.check_every < 1) o.check_every = 1;
     if (o.check_every > 64) o.check_every = 64;
     int ndev = 0;
@@ -450,6 +452,7 @@ static lbfgsb_err make_prob(lbfgsb_t* h, const lbfgsb_objective* ob, Prob& P)
     P.l = h->l.d(); P.u = h->u.d();
     P.eps = h->o.eps; P.c1 = h->o.c1; P.shrink = h->o.shrink;
     P.max_bt = h->o.max_backtracks; P.screen_full = h->o.screen_full_norm; P.mh = h->mh;
+    P.tpp = h->o.trials_per_pass >= 1 && h->o.trials_per_pass <= KT ? h->o.trials_per_pass : KT;
     P.no_projection = h->o.no_projection ? 1 : 0;
     P.max_iters = h->o.max_iters;
     P.x = h->x.d(); P.g = h->g.d(); P.d = h->d.d(); P.pp = h->pp.d(); P.pt = h->pt.d();

@@ -268,6 +268,29 @@ def test_periodic_refresh_matches_oracle(lb, orc, R, check):
     assert abs(r.f - ro.f) <= 1e-8 * abs(ro.f) and r.pg_inf <= 1e-6
 
 
+def test_trials_per_pass_does_not_change_the_trajectory(lb):
+    """opts.trials_per_pass moves only the batch boundaries of the Armijo
+    trials (the trials are sequential, alpha_t = alpha_0 beta^t by repeated
+    multiplication): x is bitwise the same at 1, 3 and 16 trials per pass on a
+    x300-scaled NNLS whose searches need several backtracks (so the host
+    continuation runs at 1 and 3)."""
+    import synth
+    p = synth.nnls_gaussian(400, 200, 24)
+    M = lb.colmajor(p.M * 300.0)
+    obj = lb.LSQObjective(M, b=_cuda(p.b * 300.0))
+    out = []
+    for tpp in (1, 3, 16):
+        s = lb.Solver(p.nvars, 5, lower=_cuda(p.lower), opts=lb.Options(trials_per_pass=tpp, tol=0.09))
+        x = torch.zeros(p.nvars, dtype=torch.float64, device="cuda")
+        r = s.solve(obj, x)
+        out.append((x.cpu().numpy(), r))
+    assert out[0][1].n_backtracks > 0 and out[0][1].status == lb.CONVERGED
+    for x, r in out[1:]:
+        assert np.array_equal(x, out[0][0]) and r.f == out[0][1].f and r.iters == out[0][1].iters
+    with pytest.raises(lb.LbfgsbError):
+        lb.Solver(p.nvars, 5, opts=lb.Options(trials_per_pass=17))
+
+
 def test_determinism_graph_vs_eager(lb):
     """Deterministic reductions: graph replay, eager launches and different
     host-check chunks give bit-identical results."""
