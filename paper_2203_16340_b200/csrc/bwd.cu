@@ -500,9 +500,6 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
 #ifndef BWDW_WCOL
 #define BWDW_WCOL 4            // columns per warp group of k_bwd_w (4 or 8)
 #endif
-#ifndef BWDW_PF
-#define BWDW_PF 0              // 1: bulk L2 prefetch of each warp's next column group
-#endif
 constexpr int WCOL = BWDW_WCOL;
 constexpr int WRS = BWDW_WRS;                   // row steps of 64 rows per trip
 constexpr int WROWS = WCOL * 2;                 // tile rows per warp (split: 2 vars per column)
@@ -632,27 +629,9 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
     const int64_t ngroups = (ncl + WCOL - 1) / WCOL;
     const int rows_per_warp = WCOL * nvg;
     const int trow0 = w * WROWS;
-#if BWDW_PF
-    // L2 prefetch of this warp's first group; each group then prefetches the warp's next one
-    // (cp.async.bulk.prefetch: one instruction per contiguous column block, no registers)
-    if (lane == 0 && w < ngroups) {
-        const int64_t jg = j0 + (int64_t)w * WCOL;
-        const int nc = (int)(j1 - jg < WCOL ? j1 - jg : WCOL);
-        const unsigned bytes = (unsigned)(((int64_t)nc * ld * 8 + 15) & ~(int64_t)15);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.M + jg * ld), "r"(bytes) : "memory");
-    }
-#endif
     for (int64_t grp = w; grp < ngroups; grp += nw) {
         const int64_t jg = j0 + grp * WCOL;
         const int nc = (int)(j1 - jg < WCOL ? j1 - jg : WCOL);
-#if BWDW_PF
-        if (lane == 0 && grp + nw < ngroups) {
-            const int64_t jn = j0 + (grp + nw) * WCOL;
-            const int ncn = (int)(j1 - jn < WCOL ? j1 - jn : WCOL);
-            const unsigned bytes = (unsigned)(((int64_t)ncn * ld * 8 + 15) & ~(int64_t)15);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.M + jn * ld), "r"(bytes) : "memory");
-        }
-#endif
         double acc[WCOL];
 #pragma unroll
         for (int c = 0; c < WCOL; ++c) acc[c] = 0.0;

@@ -218,9 +218,6 @@ __device__ void reduce_sep(const Prob& P, int ntr, double* buf, int bufn, double
 #ifndef FWD_SHORT_B
 #define FWD_SHORT_B 8          // load batch (active columns) of the short-column (MINB = 1) k_fwd
 #endif
-#ifndef FWD_PF
-#define FWD_PF 0               // 1: bulk L2 prefetch of the short-column k_fwd's next load batches
-#endif
 template <bool VEC, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double* pvec, double* qout)
 {
@@ -280,21 +277,7 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         const double* Mc = P.M + c0 * ld + row;
         int a = 0;
         constexpr int FB = MINB == 1 ? FWD_SHORT_B : 8;          // active columns per load batch
-#if FWD_PF
-        // short columns: bulk L2 prefetch of the row block's segment of the next batch's columns
-        // (one instruction per column, no registers), issued one batch ahead
-        const int64_t rb0 = (int64_t)blockIdx.x * FWD_ROWS;
-        const unsigned seg = (unsigned)((((m - rb0 < FWD_ROWS ? m - rb0 : FWD_ROWS) * 8) + 15) & ~15);
-        if (MINB == 1 && VEC && threadIdx.x < 2 * FB && threadIdx.x < nact)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                         ::"l"(P.M + (c0 + lidx[threadIdx.x]) * ld + rb0), "r"(seg) : "memory");
-#endif
         for (; a + FB <= nact; a += FB) {
-#if FWD_PF
-            if (MINB == 1 && VEC && threadIdx.x < FB && a + 2 * FB + (int)threadIdx.x < nact)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                             ::"l"(P.M + (c0 + lidx[a + 2 * FB + threadIdx.x]) * ld + rb0), "r"(seg) : "memory");
-#endif
             double2 v2[FB];
             double s2[FB];
 #pragma unroll
