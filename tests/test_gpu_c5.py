@@ -52,17 +52,9 @@ def test_c5_scaled_down_oracle_parity(lb, orc):
     assert abs(r.f - ro.f) <= 1e-8 * max(abs(ro.f), 1e-8 * 0.5 * float(b @ b))
 
 
-@pytest.mark.slow
-def test_c5_full_size_sampled_kkt(lb):
-    import synth
+def _check_kkt(A, b, x, r, n, m):
     import synth.philox as ph
-    m, n = 100000, 200000
-    free = torch.cuda.mem_get_info()[0]
-    if free < 175e9:
-        pytest.skip(f"C5 needs ~170 GB of device memory, {free / 1e9:.0f} GB free")
-    A, b, xp = synth.c5_device(m, n, seed=5)
-    r, x = _solve(lb, A, b, n)
-    assert r.status == lb.CONVERGED and r.pg_inf <= 1e-6
+    assert r.status == 0 and r.pg_inf <= 1e-6
     xh = x.cpu().numpy()
     assert np.all(xh >= 0)
     # independent residual with torch GEMVs (column chunks)
@@ -78,3 +70,33 @@ def test_c5_full_size_sampled_kkt(lb):
     g = cols.T @ resh
     pg = np.abs(np.maximum(xh[idx] - g, 0.0) - xh[idx])
     assert np.max(pg) <= 2e-6
+    return f
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled_kkt(lb):
+    """FULL size C5 on one B200, twice on the same 160 GB A: one plain handle,
+    and the bench's launch configuration -- the P-invariant group of 8 logical
+    ranks (8 column chunks of 25000, lbfgsb_solve_group).  Both converge to the
+    KKT tolerance on sampled columns and to the same objective (1e-8)."""
+    import synth
+    from paper_2203_16340_b200.sharded import ShardedGroup
+    m, n = 100000, 200000
+    torch.cuda.empty_cache()
+    free = torch.cuda.mem_get_info()[0]
+    if free < 175e9:
+        pytest.skip(f"C5 needs ~170 GB of device memory, {free / 1e9:.0f} GB free")
+    A, b, xp = synth.c5_device(m, n, seed=5)
+    r, x = _solve(lb, A, b, n)
+    f1 = _check_kkt(A, b, x, r, n, m)
+    del x
+    g = ShardedGroup(n, m, nchunks=8,
+                     make_lower=lambda l, c0, c1: torch.zeros(c1 - c0, dtype=torch.float64, device="cuda"))
+    bd = torch.from_numpy(b).cuda()
+    objs = [lb.LSQObjective(A[:, c0:c1], b=bd) for c0, c1 in g.ranges]
+    xs = [torch.zeros(c1 - c0, dtype=torch.float64, device="cuda") for c0, c1 in g.ranges]
+    rg = g.solve(objs, xs)
+    xg = torch.cat(xs)
+    f2 = _check_kkt(A, b, xg, rg, n, m)
+    assert abs(f1 - f2) <= 1e-8 * max(f1, 1e-8 * 0.5 * float(b @ b))
+    g.close()
