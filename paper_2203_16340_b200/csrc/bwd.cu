@@ -737,6 +737,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 constexpr int WT_THREADS = 256;
 constexpr int WT_NS = 3;
 constexpr int WT_STAGE_MAX = 65536;               // bytes per stage
+constexpr int WT_SMEM_MAX = 216 * 1024;           // dynamic smem (+ ~8 KB static <= 227 KB)
 
 __global__ void __launch_bounds__(WT_THREADS, 1) k_bwd_wt(Prob P, int mode, const double* rvec, double* gout,
                                                           int sc, int cmax)
@@ -862,17 +863,19 @@ __global__ void __launch_bounds__(WT_THREADS, 1) k_bwd_wt(Prob P, int mode, cons
 static size_t bwd_wt_smem(const Prob& P, int G, int* sc)
 {
     if (P.ld != P.m || (P.m & 1) || P.m >= 2048 || P.m < 64 || P.ncols < 16LL * G) return 0;
-    int s = (int)(WT_STAGE_MAX / (8 * P.m));
-    if (s < 1) return 0;
-    if (s > 64) s = 64;
     const int64_t cmax = (P.ncols + G - 1) / G + 1;
-    size_t ring = sizeof(double) * (size_t)WT_NS * s * P.m;
+    const size_t rest = sizeof(double) * (size_t)(P.m + 1 + cmax);
+    if (rest >= (size_t)WT_SMEM_MAX) return 0;
+    int s = (int)(WT_STAGE_MAX / (8 * P.m));                    // columns per stage (<= 64 KB)
+    const int sfit = (int)((WT_SMEM_MAX - rest) / (sizeof(double) * (size_t)WT_NS * P.m));
+    if (s > sfit) s = sfit;
+    if (s > 64) s = 64;
+    if (s < 1) return 0;
+    const size_t ring = sizeof(double) * (size_t)WT_NS * s * P.m;
     const size_t tail = sizeof(double) * (size_t)(EPI_TILE * (2 * P.mh + 2) > 4096 ? EPI_TILE * (2 * P.mh + 2) : 4096);
     if (ring < tail) return 0;                                  // the epilogue tile / tail buffer live in the ring
-    const size_t bytes = ring + sizeof(double) * (size_t)(P.m + 1 + cmax);
-    if (bytes > (size_t)(200 * 1024)) return 0;
     *sc = s;
-    return bytes;
+    return ring + rest;
 }
 
 // ---------------------------------------------------------------- k_qpu (QP objective)
@@ -1752,7 +1755,7 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
         if (wsm) {
             static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(k_bwd_wt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(k_bwd_wt, cudaFuncAttributeMaxDynamicSharedMemorySize, WT_SMEM_MAX);
                 attr = true;
             }
             const int64_t cmax = (P.ncols + sms - 1) / sms + 1;
