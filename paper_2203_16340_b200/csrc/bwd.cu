@@ -724,160 +724,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-// ---------------------------------------------------------------- k_bwd_wt (short columns, TMA stream)
-// m < 2048 with contiguous columns (ld == m, e.g. C4's 1000 x 100000): a CTA's
-// column range is ONE contiguous block of memory, so it is streamed in stages
-// of SC whole columns (<= 64 KB) by single cp.async.bulk copies into a 3-stage
-// shared-memory ring (mbarrier complete_tx; thread 0 refills a slot after the
-// CTA barrier that ends its consumption).  Warp w computes the dots of the
-// stage's columns w, w + 8, ... from shared memory (lane l: rows 2l, 2l+1 +
-// 64k, then a shuffle tree), and the CTA's dots wait in shared memory for
-// the epilogue, Gram and Alg. 3 tail of k_bwd_s.  No registers hold the
-// stream, so ~192 KB per SM is in flight (k_bwd_w: 128 KB in 16-byte loads).
-constexpr int WT_THREADS = 256;
-constexpr int WT_NS = 3;
-constexpr int WT_STAGE_MAX = 65536;               // bytes per stage
-constexpr int WT_SMEM_MAX = 216 * 1024;           // dynamic smem (+ ~8 KB static <= 227 KB)
-
-__global__ void __launch_bounds__(WT_THREADS, 1) k_bwd_wt(Prob P, int mode, const double* rvec, double* gout,
-                                                          int sc, int cmax)
-{
-    Ctrl* C = P.ctrl;
-    if (mode == BWD_ITER && halted(C)) return;
-    extern __shared__ __align__(128) double smt[];
-    const int64_t m = P.m, ncols = P.ncols;
-    double* stg = smt;                                          // [WT_NS][sc * m]
-    double* rs = smt + (int64_t)WT_NS * sc * m;                 // r' [m]
-    double* dots = rs + m + (m & 1);                            // [cmax]
-    __shared__ __align__(8) uint64_t full[WT_NS];
-    __shared__ double red[WT_THREADS / 32 * BWD_NB];
-    __shared__ double stash[WT_THREADS];
-    __shared__ double Gs[MAXE + MAXH + 2];
-    const int G = gridDim.x, cta = blockIdx.x;
-    const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
-    const int64_t i0 = (int64_t)cta * m / G, i1 = (int64_t)(cta + 1) * m / G;
-    const bool iter = mode == BWD_ITER;
-    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
-    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
-    double* rnext = P.rbuf[rsel ^ 1];
-    const double alpha = iter ? C->alpha : 0.0;
-    const int ccount = (int)(j1 - j0);
-    const int nst = (ccount + sc - 1) / sc;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = WT_THREADS / 32;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < WT_NS; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < WT_NS && s < nst; ++s) {                // prime the ring
-            const int64_t c0 = j0 + (int64_t)s * sc;
-            const int nc = (int)(j1 - c0 < sc ? j1 - c0 : sc);
-            const unsigned bytes = (unsigned)(nc * m * 8);
-            mbar_arrive_tx(&full[s], bytes);
-            bulk_g2s(stg + (int64_t)s * sc * m, P.M + c0 * m, bytes, &full[s]);
-        }
-    }
-    for (int64_t i = threadIdx.x; i < m; i += WT_THREADS) {      // r' = fma(alpha, q, r) (R13)
-        double r = rcur[i];
-        if (iter) {
-            r = fma(alpha, P.q[i], r);
-            if (i >= i0 && i < i1) rnext[i] = r;
-        }
-        rs[i] = r;
-    }
-    __syncthreads();
-    for (int s = 0; s < nst; ++s) {
-        const int slot = s % WT_NS;
-        const int64_t c0 = j0 + (int64_t)s * sc;
-        const int nc = (int)(j1 - c0 < sc ? j1 - c0 : sc);
-        mbar_wait(&full[slot], (unsigned)((s / WT_NS) & 1));
-        const double* A = stg + (int64_t)slot * sc * m;
-        for (int c = w; c < nc; c += nw) {
-            const double* col = A + (int64_t)c * m;
-            double acc = 0.0;
-            int64_t i = 2 * lane;
-            for (; i + 1 < m; i += 64) {
-                const double2 a = *reinterpret_cast<const double2*>(col + i);
-                const double2 r = *reinterpret_cast<const double2*>(rs + i);
-                acc = fma(a.x, r.x, acc);
-                acc = fma(a.y, r.y, acc);
-            }
-            if (i < m) acc = fma(col[i], rs[i], acc);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-            if (lane == 0) dots[c0 - j0 + c] = acc;
-        }
-        __syncthreads();                                        // the slot is consumed
-        if (threadIdx.x == 0 && s + WT_NS < nst) {
-            const int64_t cn = j0 + (int64_t)(s + WT_NS) * sc;
-            const int ncn = (int)(j1 - cn < sc ? j1 - cn : sc);
-            const unsigned bytes = (unsigned)(ncn * m * 8);
-            mbar_arrive_tx(&full[slot], bytes);
-            bulk_g2s(stg + (int64_t)slot * sc * m, P.M + cn * m, bytes, &full[slot]);
-        }
-    }
-    __syncthreads();
-    const int nvg = P.split ? 2 : 1;
-    const int nvar = ccount * nvg;
-    if (mode == BWD_PLAIN) {
-        for (int t = threadIdx.x; t < nvar; t += WT_THREADS) {
-            const int jj = t % ccount, vv = t / ccount;
-            const int64_t j = j0 + jj;
-            const double dot = dots[jj];
-            double dval = vv ? -dot : dot;
-            if (P.colscale) dval = P.colscale[j] * dot;
-            gout[j + vv * ncols] = dval;
-        }
-        return;
-    }
-    EpiCtx E;
-    epi_init(P, C, mode, E);
-    GramEnt ent;
-    const int ne = E.nb * (E.nb + 1) / 2;
-    ent.init(E.nb, ne, ne + (P.screen_full ? E.nh : 0), E.nh);
-    double gacc[3] = {0.0, 0.0, 0.0};
-    double gmax = 0.0, cnt = 0.0;
-    double* tile = stg;                                         // the ring is no longer needed
-    double* mk = stg + (int64_t)EPI_TILE * E.nb;
-    for (int vb = 0; vb < nvar; vb += EPI_TILE) {
-        const int rows = nvar - vb < EPI_TILE ? nvar - vb : EPI_TILE;
-        const int t = threadIdx.x;
-        if (t < rows) {
-            const int idx = vb + t;
-            const int jj = idx % ccount, vv = idx / ccount;
-            const int64_t j = j0 + jj;
-            const double dot = dots[jj];
-            double dval = vv ? -dot : dot;
-            if (P.colscale) dval = P.colscale[j] * dot;
-            epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)t * E.nb, mk + t, gmax, cnt);
-        }
-        if (E.gram) {
-            __syncthreads();
-            ent.accumulate(tile, mk, rows, E.nb, gacc);
-        }
-        __syncthreads();
-    }
-    if (!E.gram) return;
-    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, stg, 4096, stash, Gs);
-}
-
-// smem k_bwd_wt needs for this problem (0 = not applicable); *sc = columns per stage
-static size_t bwd_wt_smem(const Prob& P, int G, int* sc)
-{
-    if (P.ld != P.m || (P.m & 1) || P.m >= 2048 || P.m < 64 || P.ncols < 16LL * G) return 0;
-    const int64_t cmax = (P.ncols + G - 1) / G + 1;
-    const size_t rest = sizeof(double) * (size_t)(P.m + 1 + cmax);
-    if (rest >= (size_t)WT_SMEM_MAX) return 0;
-    int s = (int)(WT_STAGE_MAX / (8 * P.m));                    // columns per stage (<= 64 KB)
-    const int sfit = (int)((WT_SMEM_MAX - rest) / (sizeof(double) * (size_t)WT_NS * P.m));
-    if (s > sfit) s = sfit;
-    if (s > 64) s = 64;
-    if (s < 1) return 0;
-    const size_t ring = sizeof(double) * (size_t)WT_NS * s * P.m;
-    const size_t tail = sizeof(double) * (size_t)(EPI_TILE * (2 * P.mh + 2) > 4096 ? EPI_TILE * (2 * P.mh + 2) : 4096);
-    if (ring < tail) return 0;                                  // the epilogue tile / tail buffer live in the ring
-    *sc = s;
-    return ring + rest;
-}
-
 // ---------------------------------------------------------------- k_qpu (QP objective)
 // QP objective (the kernel dual SVM): f = 1/2 x^T Q~ x + ..., the
 // gradient is carried as w = Q~ x (like the LSQ residual, R13): w' =
@@ -1746,23 +1592,6 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
     const int sms = sm_count();
     const int Gs_ = (int)(P.ncols < sms ? P.ncols : sms);
     const size_t smem = aligned ? bwd_s_smem(P, Gs_) : 0;
-#ifndef BWDWT_ENABLE
-#define BWDWT_ENABLE 0         // 1: k_bwd_wt (TMA-staged short-column stream) when it applies
-#endif
-    if (BWDWT_ENABLE && aligned && mode != BWD_PLAIN) {
-        int sc = 0;
-        const size_t wsm = bwd_wt_smem(P, sms, &sc);
-        if (wsm) {
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_bwd_wt, cudaFuncAttributeMaxDynamicSharedMemorySize, WT_SMEM_MAX);
-                attr = true;
-            }
-            const int64_t cmax = (P.ncols + sms - 1) / sms + 1;
-            k_bwd_wt<<<sms, WT_THREADS, wsm, st>>>(P, mode, rvec, gout, sc, (int)cmax);
-            return;
-        }
-    }
     if (aligned && P.m < BWD_W_MAXM) {
         int mpad = (int)(P.m + (P.m & 1));
         if (mpad < 4096 / 2) mpad = 4096 / 2;     // tail reduce buffer reuses r' space
