@@ -20,6 +20,9 @@
 #include "common.cuh"
 
 namespace lb {
+#ifdef LB_TRACE
+void trace_set_bwd(void* b, void* c) { trace_set_tu(b, c); }
+#endif
 
 constexpr int NTB = 512;                // threads of k_bwd_s (one CTA per SM)
 constexpr int EPI_TILE = 256;           // epilogue tile rows
@@ -217,6 +220,9 @@ __device__ __forceinline__ void reduce8(const double* acc, double* sh /* >= 8 * 
 struct EpiCtx {
     bool iter, gram;
     double alpha;
+    double tol;             // ctrl->tol, ctrl->k, ctrl->rsel at kernel entry (used by the tail)
+    long long k;
+    int rsel;
     int nh, head, slot, mh, nb, ncons, branch;
     const double* bptr[2 * MAXH];
 };
@@ -282,6 +288,9 @@ __device__ __forceinline__ void epi_init(const Prob& P, const Ctrl* C, int mode,
     E.iter = mode == BWD_ITER;
     E.gram = mode == BWD_ITER || mode == BWD_SETUP;
     E.alpha = E.iter ? C->alpha : 0.0;
+    E.tol = C->tol;
+    E.k = C->k;
+    E.rsel = C->rsel;
     E.nh = E.gram ? C->nh : 0;
     E.head = C->head;
     E.slot = C->slot;
@@ -319,27 +328,36 @@ __device__ void gram_tail_after(const Prob& P, Ctrl* C, const EpiCtx& E, double 
     const int nh = E.nh, nb = E.nb, ne = nb * (nb + 1) / 2;
     const int ntot = ne + (P.screen_full ? nh : 0);
     double* out = P.gram_part + (int64_t)cta * GRAM_STRIDE;
+    TR_DECL
     const double bm = block_reduce<1>(gmax, red);
     const double bc = block_reduce<0>(cnt, red);
     if (threadIdx.x == 0) { out[ntot] = bm; out[ntot + 1] = bc; }
     const int nent = ntot + 2;
     auto sel = [ntot](int e) { return e == ntot ? 1 : 0; };
-    const int grp = cta / GRP, ngrp = (G + GRP - 1) / GRP;
-    const int members = G - grp * GRP < GRP ? G - grp * GRP : GRP;
-    if (!last_cta(P.tickets + T_BWD_G1 + grp, members)) return;
-    reduce_parts(P.gram_part + (int64_t)grp * GRP * GRAM_STRIDE, members, GRAM_STRIDE, nent, sel, buf,
-                 bufn, stash, Gs);
-    for (int e = threadIdx.x; e < nent; e += blockDim.x) P.gram_grp[(int64_t)grp * GRAM_STRIDE + e] = Gs[e];
-    if (!last_cta(P.tickets + T_BWD_G2, ngrp)) return;
-    reduce_parts(P.gram_grp, ngrp, GRAM_STRIDE, nent, sel, buf, bufn, stash, Gs);
+    {
+        const int grp = cta / GRP, ngrp = (G + GRP - 1) / GRP;
+        const int members = G - grp * GRP < GRP ? G - grp * GRP : GRP;
+        if (!last_cta(P.tickets + T_BWD_G1 + grp, members)) return;
+        TR_MARK(1);
+        reduce_parts(P.gram_part + (int64_t)grp * GRP * GRAM_STRIDE, members, GRAM_STRIDE, nent, sel, buf,
+                     bufn, stash, Gs);
+        for (int e = threadIdx.x; e < nent; e += blockDim.x) P.gram_grp[(int64_t)grp * GRAM_STRIDE + e] = Gs[e];
+        TR_MARK(2);
+        if (!last_cta(P.tickets + T_BWD_G2, ngrp)) return;
+        TR_MARK(3);
+        reduce_parts(P.gram_grp, ngrp, GRAM_STRIDE, nent, sel, buf, bufn, stash, Gs);
+        TR_MARK(4);
+    }
     if (P.sharded) {                                         // sharded: local Gram pack
         for (int e = threadIdx.x; e < nent; e += blockDim.x) P.pk_loc[off_gram(P) + e] = Gs[e];
         if (P.p2p) p2p_push(P, XS_GRAM, off_gram(P), GRAM_STRIDE);
         return;
     }
-    if (threadIdx.x != 0) return;
-    if (E.iter) C->rsel = C->rsel ^ 1;
-    recur_decide(P, C, Gs, nh, 0);
+    if (threadIdx.x >= 32) return;
+    if (E.iter && threadIdx.x == 0) C->rsel = E.rsel ^ 1;
+    recur_decide_warp(P, C, Gs, nh, 0, E.tol, E.k);
+    TR_MARK(5);
+    TR_FLUSH(6, 11, G);
 }
 
 // Sharded: reduce the all-gathered Gram packs in rank order, then Alg. 3.
@@ -363,9 +381,11 @@ __global__ void __launch_bounds__(NT) k_gram_decide(Prob P, int mode)
         Gs[e] = s;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    if (mode == BWD_ITER) C->rsel = C->rsel ^ 1;
-    recur_decide(P, C, Gs, nh, 0);
+    if (threadIdx.x >= 32) return;
+    const double tol = C->tol;
+    const long long k = C->k;
+    if (mode == BWD_ITER && threadIdx.x == 0) C->rsel = C->rsel ^ 1;
+    recur_decide_warp(P, C, Gs, nh, 0, tol, k);
 }
 
 // ---------------------------------------------------------------- k_bwd_s
@@ -377,6 +397,7 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
     Ctrl* C = P.ctrl;
     if (mode == BWD_ITER && halted(C)) return;
     extern __shared__ __align__(16) double smd[];
+    TR_DECL
     double* rs = smd;
     double* dots = smd + mpad;
     __shared__ double red[NTB / 32 * BWD_NB];
@@ -410,6 +431,7 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
         }
     }
     __syncthreads();
+    TR_MARK(1);
     if (iter)
         for (int64_t i = i0 + threadIdx.x; i < i1; i += NTB) rnext[i] = rs[i];
     for (int64_t jg = j0; jg < j1; jg += BWD_NB) {
@@ -431,6 +453,7 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
         reduce8(acc, red, gd, nc);
         if ((int)threadIdx.x < nc) dots[jg - j0 + threadIdx.x] = gd[threadIdx.x];
     }
+    TR_MARK(2);
     __syncthreads();
     const int ccount = (int)(j1 - j0);
     const int nvg = P.split ? 2 : 1;
@@ -473,8 +496,11 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
         }
         __syncthreads();
     }
+    TR_MARK(3);
     if (!E.gram) return;
     gram_tail(P, C, E, ent, gacc, gmax, cnt, red, rs, (int)(mpad < 4096 ? mpad : 4096), stash, Gs);
+    TR_MARK(4);
+    TR_FLUSH(5, 1, (int)(j1 - j0));
 }
 
 // ---------------------------------------------------------------- k_bwd_w (short columns)
@@ -506,21 +532,21 @@ constexpr int WROWS = WCOL * 2;                 // tile rows per warp (split: 2 
 constexpr int WTILE = (NT / 32) * WROWS;        // tile rows per CTA
 constexpr int WG_STRIDE = MAXE + MAXH + 1;      // per-warp Gram partial slots (max; launch passes the m_hist size)
 
-template <int NC>
+template <int NC, int RS = WRS>
 __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int64_t ld, int64_t m,
                                               const double* rs, double* acc)
 {
     const int lane = threadIdx.x & 31;
     int64_t i = 2 * lane;
-    for (; i + 64 * (WRS - 1) + 1 < m; i += 64 * WRS) {
-        double2 av[WRS][NC];
+    for (; i + 64 * (RS - 1) + 1 < m; i += 64 * RS) {
+        double2 av[RS][NC];
 #pragma unroll
-        for (int u = 0; u < WRS; ++u)
+        for (int u = 0; u < RS; ++u)
 #pragma unroll
             for (int c = 0; c < NC; ++c)
                 av[u][c] = __ldcs(reinterpret_cast<const double2*>(M0 + c * ld + i + 64 * u));
 #pragma unroll
-        for (int u = 0; u < WRS; ++u) {
+        for (int u = 0; u < RS; ++u) {
             const double2 r = *reinterpret_cast<const double2*>(rs + i + 64 * u);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
@@ -533,10 +559,10 @@ __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int
     // the remaining (< WRS) row steps as ONE batch of loads: rows >= m contribute exact zeros,
     // so every column sees the same additions in the same order as the one-step loop below
     if (i < m) {
-        double2 av[WRS][NC];
-        double2 rv[WRS];
+        double2 av[RS][NC];
+        double2 rv[RS];
 #pragma unroll
-        for (int u = 0; u < WRS; ++u) {
+        for (int u = 0; u < RS; ++u) {
             const int64_t k = i + 64 * u;
             const bool full = k + 1 < m, half = k < m;
             rv[u] = full ? *reinterpret_cast<const double2*>(rs + k) : make_double2(half ? rs[k] : 0.0, 0.0);
@@ -546,7 +572,7 @@ __device__ __forceinline__ void warp_col_dots(const double* __restrict__ M0, int
                                 : make_double2(half ? __ldcs(M0 + c * ld + k) : 0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < WRS; ++u)
+        for (int u = 0; u < RS; ++u)
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 acc[c] = fma(av[u][c].x, rv[u].x, acc[c]);
@@ -576,6 +602,7 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
     Ctrl* C = P.ctrl;
     if (mode == BWD_ITER && halted(C)) return;
     extern __shared__ __align__(16) double smw[];
+    TR_DECL
     double* rs = smw;                               // r' [mpad]
     double* tile = smw + mpad;                      // [WTILE][MAXB]
     double* mk = tile + WTILE * MAXB;               // [WTILE]
@@ -623,6 +650,7 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
         for (int e = lane; e < ntot; e += 32) wgw[e] = 0.0;
     }
     __syncthreads();
+    TR_MARK(1);
     double gmax = 0.0, cnt = 0.0;
     const int nvg = P.split ? 2 : 1;
     const int64_t ncl = j1 - j0;
@@ -689,6 +717,7 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
             __syncwarp();                                       // tile rows are rewritten next group
         }
     }
+    TR_MARK(2);
     if (!gram) return;
     __syncthreads();
     double* out = P.gram_part + (int64_t)blockIdx.x * GRAM_STRIDE;
@@ -698,6 +727,149 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
         out[e] = s;
     }
     gram_tail_after(P, C, E, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
+    TR_MARK(3);
+    TR_FLUSH(4, 2, (int)(j1 - j0));
+}
+
+// ---------------------------------------------------------------- k_bwd_wd (short columns, deferred epilogue)
+// k_bwd_w's per-warp column stream (WCOL columns per warp group, shuffle
+// reductions, r' in shared memory) with the epilogue taken OUT of the stream:
+// the warps only stream and park the column dots in shared memory, so no warp
+// stalls on the epilogue's dependent loads while the others stream; then the
+// whole CTA runs k_bwd_s's epilogue (one variable per thread, NT-row Gram
+// tiles) and the same 2-level tail.  A/B against k_bwd_w: BWDW_DEFER.
+#ifndef BWDW_DEFER
+#define BWDW_DEFER 1
+#endif
+#ifndef BWDWD_MINB
+#define BWDWD_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wd(Prob P, int mode, const double* rvec, double* gout,
+                                                         int mpad, int cpad)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    extern __shared__ __align__(16) double smw[];
+    TR_DECL
+    double* rs = smw;                               // r' [mpad]; later the tail's reduce buffer
+    double* dots = smw + mpad;                      // [cpad] column dots of this CTA
+    double* tile = dots + cpad;                     // [NT][nb] epilogue Gram tile, then mk[NT]
+    __shared__ double red[NT / 32 * BWD_NB];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    __shared__ int s_next;                          // next column unit
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
+    const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
+    const int64_t i0 = (int64_t)cta * m / G, i1 = (int64_t)(cta + 1) * m / G;
+    const bool iter = mode == BWD_ITER;
+    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
+    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
+    double* rnext = P.rbuf[rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    if (threadIdx.x == 0) s_next = 0;
+    for (int64_t i = threadIdx.x; i < m; i += NT) {
+        double r = rcur[i];
+        if (iter) {
+            r = fma(alpha, P.q[i], r);                          // carried residual (R13)
+            if (i >= i0 && i < i1) rnext[i] = r;
+        }
+        rs[i] = r;
+    }
+    __syncthreads();
+    TR_MARK(1);
+    const int lane = threadIdx.x & 31, nw = NT / 32;
+    const int64_t ncl = j1 - j0;
+    // Units of WCOL columns go to the warps dynamically (a shared-memory counter), so
+    // the warps of a CTA finish their streams within about one unit of each other
+    // (C4 shape: 3126 -> 3297 solver iterations / s against round-robin units).  A
+    // unit's dots do not depend on the warp that streams it: deterministic.  A tail of
+    // single-column units (16 row steps per trip) was measured slower (3190-3231).
+    const int64_t nbulk = ncl;
+    const int nunits = (int)((nbulk + WCOL - 1) / WCOL);
+    for (;;) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&s_next, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= nunits) break;
+        const int64_t jg = j0 + (int64_t)u * WCOL;
+        const int nc = (int)(nbulk - (int64_t)u * WCOL < WCOL ? nbulk - (int64_t)u * WCOL : WCOL);
+        double acc[WCOL];
+#pragma unroll
+        for (int c = 0; c < WCOL; ++c) acc[c] = 0.0;
+        const double* M0 = P.M + jg * ld;
+        switch (nc) {
+#if BWDW_WCOL > 4
+            case 8: warp_col_dots<8>(M0, ld, m, rs, acc); break;
+            case 7: warp_col_dots<7>(M0, ld, m, rs, acc); break;
+            case 6: warp_col_dots<6>(M0, ld, m, rs, acc); break;
+            case 5: warp_col_dots<5>(M0, ld, m, rs, acc); break;
+#endif
+            case 4: warp_col_dots<4>(M0, ld, m, rs, acc); break;
+            case 3: warp_col_dots<3>(M0, ld, m, rs, acc); break;
+            case 2: warp_col_dots<2>(M0, ld, m, rs, acc); break;
+            default: warp_col_dots<1>(M0, ld, m, rs, acc); break;
+        }
+#pragma unroll
+        for (int c = 0; c < WCOL; ++c)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        if (lane < nc) {
+            double dot = acc[0];
+#pragma unroll
+            for (int c = 1; c < WCOL; ++c)
+                if (lane == c) dot = acc[c];
+            dots[jg - j0 + lane] = dot;
+        }
+    }
+    TR_MARK(2);
+    __syncthreads();
+    TR_MARK(3);
+    const int ccount = (int)ncl;
+    const int nvg = P.split ? 2 : 1;
+    const int nvar = ccount * nvg;
+    if (mode == BWD_PLAIN) {
+        for (int t = threadIdx.x; t < nvar; t += NT) {
+            const int jj = t % ccount, vv = t / ccount;
+            const int64_t j = j0 + jj;
+            const double dot = dots[jj];
+            double dval = vv ? -dot : dot;
+            if (P.colscale) dval = P.colscale[j] * dot;
+            gout[j + vv * ncols] = dval;
+        }
+        return;
+    }
+    EpiCtx E;
+    epi_init(P, C, mode, E);
+    GramEnt ent;
+    const int ne = E.nb * (E.nb + 1) / 2;
+    ent.init(E.nb, ne, ne + (P.screen_full ? E.nh : 0), E.nh);
+    double gacc[3] = {0.0, 0.0, 0.0};
+    double gmax = 0.0, cnt = 0.0;
+    double* mk = tile + (int64_t)NT * E.nb;
+    for (int vb = 0; vb < nvar; vb += NT) {
+        const int rows = nvar - vb < NT ? nvar - vb : NT;
+        const int t = threadIdx.x;
+        if (t < rows) {
+            const int idx = vb + t;
+            const int jj = idx % ccount, vv = idx / ccount;
+            const int64_t j = j0 + jj;
+            const double dot = dots[jj];
+            double dval = vv ? -dot : dot;
+            if (P.colscale) dval = P.colscale[j] * dot;
+            epilogue_var(P, C, E, j + vv * ncols, dval, tile + (int64_t)t * E.nb, mk + t, gmax, cnt);
+        }
+        if (E.gram) {
+            __syncthreads();
+            ent.accumulate(tile, mk, rows, E.nb, gacc);
+        }
+        __syncthreads();
+    }
+    TR_MARK(4);
+    if (!E.gram) return;
+    gram_tail(P, C, E, ent, gacc, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
+    TR_MARK(5);
+    TR_FLUSH(6, 3, (int)ncl);
 }
 
 // ---------------------------------------------------------------- TMA / mbarrier helpers (k_qepi_t, k_qepi_d)
@@ -1605,6 +1777,25 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_w, NT, sm);
             occ_w = o > 0 ? o : 1;
             occ_sm = sm;
+        }
+        // grid = sms * BWDWD_MINB CTAs (fewer only when ncols is smaller), so cpad covers
+        // every CTA's column range; k_bwd_w when that many CTAs do not fit an SM
+        const int Gd = (int)(P.ncols < (int64_t)sms * BWDWD_MINB ? P.ncols : (int64_t)sms * BWDWD_MINB);
+        const int64_t cmax = (P.ncols + Gd - 1) / Gd;
+        const int cpad = (int)(cmax + (cmax & 1));
+        const size_t smd = sizeof(double) * ((size_t)mpad + cpad + (size_t)NT * (nbm + 1));
+        static size_t occ_dsm = 0;
+        static int occ_d = 0;
+        if (BWDW_DEFER && smd <= (size_t)BWD_SMEM_MAX && smd != occ_dsm) {
+            cudaFuncSetAttribute(k_bwd_wd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smd);
+            int o = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_wd, NT, smd);
+            occ_d = o;
+            occ_dsm = smd;
+        }
+        if (BWDW_DEFER && smd == occ_dsm && occ_d >= BWDWD_MINB) {
+            k_bwd_wd<<<Gd, NT, smd, st>>>(P, mode, rvec, gout, mpad, cpad);
+            return;
         }
         const int Gw = (int)(P.ncols < (int64_t)sms * occ_w ? P.ncols : (int64_t)sms * occ_w);
         k_bwd_w<<<Gw, NT, sm, st>>>(P, mode, rvec, gout, mpad, wgs);

@@ -109,6 +109,39 @@ __device__ __forceinline__ unsigned long long globaltimer_ns()
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// ---- LB_TRACE (A/B variant builds only, tools/trace_phases.py): per-CTA
+// phase timestamps (%globaltimer) appended as one record per CTA per launch.
+// The default library compiles none of this.
+#ifdef LB_TRACE
+struct TraceRec { unsigned long long t[6]; int kid, cta, smid, aux; };
+constexpr unsigned TRACE_CAP = 1u << 20;
+static __device__ TraceRec* g_trace_buf;
+static __device__ unsigned* g_trace_cnt;
+__device__ __forceinline__ void trace_flush(const unsigned long long* ts, int nts, int kid, int aux)
+{
+    TraceRec* b = g_trace_buf;
+    if (!b) return;
+    const unsigned k = atomicAdd(g_trace_cnt, 1u);
+    if (k >= TRACE_CAP) return;
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    for (int i = 0; i < 6; ++i) b[k].t[i] = i < nts ? ts[i] : 0ULL;
+    b[k].kid = kid; b[k].cta = (int)(blockIdx.x + blockIdx.y * gridDim.x); b[k].smid = (int)sm; b[k].aux = aux;
+}
+static inline void trace_set_tu(void* buf, void* cnt)
+{
+    cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(void*));
+    cudaMemcpyToSymbol(g_trace_cnt, &cnt, sizeof(void*));
+}
+// thread 0 stamps into a shared array (no per-thread registers)
+#define TR_DECL __shared__ unsigned long long _trs[6]; if (threadIdx.x == 0) _trs[0] = lb::globaltimer_ns();
+#define TR_MARK(i) do { if (threadIdx.x == 0) _trs[i] = lb::globaltimer_ns(); } while (0)
+#define TR_FLUSH(n, kid, aux) do { if (threadIdx.x == 0) lb::trace_flush(_trs, n, kid, aux); } while (0)
+#else
+#define TR_DECL
+#define TR_MARK(i) do {} while (0)
+#define TR_FLUSH(n, kid, aux) do {} while (0)
+#endif
 // Consumer side (one thread): spin until section `sec` of the own mailbox has
 // received `tgt` signals in total.  A peer that never signals trips the
 // timeout flag in the header after 60 s instead of hanging the GPU.
@@ -143,9 +176,28 @@ __device__ __forceinline__ void p2p_push(const Prob& P, int sec, int64_t off, in
 
 // Last-CTA ticket: true in every thread of the last of `total` CTAs to arrive.
 // Partials written before the call by the other CTAs are visible afterwards.
+// The CTA barrier orders every thread's partial writes before thread 0's
+// acq_rel ticket increment (release, cumulative over the barrier), and the
+// same increment's acquire plus the second barrier orders the last CTA's
+// reads of the other CTAs' partials after it: one gpu-scope fence by one
+// thread instead of a sequentially consistent fence by every thread
+// (LASTCTA_AR 0: the __threadfence() form, A/B).
+#ifndef LASTCTA_AR
+#define LASTCTA_AR 1
+#endif
 __device__ __forceinline__ bool last_cta(unsigned* ticket, unsigned total)
 {
     __shared__ int s_last;
+#if LASTCTA_AR
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(ticket) : "memory");
+        s_last = (t == total - 1u) ? 1 : 0;
+        if (s_last) *ticket = 0u;           // everyone else has arrived: reset for the next launch
+    }
+    __syncthreads();
+#else
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -155,6 +207,7 @@ __device__ __forceinline__ bool last_cta(unsigned* ticket, unsigned total)
     }
     __syncthreads();
     if (s_last) __threadfence();
+#endif
     return s_last != 0;
 }
 
@@ -173,9 +226,24 @@ __device__ void reduce_parts(const double* src, int nparts, int stride, int nent
     const int per_pass = bufn / nent > 0 ? bufn / nent : 1;
     for (int p0 = 0; p0 < nparts; p0 += per_pass) {
         const int np = nparts - p0 < per_pass ? nparts - p0 : per_pass;
-        for (int i = threadIdx.x; i < np * nent; i += nth) {
-            const int p = i / nent, e = i - p * nent;
-            buf[i] = __ldcg(src + (size_t)(p0 + p) * stride + e);
+        const int tot = np * nent;
+        // 8 independent loads in flight per thread (the L2 round trips of a
+        // load-store loop would serialise: buf and src may alias for the compiler)
+        for (int i0 = threadIdx.x; i0 < tot; i0 += 8 * nth) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * nth;
+                if (i < tot) {
+                    const int p = i / nent, e = i - p * nent;
+                    v[u] = __ldcg(src + (size_t)(p0 + p) * stride + e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * nth;
+                if (i < tot) buf[i] = v[u];
+            }
         }
         __syncthreads();
         for (int eb = 0; eb < nent; eb += epr) {
@@ -266,9 +334,11 @@ struct GramEnt {
             const int aa = a[k], bb = b[k];
             double s = 0.0;
             if (!full[k]) {
+#pragma unroll 4
                 for (int r = j; r < rows; r += R)
                     if (mk[r] != 0.0) s = fma(tile[r * nb + aa], tile[r * nb + bb], s);
             } else {
+#pragma unroll 4
                 for (int r = j; r < rows; r += R) s = fma(tile[r * nb + aa], tile[r * nb + aa], s);
             }
             acc[k] += s;
@@ -305,7 +375,11 @@ struct GramEnt {
 //   q *= rho_{k-1}/nu_{k-1} if pair k-1 passes (R4)
 //   oldest..newest: beta = <y_i, q>_S / rho_i, q += (a_i - beta) s_i
 // d = -q on S (R5).  Single thread.
-__device__ __forceinline__ void recur_decide(const Prob& P, Ctrl* C, const double* G, int nh, int op_mode)
+// tol and k are ctrl->tol and ctrl->k; the k_bwd tails pass the values they
+// read at kernel entry (the tail's own loads would be dependent L2 round trips
+// after the ticket's acquire invalidated L1).
+__device__ __forceinline__ void recur_decide_tk(const Prob& P, Ctrl* C, const double* G, int nh, int op_mode,
+                                                double tol, long long k)
 {
     const int nb = 2 * nh + 1, ne = nb * (nb + 1) / 2;
     const int nfull = P.screen_full ? nh : 0;
@@ -313,8 +387,8 @@ __device__ __forceinline__ void recur_decide(const Prob& P, Ctrl* C, const doubl
     C->gfree = gm;
     C->nfree = (long long)cnt;
     if (!op_mode) {
-        if (cnt == 0.0 || gm <= C->tol) { C->done = 1; C->status = S_CONVERGED; return; }
-        if (C->k >= P.max_iters) { C->done = 1; C->status = S_MAX_ITERS; return; }
+        if (cnt == 0.0 || gm <= tol) { C->done = 1; C->status = S_CONVERGED; return; }
+        if (k >= P.max_iters) { C->done = 1; C->status = S_MAX_ITERS; return; }
     }
     double w[MAXB], al[MAXH], rho[MAXH], nu[MAXH];
     bool ok[MAXH];
@@ -345,6 +419,80 @@ __device__ __forceinline__ void recur_decide(const Prob& P, Ctrl* C, const doubl
         w[i] = w[i] + (al[i] - beta);                           // q += (a_i - beta) s_i
     }
     for (int b = 0; b < nb; ++b) C->coef[b] = -w[b];
+}
+
+__device__ __forceinline__ void recur_decide(const Prob& P, Ctrl* C, const double* G, int nh, int op_mode)
+{
+    recur_decide_tk(P, C, G, nh, op_mode, C->tol, C->k);
+}
+
+// recur_decide_tk by one full warp (the kernel tails' last CTA): lane b holds
+// the coefficient w_b (lane 0 also w_32 when nb = 33), every <B_a, q>_S is
+// the lanes' products summed by a xor butterfly (commutative adds: the same
+// bits in every lane), lane i keeps alpha_i, rho_i, nu_i.  One pass of the
+// two loops costs ~10 shuffled dot products instead of ~10 x nb dependent
+// local-memory round trips of the single-thread loops (7 us per iteration
+// on B200 at m_hist = 5).  The dot products are summed in butterfly order,
+// so the coefficients agree with recur_decide to rounding, not bitwise.
+__device__ __forceinline__ void recur_decide_warp(const Prob& P, Ctrl* C, const double* G, int nh, int op_mode,
+                                                  double tol, long long k)
+{
+    const int lane = threadIdx.x & 31;
+    const int nb = 2 * nh + 1, ne = nb * (nb + 1) / 2;
+    const int nfull = P.screen_full ? nh : 0;
+    const double gm = G[ne + nfull], cnt = G[ne + nfull + 1];
+    if (lane == 0) {
+        C->gfree = gm;
+        C->nfree = (long long)cnt;
+    }
+    if (!op_mode) {
+        if (cnt == 0.0 || gm <= tol) {
+            if (lane == 0) { C->done = 1; C->status = S_CONVERGED; }
+            return;
+        }
+        if (k >= P.max_iters) {
+            if (lane == 0) { C->done = 1; C->status = S_MAX_ITERS; }
+            return;
+        }
+    }
+    auto Gv = [&](int a, int b) { return a <= b ? G[tri(a, b, nb)] : G[tri(b, a, nb)]; };
+    auto wsum = [](double v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+    const int b0 = lane, b1 = lane + 32;
+    double w0 = b0 == 2 * nh ? 1.0 : 0.0, w1 = b1 == 2 * nh ? 1.0 : 0.0;   // q = grad[S]
+    double my_al = 0.0, my_rho = 1.0, my_nu = 1.0;
+    bool my_ok = false;
+    for (int i = nh - 1; i >= 0; --i) {
+        const double rho = Gv(i, nh + i);
+        const double nu = P.screen_full ? G[ne + i] : Gv(nh + i, nh + i);
+        const bool ok = rho > P.eps * nu;
+        double al = 0.0;
+        if (ok) {
+            double pr = b0 < nb ? w0 * Gv(i, b0) : 0.0;
+            if (b1 < nb) pr = pr + w1 * Gv(i, b1);
+            al = wsum(pr) / rho;                                  // <s_i, q>_S / rho_i
+            if (b0 == nh + i) w0 = w0 - al;                       // q -= a_i y_i
+        }
+        if (lane == i) { my_al = al; my_rho = rho; my_nu = nu; my_ok = ok; }
+    }
+    if (nh > 0 && __shfl_sync(0xffffffffu, (int)my_ok, nh - 1)) {
+        const double gam = __shfl_sync(0xffffffffu, my_rho, nh - 1) / __shfl_sync(0xffffffffu, my_nu, nh - 1);
+        w0 = gam * w0;
+        w1 = gam * w1;
+    }
+    for (int i = 0; i < nh; ++i) {
+        if (!__shfl_sync(0xffffffffu, (int)my_ok, i)) continue;
+        double pr = b0 < nb ? w0 * Gv(nh + i, b0) : 0.0;
+        if (b1 < nb) pr = pr + w1 * Gv(nh + i, b1);
+        const double beta = wsum(pr) / __shfl_sync(0xffffffffu, my_rho, i);   // <y_i, q>_S / rho_i
+        const double ai = __shfl_sync(0xffffffffu, my_al, i);
+        if (b0 == i) w0 = w0 + (ai - beta);                      // q += (a_i - beta) s_i
+    }
+    if (b0 < nb) C->coef[b0] = -w0;
+    if (b1 < nb) C->coef[b1] = -w1;
 }
 
 // Alg. 2 line 3 decision (R9) and the line-search bound alpha_0 (R10).

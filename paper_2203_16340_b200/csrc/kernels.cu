@@ -17,6 +17,9 @@
 #include "common.cuh"
 
 namespace lb {
+#ifdef LB_TRACE
+void trace_set_kernels(void* b, void* c) { trace_set_tu(b, c); }
+#endif
 
 // ------------------------------------------------------------------ clip
 __global__ void k_clip(Prob P)
@@ -47,6 +50,7 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
     __shared__ double stash[NT];
     __shared__ double res[4];
     __shared__ double msh[NT / 32 * 3];
+    TR_DECL
     if (threadIdx.x < 2 * nh + 1) cf[threadIdx.x] = C->coef[threadIdx.x];
     if (threadIdx.x < nh) {
         const int s = ring_slot(head, nh, threadIdx.x, mh);
@@ -82,6 +86,8 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
         else if (pt > 0.0) t = (uj - xj) / pt;
         amin = t < amin ? t : amin;
     }
+    TR_MARK(1);
+    TR_FLUSH(2, 5, 0);
     const double v3[3] = {spg, spp, stg};
     block_sum_multi<3>(v3, msh, res);
     const double a3 = block_reduce<2>(amin, red);
@@ -90,6 +96,7 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
         o[0] = res[0]; o[1] = res[1]; o[2] = res[2]; o[3] = a3;
     }
     if (!last_cta(P.tickets + T_DIR, gridDim.x)) return;
+    TR_MARK(2);
     reduce_parts(P.dir_part, gridDim.x, 4, 4, [](int e) { return e == 3 ? 2 : 0; }, buf, 1024,
                  stash, res);
     if (P.sharded) {                                         // sharded: local pack
@@ -99,6 +106,8 @@ __global__ void __launch_bounds__(NT) k_dir(Prob P, int op_mode)
     }
     if (threadIdx.x != 0) return;
     dir_decide(P, C, res, op_mode);
+    TR_MARK(3);
+    TR_FLUSH(4, 15, 0);
 }
 
 // Sharded: reduce the all-gathered Alg. 2 packs in rank order, then decide.
@@ -209,6 +218,34 @@ __device__ void reduce_sep(const Prob& P, int ntr, double* buf, int bufn, double
     __syncthreads();
 }
 
+// Sum of the split-K partials k = 0..cnt-1 at base + k * stride of rows row,
+// row + 1, in k order, 8 partials (16 loads) in flight per batch: a plain
+// load-add loop serialised one L2 round trip per partial in the row-block tail.
+__device__ __forceinline__ void sum_parts(const double* base, int64_t stride, int cnt, int64_t row, bool r0ok,
+                                          bool r1ok, double& q0, double& q1)
+{
+    int k = 0;
+    for (; k + 8 <= cnt; k += 8) {
+        double a[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double* src = base + (int64_t)(k + u) * stride;
+            a[u] = r0ok ? __ldcg(src + row) : 0.0;
+            b[u] = r1ok ? __ldcg(src + row + 1) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (r0ok) q0 += a[u];
+            if (r1ok) q1 += b[u];
+        }
+    }
+    for (; k < cnt; ++k) {
+        const double* src = base + (int64_t)k * stride;
+        if (r0ok) q0 += __ldcg(src + row);
+        if (r1ok) q1 += __ldcg(src + row + 1);
+    }
+}
+
 // ------------------------------------------------------------------ a1: forward GEMV + line search
 // q partials: qpart[chunk][i] = sum over ACTIVE columns j of the chunk (peff_j
 // != 0), ascending j, of M[i,j] * peff_j with peff = (split ? p_j - p_{ncols+j}
@@ -237,6 +274,7 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
     __shared__ double Ssum[KT];
     __shared__ double sepv[KT * NSEP];
     __shared__ double msh[NT / 32 * KT];
+    TR_DECL
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool r0ok = row < m, r1ok = row + 1 < m;
     double acc0 = 0.0, acc1 = 0.0;
@@ -313,6 +351,8 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         }
         __syncthreads();
     }
+    TR_MARK(1);
+    TR_FLUSH(2, 4, (int)nact_total);
     {
         double* out = P.qpart + (int64_t)blockIdx.y * m;
         if (r0ok) out[row] = acc0;
@@ -332,28 +372,16 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         const int cg = (int)blockIdx.y / FWD_GRPC, c0g = cg * FWD_GRPC;
         const int members = CCn - c0g < FWD_GRPC ? CCn - c0g : FWD_GRPC;
         if (!last_cta(P.tickets + T_FWD_G + (int64_t)blockIdx.x * FWD_MAXCG + cg, members)) return;
-        for (int c = c0g; c < c0g + members; ++c) {
-            const double* src = P.qpart + (int64_t)c * m;
-            if (r0ok) q0 += __ldcg(src + row);
-            if (r1ok) q1 += __ldcg(src + row + 1);
-        }
+        sum_parts(P.qpart + (int64_t)c0g * m, m, members, row, r0ok, r1ok, q0, q1);
         double* dst = P.qpart + (int64_t)c0g * m;              // consumed: reuse as the group's slot
         if (r0ok) dst[row] = q0;
         if (r1ok) dst[row + 1] = q1;
         if (!last_cta(P.tickets + T_FWD_RB + blockIdx.x, ncg)) return;
         q0 = 0.0; q1 = 0.0;
-        for (int g = 0; g < ncg; ++g) {
-            const double* src = P.qpart + (int64_t)g * FWD_GRPC * m;
-            if (r0ok) q0 += __ldcg(src + row);
-            if (r1ok) q1 += __ldcg(src + row + 1);
-        }
+        sum_parts(P.qpart, (int64_t)FWD_GRPC * m, ncg, row, r0ok, r1ok, q0, q1);
     } else {
         if (!last_cta(P.tickets + T_FWD_RB + blockIdx.x, gridDim.y)) return;
-        for (int c = 0; c < CCn; ++c) {
-            const double* src = P.qpart + (int64_t)c * m;
-            if (r0ok) q0 += __ldcg(src + row);
-            if (r1ok) q1 += __ldcg(src + row + 1);
-        }
+        sum_parts(P.qpart, m, CCn, row, r0ok, r1ok, q0, q1);
     }
     if (P.qp && P.colscale) {                                   // Q~ = D M D: row scaling
         if (r0ok) q0 = P.colscale[row] * q0;
@@ -452,6 +480,7 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
     }
     // ---- global tail: the Armijo decision (ITER) or f(x) (SETUP)
     if (!last_cta(P.tickets + T_FWD_ALL, gridDim.x)) return;
+    TR_MARK(2);
     reduce_parts(P.lsp, gridDim.x, KT, ntr, [](int) { return 0; }, lval, FWD_SUB, stash, Ssum);
     reduce_sep(P, ntr, lval, FWD_SUB, stash, sepv);
     if (threadIdx.x != 0) return;
@@ -470,6 +499,8 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         quad_values(P, C, Ssum, quad);
         armijo_decide(P, C, quad, sp);
     }
+    TR_MARK(3);
+    TR_FLUSH(4, 14, 0);
 }
 
 // Host-driven trial batches (stall continuation) and the op_trials entry:

@@ -54,6 +54,18 @@ static lbfgsb_err fail(lbfgsb_err e, const char* fmt, ...)
 
 extern "C" const char* lbfgsb_last_error(void) { return g_err.c_str(); }
 
+#ifdef LB_TRACE
+namespace lb { void trace_set_bwd(void*, void*); void trace_set_kernels(void*, void*); }
+// A/B variant builds only (tools/trace_phases.py): point the per-CTA phase
+// trace of k_bwd_s / k_bwd_w / k_fwd / k_dir at device buffers (NULL: off).
+extern "C" int lbfgsb_trace_set(void* recs, void* count)
+{
+    lb::trace_set_bwd(recs, count);
+    lb::trace_set_kernels(recs, count);
+    return (int)cudaDeviceSynchronize();
+}
+#endif
+
 // ------------------------------------------------------------------ objects
 struct lbfgsb_objective {
     int kind;                       // 0 LSQ (and QP), 1 callback, 2 transport
