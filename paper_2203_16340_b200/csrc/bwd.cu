@@ -227,28 +227,46 @@ struct EpiCtx {
     const double* bptr[2 * MAXH];
 };
 
-// Per-variable epilogue core (Alg. 1 lines 7-9, Eq. (1)): x', g', s, y, mask.
-// Returns 1 when the variable is fixed (not in S^{k+1}).
-__device__ __forceinline__ bool epi_core(const Prob& P, const Ctrl* C, const EpiCtx& E, int64_t v,
-                                         double dval, double& xn_o, double& gn_o, double& sv_o,
-                                         double& yv_o, double& gmax, double& cnt)
+// Per-variable epilogue (Alg. 1 lines 7-9, Eq. (1)): x', g', s, y, mask, and
+// the variable's row of the Gram tile.  Every global load comes first -- x, l,
+// u, p, c, g, E_k and the ring values of the Gram row (straight into the tile
+// row, 8 loads in flight per batch) -- because a load issued after a store
+// through a pointer that may alias it cannot be hoisted: with the ring reads
+// after the x / g / s / y stores (and each ring value stored to the tile before
+// the next was loaded) the epilogue cost 2 nh + 2 dependent L2 round trips per
+// variable (C4 shape: 19 us for k_bwd_wd's 2 tiles).
+__device__ __forceinline__ void epilogue_var(const Prob& P, const Ctrl* C, const EpiCtx& E, int64_t v,
+                                             double dval, double* trow, double* mkv, double& gmax,
+                                             double& cnt)
 {
     const double xo = P.x[v], lv = P.l[v], uv = P.u[v];
-    double xn = xo;
-    if (E.iter) {
-        const double pv = E.branch ? P.pp[v] : P.pt[v];
-        xn = clipd(fma(E.alpha, pv, xo), lv, uv);               // Alg. 1 line 7
+    const double pv = E.iter ? (E.branch ? P.pp[v] : P.pt[v]) : 0.0;
+    const double cv = P.c ? P.c[v] : 0.0;
+    const double go = E.iter ? P.g[v] : 0.0;
+    double ev[MAXC];
+#pragma unroll
+    for (int k = 0; k < MAXC; ++k) ev[k] = k < E.ncons ? P.Ecol[k][v] : 0.0;
+    const int nr = E.gram ? 2 * E.nh : 0;
+    for (int b0 = 0; b0 < nr; b0 += 8) {
+        double t8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t8[u] = b0 + u < nr ? E.bptr[b0 + u][v] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (b0 + u < nr) trow[b0 + u] = t8[u];
     }
+    double xn = xo;
+    if (E.iter) xn = clipd(fma(E.alpha, pv, xo), lv, uv);      // Alg. 1 line 7
     double gn = dval;
-    if (P.c) gn = gn + P.c[v];
+    if (P.c) gn = gn + cv;
     gn = gn + P.delta * xn;
     if (P.ent != 0.0) gn = gn + P.ent * (log(xn) + 1.0);       // d/dx x log x (N2 entropy)
-    for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * P.Ecol[k][v];
+    for (int k = 0; k < E.ncons; ++k) gn = gn + C->ccoef[k] * ev[k];
     double sv = 0.0, yv = 0.0;
     if (E.iter) {
         const int64_t so = (int64_t)E.slot * P.n + v;
         sv = xn - xo;                                           // s^k
-        yv = gn - P.g[v];                                       // y^k
+        yv = gn - go;                                           // y^k
         P.S[so] = sv;
         P.Y[so] = yv;
     }
@@ -261,24 +279,13 @@ __device__ __forceinline__ bool epi_core(const Prob& P, const Ctrl* C, const Epi
         gmax = ag > gmax ? ag : gmax;
         cnt += 1.0;
     }
-    xn_o = xn; gn_o = gn; sv_o = sv; yv_o = yv;
-    return fixed;
-}
-
-// Per-variable epilogue; writes the variable's row of the Gram tile.
-__device__ __forceinline__ void epilogue_var(const Prob& P, const Ctrl* C, const EpiCtx& E, int64_t v,
-                                             double dval, double* trow, double* mkv, double& gmax,
-                                             double& cnt)
-{
-    double xn, gn, sv, yv;
-    const bool fixed = epi_core(P, C, E, v, dval, xn, gn, sv, yv, gmax, cnt);
     if (!E.gram) return;
-    for (int b = 0; b < E.nh; ++b) {
-        const int sl = ring_slot(E.head, E.nh, b, E.mh);
-        const bool cur = E.iter && sl == E.slot;
-        trow[b] = cur ? sv : E.bptr[b][v];
-        trow[E.nh + b] = cur ? yv : E.bptr[E.nh + b][v];
-    }
+    if (E.iter)                                                 // the new pair's slot holds (s, y) of this step
+        for (int b = 0; b < E.nh; ++b)
+            if (ring_slot(E.head, E.nh, b, E.mh) == E.slot) {
+                trow[b] = sv;
+                trow[E.nh + b] = yv;
+            }
     trow[2 * E.nh] = gn;
     *mkv = fixed ? 0.0 : 1.0;
 }
@@ -778,7 +785,7 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wd(Prob P, int mode, con
     }
     __syncthreads();
     TR_MARK(1);
-    const int lane = threadIdx.x & 31, nw = NT / 32;
+    const int lane = threadIdx.x & 31;
     const int64_t ncl = j1 - j0;
     // Units of WCOL columns go to the warps dynamically (a shared-memory counter), so
     // the warps of a CTA finish their streams within about one unit of each other

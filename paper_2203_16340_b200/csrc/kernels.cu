@@ -335,19 +335,34 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
                 acc1 = fma(v2[e].y, s2[e], acc1);
             }
         }
-        for (; a < nact; ++a) {
-            const double* ptr = Mc + (int64_t)lidx[a] * ld;
-            const double s = lval[a];
-            double vx = 0.0, vy = 0.0;
-            if (VEC && r1ok) {
-                const double2 t = __ldcs(reinterpret_cast<const double2*>(ptr));
-                vx = t.x; vy = t.y;
-            } else {
-                vx = r0ok ? __ldcs(ptr) : 0.0;
-                vy = r1ok ? __ldcs(ptr + 1) : 0.0;
+        // the last (< FB) active columns as ONE predicated batch: a one-column-at-a-time
+        // loop put up to FB - 1 dependent HBM round trips at the end of every chunk (the
+        // slowest chunk ends the launch).  Same FMAs in the same order.
+        const int rem = nact - a;
+        if (rem > 0) {
+            double2 v2[FB];
+            double s2[FB];
+#pragma unroll
+            for (int e = 0; e < FB; ++e) {
+                v2[e] = make_double2(0.0, 0.0);
+                s2[e] = 0.0;
+                if (e < rem) {
+                    const double* ptr = Mc + (int64_t)lidx[a + e] * ld;
+                    if (VEC && r1ok) {
+                        v2[e] = __ldcs(reinterpret_cast<const double2*>(ptr));
+                    } else {
+                        v2[e].x = r0ok ? __ldcs(ptr) : 0.0;
+                        v2[e].y = r1ok ? __ldcs(ptr + 1) : 0.0;
+                    }
+                    s2[e] = lval[a + e];
+                }
             }
-            acc0 = fma(vx, s, acc0);
-            acc1 = fma(vy, s, acc1);
+#pragma unroll
+            for (int e = 0; e < FB; ++e)
+                if (e < rem) {
+                    acc0 = fma(v2[e].x, s2[e], acc0);
+                    acc1 = fma(v2[e].y, s2[e], acc1);
+                }
         }
         __syncthreads();
     }
@@ -377,10 +392,12 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         if (r0ok) dst[row] = q0;
         if (r1ok) dst[row + 1] = q1;
         if (!last_cta(P.tickets + T_FWD_RB + blockIdx.x, ncg)) return;
+        TR_MARK(2);
         q0 = 0.0; q1 = 0.0;
         sum_parts(P.qpart, (int64_t)FWD_GRPC * m, ncg, row, r0ok, r1ok, q0, q1);
     } else {
         if (!last_cta(P.tickets + T_FWD_RB + blockIdx.x, gridDim.y)) return;
+        TR_MARK(2);
         sum_parts(P.qpart, m, CCn, row, r0ok, r1ok, q0, q1);
     }
     if (P.qp && P.colscale) {                                   // Q~ = D M D: row scaling
@@ -479,8 +496,10 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         if (threadIdx.x < KT) P.lsp[(int64_t)blockIdx.x * KT + threadIdx.x] = Ssum[threadIdx.x];
     }
     // ---- global tail: the Armijo decision (ITER) or f(x) (SETUP)
+    TR_MARK(3);
+    TR_FLUSH(4, 24, 0);
     if (!last_cta(P.tickets + T_FWD_ALL, gridDim.x)) return;
-    TR_MARK(2);
+    TR_MARK(4);
     reduce_parts(P.lsp, gridDim.x, KT, ntr, [](int) { return 0; }, lval, FWD_SUB, stash, Ssum);
     reduce_sep(P, ntr, lval, FWD_SUB, stash, sepv);
     if (threadIdx.x != 0) return;
@@ -499,8 +518,8 @@ __global__ void __launch_bounds__(NT, MINB) k_fwd(Prob P, int mode, const double
         quad_values(P, C, Ssum, quad);
         armijo_decide(P, C, quad, sp);
     }
-    TR_MARK(3);
-    TR_FLUSH(4, 14, 0);
+    TR_MARK(5);
+    TR_FLUSH(6, 14, 0);
 }
 
 // Host-driven trial batches (stall continuation) and the op_trials entry:

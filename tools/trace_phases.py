@@ -99,12 +99,29 @@ for kd, nm in names.items():
     med["launches"] = len(per)
     med["ctas"] = per[len(per) // 2]["ctas"]
     out["kernels"][nm] = med
-# global tails: k_fwd / k_dir last-CTA records (entry of the tail -> decision done)
-for kd, nm in ((14, "k_fwd_tail"), (15, "k_dir_tail")):
+# k_fwd tails: row-block finisher (kid 24: [entry, stream end, row-block ticket won, q + trial sums done]) and
+# the global finisher (kid 14: [.., global ticket won, Armijo done]); k_dir global tail (kid 15: [.., ticket, done])
+idx = np.nonzero(kid == 24)[0]
+if idx.size:
+    out["kernels"]["k_fwd_rowblock_tail"] = {"work_us_median": float(np.median((t[idx, 3] - t[idx, 2]) / 1e3)),
+                                             "records": int(idx.size)}
+idx = np.nonzero(kid == 14)[0]
+if idx.size:
+    out["kernels"]["k_fwd_tail"] = {"rowblock_work_us_median": float(np.median((t[idx, 3] - t[idx, 2]) / 1e3)),
+                                    "ticket_us_median": float(np.median((t[idx, 4] - t[idx, 3]) / 1e3)),
+                                    "global_work_us_median": float(np.median((t[idx, 5] - t[idx, 4]) / 1e3)),
+                                    "launches": int(idx.size)}
+idx = np.nonzero(kid == 15)[0]
+if idx.size:
+    out["kernels"]["k_dir_tail"] = {"tail_us_median": float(np.median((t[idx, 3] - t[idx, 2]) / 1e3)),
+                                    "launches": int(idx.size)}
+# launch ends of k_fwd / k_dir: their global tails (the i-th tail record belongs to the i-th launch)
+for kd, nm, col in ((14, "k_fwd", 5), (15, "k_dir", 3)):
     idx = np.nonzero(kid == kd)[0]
-    if idx.size:
-        out["kernels"][nm] = {"tail_us_median": float(np.median((t[idx, 3] - t[idx, 2]) / 1e3)),
-                              "launches": int(idx.size)}
+    spans_k = [i for i, sp in enumerate(allspans) if sp[2] == nm]
+    for i, rec in zip(spans_k, idx):
+        s0, e0, n0 = allspans[i]
+        allspans[i] = (s0, max(e0, t[rec, col]), n0)
 # Gram tail of the last CTA (kid 11): level-1 ticket | level-1 reduce | level-2 ticket | level-2 reduce | Alg. 3
 idx = np.nonzero(kid == 11)[0]
 if idx.size:
