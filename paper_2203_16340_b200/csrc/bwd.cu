@@ -879,6 +879,219 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wd(Prob P, int mode, con
     TR_FLUSH(6, 3, (int)ncl);
 }
 
+// ---------------------------------------------------------------- k_bwd_wo (short columns, overlapped epilogue)
+// k_bwd_wd's dynamic column units, with the epilogue cut into mini-tiles of MT
+// columns run by the warp that completes a mini-tile's last unit (a shared
+// counter per mini-tile) right away, while the other warps keep streaming: the
+// epilogue of its columns (one lane per column; the two halves of a split
+// operator in turn) into a warp-private tile, and the mini-tile's masked-Gram
+// partial into shared memory; the CTA sums the partials in mini-tile order.  The dependent loads of the epilogue then overlap the other
+// warps' column streams instead of following them (k_bwd_wd: 14.6 us of its
+// 142 us at the C4 shape).  A partial does not depend on the warp that computes
+// it: deterministic.  BWDW_OVL selects it over k_bwd_wd (A/B).
+#ifndef BWDW_OVL
+#define BWDW_OVL 1
+#endif
+constexpr int MT = 32;                          // columns per epilogue mini-tile
+__global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wo(Prob P, int mode, const double* rvec, double* gout,
+                                                         int mpad, int cpad, int pstride)
+{
+    Ctrl* C = P.ctrl;
+    if (mode == BWD_ITER && halted(C)) return;
+    extern __shared__ __align__(16) double smw[];
+    TR_DECL
+    const int nw = NT / 32, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nbm = 2 * P.mh + 1;
+    const int nmt_max = (cpad + MT - 1) / MT;
+    double* rs = smw;                                           // r' [mpad]; later the tail's reduce buffer
+    double* dots = smw + mpad;                                  // [cpad]
+    double* wtile = dots + cpad + (int64_t)w * MT * (nbm + 1);  // this warp's [MT][nbm] rows, then mk[MT]
+    double* part = dots + cpad + (int64_t)nw * MT * (nbm + 1);  // [2 nmt_max][pstride] mini-tile partials
+    int* mt_done = reinterpret_cast<int*>(part + (int64_t)2 * nmt_max * pstride);   // [nmt_max]
+    __shared__ double red[NT / 32 * BWD_NB];
+    __shared__ double stash[NT];
+    __shared__ double Gs[MAXE + MAXH + 2];
+    __shared__ int s_next;
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int64_t m = P.m, ld = P.ld, ncols = P.ncols;
+    const int64_t j0 = (int64_t)cta * ncols / G, j1 = (int64_t)(cta + 1) * ncols / G;
+    const int64_t i0 = (int64_t)cta * m / G, i1 = (int64_t)(cta + 1) * m / G;
+    const bool iter = mode == BWD_ITER;
+    const int rsel = mode == BWD_PLAIN ? 0 : C->rsel;
+    const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
+    double* rnext = P.rbuf[rsel ^ 1];
+    const double alpha = iter ? C->alpha : 0.0;
+    const int ccount = (int)(j1 - j0);
+    const int nmt = (ccount + MT - 1) / MT;
+    if (threadIdx.x == 0) s_next = 0;
+    for (int i = threadIdx.x; i < nmt; i += NT) mt_done[i] = 0;
+    for (int64_t i = threadIdx.x; i < m; i += NT) {
+        double r = rcur[i];
+        if (iter) {
+            r = fma(alpha, P.q[i], r);                          // carried residual (R13)
+            if (i >= i0 && i < i1) rnext[i] = r;
+        }
+        rs[i] = r;
+    }
+    __syncthreads();
+    TR_MARK(1);
+    const bool epi = mode != BWD_PLAIN;
+    EpiCtx E;
+    if (epi) epi_init(P, C, mode, E);                           // first needed after a warp's first mini-tile
+    const bool gram = epi && E.gram;
+    const int nb = epi ? E.nb : 1;
+    const int ne = nb * (nb + 1) / 2;
+    const int ntot = gram ? ne + (P.screen_full ? E.nh : 0) : 0;
+    // Gram entry -> basis pair for this lane's entries e = lane + 32 k (upper triangle, row-major,
+    // then ||y_i||^2 with b = 255); registers for k < 4, computed on the fly beyond
+    auto entry = [&](int e, int& aa, int& bb) {
+        if (e < ne) {
+            int rem = e;
+            aa = 0;
+            while (rem >= nb - aa) { rem -= nb - aa; ++aa; }
+            bb = aa + rem;
+        } else {
+            aa = E.nh + (e - ne);
+            bb = 255;
+        }
+    };
+    int eaa[4], ebb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) entry(lane + 32 * q, eaa[q], ebb[q]);
+    const int nunits = (ccount + WCOL - 1) / WCOL;
+    const int nvg = P.split ? 2 : 1;
+    double gmax = 0.0, cnt = 0.0;
+    double* mkw = wtile + MT * nbm;
+    // epilogue + Gram partial of mini-tile i (its dots are complete); whole warp
+    auto do_mt = [&](int i) {
+        const int c0 = i * MT, cn = ccount - c0 < MT ? ccount - c0 : MT;
+        for (int vv = 0; vv < nvg; ++vv) {
+            double* tr = wtile + lane * nbm;
+            if (lane < cn) {
+                const int jj = c0 + lane;
+                const int64_t j = j0 + jj;
+                const double dot = dots[jj];
+                double dval = vv ? -dot : dot;
+                if (P.colscale) dval = P.colscale[j] * dot;
+                epilogue_var(P, C, E, j + vv * ncols, dval, tr, mkw + lane, gmax, cnt);
+            } else if (gram) {
+                for (int b = 0; b < nb; ++b) tr[b] = 0.0;
+                mkw[lane] = 0.0;
+            }
+            __syncwarp();
+            if (gram) {
+                double* po = part + (int64_t)(i * nvg + vv) * pstride;
+                for (int e = lane; e < ntot; e += 32) {
+                    int aa, bb;
+                    if (e < 128) {
+                        const int q = e >> 5;
+                        aa = q == 0 ? eaa[0] : q == 1 ? eaa[1] : q == 2 ? eaa[2] : eaa[3];
+                        bb = q == 0 ? ebb[0] : q == 1 ? ebb[1] : q == 2 ? ebb[2] : ebb[3];
+                    } else {
+                        entry(e, aa, bb);
+                    }
+                    double sacc = 0.0;
+                    if (bb != 255) {
+                        for (int r0 = 0; r0 < MT; r0 += 8) {
+                            double m8[8], a8[8], b8[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                m8[q] = mkw[r0 + q];
+                                a8[q] = wtile[(r0 + q) * nbm + aa];
+                                b8[q] = wtile[(r0 + q) * nbm + bb];
+                            }
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (m8[q] != 0.0) sacc = fma(a8[q], b8[q], sacc);
+                        }
+                    } else {
+                        for (int r0 = 0; r0 < MT; r0 += 8) {
+                            double a8[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) a8[q] = wtile[(r0 + q) * nbm + aa];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) sacc = fma(a8[q], a8[q], sacc);
+                        }
+                    }
+                    po[e] = sacc;
+                }
+            }
+            __syncwarp();                                       // the tile rows are rewritten next
+        }
+    };
+    for (;;) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&s_next, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= nunits) break;
+        const int64_t jg = j0 + (int64_t)u * WCOL;
+        const int nc = ccount - u * WCOL < WCOL ? ccount - u * WCOL : WCOL;
+        double acc[WCOL];
+#pragma unroll
+        for (int c = 0; c < WCOL; ++c) acc[c] = 0.0;
+        const double* M0 = P.M + jg * ld;
+        switch (nc) {
+#if BWDW_WCOL > 4
+            case 8: warp_col_dots<8>(M0, ld, m, rs, acc); break;
+            case 7: warp_col_dots<7>(M0, ld, m, rs, acc); break;
+            case 6: warp_col_dots<6>(M0, ld, m, rs, acc); break;
+            case 5: warp_col_dots<5>(M0, ld, m, rs, acc); break;
+#endif
+            case 4: warp_col_dots<4>(M0, ld, m, rs, acc); break;
+            case 3: warp_col_dots<3>(M0, ld, m, rs, acc); break;
+            case 2: warp_col_dots<2>(M0, ld, m, rs, acc); break;
+            default: warp_col_dots<1>(M0, ld, m, rs, acc); break;
+        }
+#pragma unroll
+        for (int c = 0; c < WCOL; ++c)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        if (lane < nc) {
+            double dot = acc[0];
+#pragma unroll
+            for (int c = 1; c < WCOL; ++c)
+                if (lane == c) dot = acc[c];
+            dots[u * WCOL + lane] = dot;
+        }
+        __syncwarp();
+        const int mt = (u * WCOL) / MT;
+        int prev = 0;
+        if (lane == 0) {                                        // release the unit to its mini-tile
+            __threadfence_block();
+            prev = atomicAdd(&mt_done[mt], 1);
+            __threadfence_block();
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        const int cmt = ccount - mt * MT < MT ? ccount - mt * MT : MT;
+        if (epi && prev + 1 == (cmt + WCOL - 1) / WCOL) do_mt(mt);   // this warp completed the mini-tile
+    }
+    TR_MARK(2);
+    TR_MARK(3);
+    __syncthreads();
+    TR_MARK(4);
+    if (!epi) {
+        for (int t = threadIdx.x; t < ccount * nvg; t += NT) {
+            const int jj = t % ccount, vv = t / ccount;
+            const int64_t j = j0 + jj;
+            const double dot = dots[jj];
+            double dval = vv ? -dot : dot;
+            if (P.colscale) dval = P.colscale[j] * dot;
+            gout[j + vv * ncols] = dval;
+        }
+        return;
+    }
+    if (!gram) return;
+    double* out = P.gram_part + (int64_t)cta * GRAM_STRIDE;
+    for (int e = threadIdx.x; e < ntot; e += NT) {              // mini-tile partials in mini-tile order
+        double sacc = 0.0;
+        for (int k = 0; k < nmt * nvg; ++k) sacc += part[(int64_t)k * pstride + e];
+        out[e] = sacc;
+    }
+    gram_tail_after(P, C, E, gmax, cnt, red, rs, mpad < 4096 ? mpad : 4096, stash, Gs);
+    TR_MARK(5);
+    TR_FLUSH(6, 3, ccount);
+}
+
 // ---------------------------------------------------------------- TMA / mbarrier helpers (k_qepi_t, k_qepi_d)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt)
@@ -1799,6 +2012,25 @@ void launch_bwd(const Prob& P, cudaStream_t st, int mode, const double* rvec, do
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_wd, NT, smd);
             occ_d = o;
             occ_dsm = smd;
+        }
+        if (BWDW_OVL && cmax >= 2 * MT) {                       // mini-tiles pay off from 2 per CTA (C1: k_bwd_wd)
+            const int nmt_max = (cpad + MT - 1) / MT;
+            const int pst = nbm * (nbm + 1) / 2 + P.mh;             // Gram entries + full norms for m_hist
+            const size_t smo = sizeof(double) * ((size_t)mpad + cpad + (size_t)(NT / 32) * MT * (nbm + 1) +
+                                                 (size_t)2 * nmt_max * pst) + sizeof(int) * (size_t)nmt_max;
+            static size_t occ_osm = 0;
+            static int occ_o = 0;
+            if (smo <= (size_t)BWD_SMEM_MAX && smo != occ_osm) {
+                cudaFuncSetAttribute(k_bwd_wo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smo);
+                int o = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_bwd_wo, NT, smo);
+                occ_o = o;
+                occ_osm = smo;
+            }
+            if (smo == occ_osm && occ_o >= BWDWD_MINB) {
+                k_bwd_wo<<<Gd, NT, smo, st>>>(P, mode, rvec, gout, mpad, cpad, pst);
+                return;
+            }
         }
         if (BWDW_DEFER && smd == occ_dsm && occ_d >= BWDWD_MINB) {
             k_bwd_wd<<<Gd, NT, smd, st>>>(P, mode, rvec, gout, mpad, cpad);

@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round 2 (session 2): k_bwd_wd at 3 CTAs/SM (one epilogue tile per CTA at C4) vs 2
+set -u
+O=gpurun_out/r02y; mkdir -p $O
+for v in trace trace_wd3; do
+  for sh in c2 c4; do
+    timeout 600 python tools/_prof_with_lib.py tools/_var/$v/liblbfgsb.so tools/trace_phases.py $sh >> $O/trace_$v.jsonl 2>> $O/trace.err
+  done
+done
+for i in 1 2; do
+  for v in default wd3; do
+    if [ $v = default ]; then L=paper_2203_16340_b200/liblbfgsb.so; else L=tools/_var/$v/liblbfgsb.so; fi
+    for sh in c2 c4 c1; do
+      LB_LIB=$v timeout 600 python tools/_prof_with_lib.py $L tools/ab_solve.py $sh 7 >> $O/ab_solve.log 2>&1
+    done
+  done
+done
+echo done > $O/done
