@@ -1,0 +1,145 @@
+"""Short-column backward GEMV variants against the CPU oracle (-m gpu).
+
+m < 2048 rows selects the short-column kernels (bwd.cu launch_bwd):
+  * k_bwd_wo when a CTA owns >= 64 columns (C4's 1000 x 100000 operator):
+    dynamic 4-column units per warp, the epilogue in 32-column mini-tiles run
+    by the warp that completes them, Gram partials summed in mini-tile order;
+  * k_bwd_wd below that (C1).
+The unit -> warp and mini-tile -> warp assignments are dynamic (shared-memory
+counters), so besides oracle parity these tests check that the results are
+bitwise reproducible run to run.  Tolerances are those of test_gpu_parity.py
+(DESIGN.md section 6)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2203_16340_b200 as lb
+    lb.load()
+    return lb
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def _solve(lb, prob, opts=None, m_hist=5):
+    M = lb.colmajor(prob.M)
+    b = None if prob.b is None else _cuda(prob.b)
+    c = None if prob.c is None else _cuda(prob.c)
+    cs = None if prob.colscale is None else _cuda(prob.colscale)
+    obj = lb.LSQObjective(M, b=b, c=c, delta=prob.delta, colscale=cs, split=prob.split)
+    lo = None if prob.lower is None else _cuda(prob.lower)
+    up = None if prob.upper is None else _cuda(prob.upper)
+    s = lb.Solver(prob.nvars, m_hist, lower=lo, upper=up, opts=opts or lb.Options())
+    x = torch.zeros(prob.nvars, dtype=torch.float64, device="cuda")
+    r = s.solve(obj, x)
+    return r, x.cpu().numpy()
+
+
+def _nnls_pos(m, n, seed):
+    """Box-constrained LSQ 0 <= x <= 0.05 on the NNLS Gaussian data: with n >> m
+    the plain NNLS fits b exactly (f* = 0, where a relative f test is void); the
+    upper bound keeps f* > 0 and puts variables on both bounds."""
+    import synth
+    prob = synth.nnls_gaussian(m, n, seed)
+    prob.upper = np.full(n, 0.05)
+    return prob
+
+
+def _oracle(orc, prob, opts=None, m_hist=5):
+    P = orc.LSQ(prob.M, b=prob.b, c=prob.c, delta=prob.delta, colscale=prob.colscale, split=prob.split)
+    return orc.minimize_lsq(P, l=prob.lower, u=prob.upper, m_hist=m_hist, opts=opts or orc.Options())
+
+
+@pytest.mark.parametrize("m,n", [(1000, 30000), (999, 25001), (63, 40000), (2047, 20000)])
+def test_gemvt_parity_short_columns(lb, orc, m, n):
+    """g = M^T r (BWD_PLAIN through k_bwd_wo) element by element, ragged m and n."""
+    rng = np.random.default_rng(m + 3 * n)
+    A = rng.standard_normal((m, n))
+    r = rng.standard_normal(m)
+    obj = lb.LSQObjective(lb.colmajor(A))
+    g = torch.empty(n, dtype=torch.float64, device="cuda")
+    lb.op_gemvt(obj, _cuda(r), g)
+    ref = orc.matvec_t(A, r)
+    assert np.all(np.abs(g.cpu().numpy() - ref) <= 1e-12 * (np.abs(A).T @ np.abs(r)))
+
+
+def test_gemvt_short_columns_split_and_colscale(lb, orc):
+    rng = np.random.default_rng(77)
+    m, n = 700, 26000
+    A = rng.standard_normal((m, n))
+    r = rng.standard_normal(m)
+    bound = np.abs(A).T @ np.abs(r)
+    gt = orc.matvec_t(A, r)
+    obj = lb.LSQObjective(lb.colmajor(A), split=True)
+    g = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    lb.op_gemvt(obj, _cuda(r), g)
+    gg = g.cpu().numpy()
+    assert np.array_equal(gg[:n], -gg[n:])
+    assert np.all(np.abs(gg[:n] - gt) <= 1e-12 * bound)
+    w = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    obj2 = lb.LSQObjective(lb.colmajor(A), colscale=_cuda(w))
+    g2 = torch.empty(n, dtype=torch.float64, device="cuda")
+    lb.op_gemvt(obj2, _cuda(r), g2)
+    assert np.all(np.abs(g2.cpu().numpy() - w * gt) <= 1e-12 * bound)
+
+
+@pytest.mark.parametrize("m,n,seed", [(700, 40000, 61), (1000, 30011, 62)])
+def test_nnls_end_to_end_short_columns(lb, orc, m, n, seed):
+    prob = _nnls_pos(m, n, seed)
+    r, x = _solve(lb, prob)
+    ro = _oracle(orc, prob)
+    assert r.status == lb.CONVERGED and ro.status == orc.CONVERGED
+    assert r.pg_inf <= 1e-6 and ro.pg_inf <= 1e-6
+    assert abs(r.f - ro.f) <= 1e-8 * abs(ro.f)
+    assert np.all(x >= 0.0)
+
+
+def test_first_iterations_match_oracle_short_columns(lb, orc):
+    """Trajectory parity on k_bwd_wo (1000 x 30000): f to 1e-12 and x to 1e-10
+    of its magnitude after k = 1..4 iterations."""
+    prob = _nnls_pos(1000, 30000, 63)
+    for k in range(1, 5):
+        r, x = _solve(lb, prob, opts=lb.Options(max_iters=k, tol=1e-12))
+        ro = _oracle(orc, prob, opts=orc.Options(max_iters=k, tol=1e-12))
+        assert r.iters == ro.iters == k
+        assert abs(r.f - ro.f) <= 1e-12 * abs(ro.f)
+        assert np.max(np.abs(x - ro.x)) <= 1e-10 * max(np.max(np.abs(ro.x)), 1e-300)
+
+
+def test_lasso_split_short_columns(lb, orc):
+    """Split operator [A, -A] on k_bwd_wo (both halves of a mini-tile's columns):
+    the first 10 iterations against the oracle's (a full lasso solve takes the
+    oracle minutes at this size)."""
+    import synth
+    prob = synth.lasso_split(400, 20000, 64)
+    r, x = _solve(lb, prob, opts=lb.Options(max_iters=10, tol=1e-12))
+    ro = _oracle(orc, prob, opts=orc.Options(max_iters=10, tol=1e-12))
+    assert r.iters == ro.iters == 10
+    assert abs(r.f - ro.f) <= 1e-10 * abs(ro.f)
+    assert np.max(np.abs(x - ro.x)) <= 1e-8 * max(np.max(np.abs(ro.x)), 1e-300)
+    n = prob.ncols
+    assert np.max(x[:n] * x[n:]) <= 1e-12
+
+
+@pytest.mark.parametrize("m_hist", [1, 5, 9])
+def test_short_columns_bitwise_reproducible(lb, m_hist):
+    """Dynamic unit / mini-tile scheduling: repeated solves (graph and eager,
+    history lengths whose Gram entries span one to four per-lane registers and
+    beyond) are bitwise identical."""
+    import synth
+    prob = synth.nnls_gaussian(800, 33000, 65)
+    out = []
+    for opts in (lb.Options(), lb.Options(), lb.Options(use_graph=False)):
+        r, x = _solve(lb, prob, opts=opts, m_hist=m_hist)
+        out.append((x, r.f, r.iters))
+    for x, f, it in out[1:]:
+        assert np.array_equal(x, out[0][0]) and f == out[0][1] and it == out[0][2]

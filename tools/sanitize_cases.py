@@ -45,6 +45,16 @@ def lasso():
     print("lasso", s.solve(obj, x).status_name)
 
 
+def c4split():
+    p = synth.lasso_split(400, 20000, 64)          # split operator on k_bwd_wo (>= 64 columns per CTA)
+    obj = lb.LSQObjective(lb.colmajor(p.M), b=torch.from_numpy(p.b).cuda(), c=torch.from_numpy(p.c).cuda(),
+                          delta=p.delta, split=True)
+    s = lb.Solver(p.nvars, 5, lower=torch.zeros(p.nvars, dtype=torch.float64, device="cuda"),
+                  opts=lb.Options(max_iters=30))
+    x = torch.zeros(p.nvars, dtype=torch.float64, device="cuda")
+    print("c4split", s.solve(obj, x).status_name)
+
+
 def al():
     p = synth.svm_dual_linear(400, 20, 6)
     M = lb.colmajor(p.M)
