@@ -311,6 +311,9 @@ __device__ __forceinline__ void epi_init(const Prob& P, const Ctrl* C, int mode,
     }
 }
 
+#ifndef RECUR_WARP
+#define RECUR_WARP 1           // Alg. 3 of the k_bwd tails on one warp (0: thread 0, serial sums; A/B)
+#endif
 __device__ void gram_tail_after(const Prob& P, Ctrl* C, const EpiCtx& E, double gmax, double cnt,
                                 double* red, double* buf, int bufn, double* stash, double* Gs);
 
@@ -360,9 +363,15 @@ __device__ void gram_tail_after(const Prob& P, Ctrl* C, const EpiCtx& E, double 
         if (P.p2p) p2p_push(P, XS_GRAM, off_gram(P), GRAM_STRIDE);
         return;
     }
+#if RECUR_WARP
     if (threadIdx.x >= 32) return;
     if (E.iter && threadIdx.x == 0) C->rsel = E.rsel ^ 1;
     recur_decide_warp(P, C, Gs, nh, 0, E.tol, E.k);
+#else
+    if (threadIdx.x != 0) return;
+    if (E.iter) C->rsel = E.rsel ^ 1;
+    recur_decide_tk(P, C, Gs, nh, 0, E.tol, E.k);
+#endif
     TR_MARK(5);
     TR_FLUSH(6, 11, G);
 }
@@ -420,19 +429,21 @@ __global__ void __launch_bounds__(NTB, 1) k_bwd_s(Prob P, int mode, const double
     const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
     double* rnext = P.rbuf[rsel ^ 1];
     const double alpha = iter ? C->alpha : 0.0;
-    // r' once per CTA.  The loads of a batch of 8 rows are issued before any store: a
+    // r' once per CTA.  The loads of a batch of RPB rows are issued before any store: a
     // global store between them (rnext may alias rcur / q for the compiler) serialised
-    // the 2 x 39 L2 round trips per thread (7% of the kernel's stall samples in ncu)
-    for (int64_t ib = threadIdx.x; ib < m; ib += 8 * (int64_t)NTB) {
-        double rv[8], qv[8];
+    // the 2 x 39 L2 round trips per thread (7% of the kernel's stall samples in ncu);
+    // RPB = 20 covers C2's 20000 rows in two batches
+    constexpr int RPB = 20;
+    for (int64_t ib = threadIdx.x; ib < m; ib += RPB * (int64_t)NTB) {
+        double rv[RPB], qv[RPB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < RPB; ++u) {
             const int64_t i = ib + (int64_t)u * NTB;
             rv[u] = i < m ? __ldcg(rcur + i) : 0.0;
             qv[u] = (iter && i < m) ? __ldcg(P.q + i) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < RPB; ++u) {
             const int64_t i = ib + (int64_t)u * NTB;
             if (i < m) rs[i] = iter ? fma(alpha, qv[u], rv[u]) : rv[u];     // carried residual (R13)
         }
@@ -627,13 +638,25 @@ __global__ void __launch_bounds__(NT, BWDW_MINB) k_bwd_w(Prob P, int mode, const
     const double* rcur = mode == BWD_PLAIN ? rvec : P.rbuf[rsel];
     double* rnext = P.rbuf[rsel ^ 1];
     const double alpha = iter ? C->alpha : 0.0;
-    for (int64_t i = threadIdx.x; i < m; i += NT) {
-        double r = rcur[i];
-        if (iter) {
-            r = fma(alpha, P.q[i], r);                          // carried residual (R13)
-            if (i >= i0 && i < i1) rnext[i] = r;
+    for (int64_t ib = threadIdx.x; ib < m; ib += 8 * (int64_t)NT) {    // 8 rows' loads before any store
+        double rv[8], qv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = ib + (int64_t)u * NT;
+            rv[u] = i < m ? rcur[i] : 0.0;
+            qv[u] = (iter && i < m) ? P.q[i] : 0.0;
         }
-        rs[i] = r;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = ib + (int64_t)u * NT;
+            if (i >= m) continue;
+            double r = rv[u];
+            if (iter) {
+                r = fma(alpha, qv[u], r);                       // carried residual (R13)
+                if (i >= i0 && i < i1) rnext[i] = r;
+            }
+            rs[i] = r;
+        }
     }
     const bool epi = mode != BWD_PLAIN;
     EpiCtx E;
@@ -775,13 +798,25 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wd(Prob P, int mode, con
     double* rnext = P.rbuf[rsel ^ 1];
     const double alpha = iter ? C->alpha : 0.0;
     if (threadIdx.x == 0) s_next = 0;
-    for (int64_t i = threadIdx.x; i < m; i += NT) {
-        double r = rcur[i];
-        if (iter) {
-            r = fma(alpha, P.q[i], r);                          // carried residual (R13)
-            if (i >= i0 && i < i1) rnext[i] = r;
+    for (int64_t ib = threadIdx.x; ib < m; ib += 8 * (int64_t)NT) {    // 8 rows' loads before any store
+        double rv[8], qv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = ib + (int64_t)u * NT;
+            rv[u] = i < m ? rcur[i] : 0.0;
+            qv[u] = (iter && i < m) ? P.q[i] : 0.0;
         }
-        rs[i] = r;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = ib + (int64_t)u * NT;
+            if (i >= m) continue;
+            double r = rv[u];
+            if (iter) {
+                r = fma(alpha, qv[u], r);                       // carried residual (R13)
+                if (i >= i0 && i < i1) rnext[i] = r;
+            }
+            rs[i] = r;
+        }
     }
     __syncthreads();
     TR_MARK(1);
@@ -925,13 +960,25 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wo(Prob P, int mode, con
     const int nmt = (ccount + MT - 1) / MT;
     if (threadIdx.x == 0) s_next = 0;
     for (int i = threadIdx.x; i < nmt; i += NT) mt_done[i] = 0;
-    for (int64_t i = threadIdx.x; i < m; i += NT) {
-        double r = rcur[i];
-        if (iter) {
-            r = fma(alpha, P.q[i], r);                          // carried residual (R13)
-            if (i >= i0 && i < i1) rnext[i] = r;
+    for (int64_t ib = threadIdx.x; ib < m; ib += 8 * (int64_t)NT) {    // 8 rows' loads before any store
+        double rv[8], qv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = ib + (int64_t)u * NT;
+            rv[u] = i < m ? rcur[i] : 0.0;
+            qv[u] = (iter && i < m) ? P.q[i] : 0.0;
         }
-        rs[i] = r;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = ib + (int64_t)u * NT;
+            if (i >= m) continue;
+            double r = rv[u];
+            if (iter) {
+                r = fma(alpha, qv[u], r);                       // carried residual (R13)
+                if (i >= i0 && i < i1) rnext[i] = r;
+            }
+            rs[i] = r;
+        }
     }
     __syncthreads();
     TR_MARK(1);
