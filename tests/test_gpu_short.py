@@ -143,3 +143,29 @@ def test_short_columns_bitwise_reproducible(lb, m_hist):
         out.append((x, r.f, r.iters))
     for x, f, it in out[1:]:
         assert np.array_equal(x, out[0][0]) and f == out[0][1] and it == out[0][2]
+
+
+@pytest.mark.parametrize("m,n", [(16, 2_000_000), (16, 6_500_000)])
+def test_short_column_fallbacks(lb, orc, m, n):
+    """Very many short columns: the mini-tile partials of k_bwd_wo no longer fit
+    shared memory (2 M columns: k_bwd_wd), then neither do k_bwd_wd's column
+    dots (6.5 M columns: k_bwd_w, round 1's per-warp-epilogue kernel).  GEMV^T
+    element by element, and the first 3 iterations against the oracle."""
+    import synth
+    rng = np.random.default_rng(m + n)
+    A = np.asfortranarray(rng.standard_normal((m, n)) / np.sqrt(m))
+    r = rng.standard_normal(m)
+    obj = lb.LSQObjective(lb.colmajor(A))
+    g = torch.empty(n, dtype=torch.float64, device="cuda")
+    lb.op_gemvt(obj, _cuda(r), g)
+    assert np.all(np.abs(g.cpu().numpy() - orc.matvec_t(A, r)) <= 1e-12 * (np.abs(A).T @ np.abs(r)))
+    prob = synth.Problem("nnls", "fallback", A, b=rng.standard_normal(m), lower=np.zeros(n),
+                         upper=np.full(n, 0.05))
+    r3, x = _solve(lb, prob, opts=lb.Options(max_iters=3, tol=1e-12))
+    ro = _oracle(orc, prob, opts=orc.Options(max_iters=3, tol=1e-12))
+    assert r3.iters == ro.iters == 3
+    # f falls by ~10 orders of magnitude in 3 steps here (16 rows, millions of columns): its rounding
+    # floor is that of the carried residual, eps * f(x0) = eps * ||b||^2 / 2, so compare on that scale
+    f0 = 0.5 * float(prob.b @ prob.b)
+    assert abs(r3.f - ro.f) <= 1e-12 * f0
+    assert np.max(np.abs(x - ro.x)) <= 1e-10 * max(np.max(np.abs(ro.x)), 1e-300)
