@@ -51,6 +51,11 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# context for roofline.frac above 1: the copy peak counts read + write bytes, a read-dominated stream can
+# exceed it; the measured pure-read ceiling of this GPU type (a GEMV^T-shaped TMA stream of the C2 matrix,
+# tools/bw_probe.cu) is reported beside it
+READ_PROBE_GBS = 7170.0
+READ_PROBE_SRC = "profiles/r01_bw_probe.txt (seg_stream: 1.6 GB GEMV^T-shaped TMA column stream, 7.17 TB/s)"
 sys.path.insert(0, ROOT)
 
 M_ROWS, N_COLS, SEED, M_HIST, TOL = 20000, 10000, 2, 5, 1e-6
@@ -384,7 +389,7 @@ def measure_c2(args, with_cpu=True):
     bwd_avg_s = (bwd_ms / max(bwd_n, 1)) / 1e3
     achieved = bwd_bytes / bwd_avg_s / 1e9 if bwd_n else None
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "r01_kbwd_dram_bytes.json")
+    tfile = os.path.join(ROOT, "profiles", "r02b_kbwd_s_dram_bytes.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -396,7 +401,9 @@ def measure_c2(args, with_cpu=True):
                 "k_fwd_share_of_step": (fwd_ms / ms_p) if ms_p else None,
                 "events": f"CUDA events around every k_fwd / k_bwd launch of {args.steps} profiled steps "
                           f"({ms_p / args.steps:.3f} ms per step with the event nodes)",
-                "k_fwd_avg_launch_us": 1e3 * fwd_ms / max(fwd_n, 1)}
+                "k_fwd_avg_launch_us": 1e3 * fwd_ms / max(fwd_n, 1),
+                "read_probe_gbs": READ_PROBE_GBS, "frac_of_read_probe": (achieved / READ_PROBE_GBS) if achieved else None,
+                "read_probe_source": READ_PROBE_SRC}
     if fwd_n and nact:
         # k_fwd reads only the active columns: 8 m n_p + qpart / r / q vectors
         cols = nact / fwd_n
@@ -681,8 +688,11 @@ def run_c5(args) -> int:
                 "events": f"CUDA events around the {nloc} local k_bwd launches of every iteration of {kp} "
                           f"profiled steps ({ms_p / kp:.1f} ms per step with the event nodes)",
                 "share_of_step": (bwd_ms / kp) / (ms_p / kp) if ms_p else None,
-                "k_fwd_share_of_step": (fwd_ms / kp) / (ms_p / kp) if ms_p else None}
-        tfile = os.path.join(ROOT, "profiles", "r02_c5_kbwd_dram_bytes.json")
+                "k_fwd_share_of_step": (fwd_ms / kp) / (ms_p / kp) if ms_p else None,
+                "read_probe_gbs": READ_PROBE_GBS,
+                "frac_of_read_probe": (achieved / READ_PROBE_GBS) if achieved else None,
+                "read_probe_source": READ_PROBE_SRC}
+        tfile = os.path.join(ROOT, "profiles", "r02b_c5_kbwd_dram_bytes.json")
         if os.path.exists(tfile):
             tr = json.load(open(tfile))
             roof["traffic"] = tr.get("dram_bytes_per_launch")
