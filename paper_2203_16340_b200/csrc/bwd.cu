@@ -958,6 +958,7 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wo(Prob P, int mode, con
     const double alpha = iter ? C->alpha : 0.0;
     const int ccount = (int)(j1 - j0);
     const int nmt = (ccount + MT - 1) / MT;
+    LB_CHECK(ccount >= 1 && ccount <= cpad && nmt <= nmt_max);
     if (threadIdx.x == 0) s_next = 0;
     for (int i = threadIdx.x; i < nmt; i += NT) mt_done[i] = 0;
     for (int64_t ib = threadIdx.x; ib < m; ib += 8 * (int64_t)NT) {    // 8 rows' loads before any store
@@ -1028,6 +1029,7 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wo(Prob P, int mode, con
             __syncwarp();
             if (gram) {
                 double* po = part + (int64_t)(i * nvg + vv) * pstride;
+                LB_CHECK(i * nvg + vv < 2 * nmt_max && ntot <= pstride && nb <= nbm);
                 for (int e = lane; e < ntot; e += 32) {
                     int aa, bb;
                     if (e < 128) {
@@ -1098,10 +1100,12 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wo(Prob P, int mode, con
 #pragma unroll
             for (int c = 1; c < WCOL; ++c)
                 if (lane == c) dot = acc[c];
+            LB_CHECK(u * WCOL + lane < ccount);
             dots[u * WCOL + lane] = dot;
         }
         __syncwarp();
         const int mt = (u * WCOL) / MT;
+        LB_CHECK(mt < nmt);
         int prev = 0;
         if (lane == 0) {                                        // release the unit to its mini-tile
             __threadfence_block();

@@ -4,6 +4,7 @@
 #pragma once
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include "impl.cuh"
 
 namespace lb {
@@ -109,6 +110,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns()
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// ---- LB_CHECK (debug variant builds only): device-side bounds / invariant checks that trap;
+// compute-sanitizer's stand-in where it is not available.  The default library compiles none of this.
+#ifdef LB_CHECK_ON
+#define LB_CHECK(c) do { if (!(c)) { printf("LB_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); __trap(); } } while (0)
+#else
+#define LB_CHECK(c) do {} while (0)
+#endif
+
 // ---- LB_TRACE (A/B variant builds only, tools/trace_phases.py): per-CTA
 // phase timestamps (%globaltimer) appended as one record per CTA per launch.
 // The default library compiles none of this.
