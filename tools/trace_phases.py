@@ -99,6 +99,22 @@ for kd, nm in names.items():
     med["launches"] = len(per)
     med["ctas"] = per[len(per) // 2]["ctas"]
     out["kernels"][nm] = med
+# optional: per-CTA records of one mid-solve launch of a kernel (TRACE_DUMP=name), for placement analysis
+dump = os.environ.get("TRACE_DUMP")
+if dump:
+    kd = {v: k for k, v in names.items()}[dump]
+    idx = np.nonzero(kid == kd)[0]
+    launches, cur, seen = [], [], set()
+    for i in idx:
+        c = meta[i, 1]
+        if c in seen:
+            launches.append(cur); cur, seen = [], set()
+        cur.append(i); seen.add(c)
+    ln = launches[len(launches) // 2]
+    t0 = t[ln, 0].min()
+    recs = [{"cta": int(meta[i, 1]), "sm": int(meta[i, 2]), "aux": int(meta[i, 3]),
+             "t": [round((t[i, q] - t0) / 1e3, 3) for q in range(nmarks[kd])]} for i in ln]
+    out["dump"] = {"kernel": dump, "records": recs}
 # k_fwd tails: row-block finisher (kid 24: [entry, stream end, row-block ticket won, q + trial sums done]) and
 # the global finisher (kid 14: [.., global ticket won, Armijo done]); k_dir global tail (kid 15: [.., ticket, done])
 idx = np.nonzero(kid == 24)[0]
