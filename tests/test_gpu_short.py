@@ -169,3 +169,27 @@ def test_short_column_fallbacks(lb, orc, m, n):
     f0 = 0.5 * float(prob.b @ prob.b)
     assert abs(r3.f - ro.f) <= 1e-12 * f0
     assert np.max(np.abs(x - ro.x)) <= 1e-10 * max(np.max(np.abs(ro.x)), 1e-300)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_loopback_short_columns(lb, orc, P):
+    """Column sharding on the short-column kernel (>= 64 columns per CTA in every shard: k_bwd_wo, whose
+    Gram tail then writes the sharded pack): P logical ranks with the P2P exchange equal the copy exchange
+    bitwise, and reach the oracle's optimum."""
+    from test_gpu_sharded import _gather_x, _shards
+    prob = _nnls_pos(700, 80000, 66)
+    out = []
+    for p2p in (False, True):
+        sv, ob, xs, keep = _shards(lb, prob, P)
+        if p2p:
+            lb.p2p_connect_local(sv, prob.M.shape[0])
+        r = lb.solve_loopback(sv, ob, xs)
+        out.append((r, _gather_x(prob, P, xs)))
+    (r0, x0), (r1, x1) = out
+    assert r1.status == lb.CONVERGED and r1.pg_inf <= 1e-6
+    assert np.array_equal(x0, x1) and r0.f == r1.f and r0.iters == r1.iters
+    ro = _oracle(orc, prob)
+    assert ro.pg_inf <= 1e-6
+    # 80000 columns under the 0.05 bound still fit b almost exactly (f* ~ 1e-11): compare f on the scale of
+    # its rounding floor, that of the carried residual, eps * f(x0) = eps * ||b||^2 / 2
+    assert abs(r1.f - ro.f) <= 1e-12 * 0.5 * float(prob.b @ prob.b)
