@@ -1114,7 +1114,10 @@ __global__ void __launch_bounds__(NT, BWDWD_MINB) k_bwd_wo(Prob P, int mode, con
         }
         prev = __shfl_sync(0xffffffffu, prev, 0);
         const int cmt = ccount - mt * MT < MT ? ccount - mt * MT : MT;
-        if (epi && prev + 1 == (cmt + WCOL - 1) / WCOL) do_mt(mt);   // this warp completed the mini-tile
+        if (epi && prev + 1 == (cmt + WCOL - 1) / WCOL) {          // this warp completed the mini-tile
+            __syncwarp();                                       // lane 0's acquire before every lane's reads
+            do_mt(mt);
+        }
     }
     TR_MARK(2);
     TR_MARK(3);
