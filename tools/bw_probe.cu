@@ -24,6 +24,27 @@ __global__ void ldg_sum(const double2* __restrict__ a, size_t n2, double* out)
     if (s == 123.456) out[0] = s;
 }
 
+// the same with 256-bit loads (LDG.E.ENL2.256, sm_100a): half the load instructions per byte
+__device__ __forceinline__ void ld256cs(const double* p, double& a, double& b, double& c, double& d)
+{
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+template <int U>
+__global__ void ldg256_sum(const double* __restrict__ a, size_t n4, double* out)
+{
+    double s = 0.0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < n4; i += U * stride) {
+        double v[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ld256cs(a + 4 * (i + u * stride), v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += (v[u][0] + v[u][1]) + (v[u][2] + v[u][3]);
+    }
+    if (s == 123.456) out[0] = s;
+}
+
 // contiguous chunk per CTA (like a persistent column range)
 template <int U>
 __global__ void ldg_chunk(const double2* __restrict__ a, size_t n2, double* out)
@@ -290,6 +311,15 @@ int main(int argc, char** argv)
         rep(nm, timeit([&] { ldg_sum<8><<<sms * k, 256>>>(a2, n / 2, out); }, 10));
         snprintf(nm, 64, "ldg_chunk<8> grid=%dx%d tpb=256", sms, k);
         rep(nm, timeit([&] { ldg_chunk<8><<<sms * k, 256>>>(a2, n / 2, out); }, 10));
+    }
+    for (int k : {1, 2, 4}) {
+        char nm[64];
+        snprintf(nm, 64, "ldg256_sum<2> grid=%dx%d tpb=256", sms, k);
+        rep(nm, timeit([&] { ldg256_sum<2><<<sms * k, 256>>>(a, n / 4, out); }, 10));
+        snprintf(nm, 64, "ldg256_sum<4> grid=%dx%d tpb=256", sms, k);
+        rep(nm, timeit([&] { ldg256_sum<4><<<sms * k, 256>>>(a, n / 4, out); }, 10));
+        snprintf(nm, 64, "ldg256_sum<8> grid=%dx%d tpb=256", sms, k);
+        rep(nm, timeit([&] { ldg256_sum<8><<<sms * k, 256>>>(a, n / 4, out); }, 10));
     }
     rep("ldg_chunk<8> grid=148 tpb=512", timeit([&] { ldg_chunk<8><<<sms, 512>>>(a2, n / 2, out); }, 10));
     rep("ldg_chunk<16> grid=148 tpb=512", timeit([&] { ldg_chunk<16><<<sms, 512>>>(a2, n / 2, out); }, 10));
