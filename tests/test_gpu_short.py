@@ -1,4 +1,5 @@
-"""Short-column backward GEMV variants against the CPU oracle (-m gpu).
+"""Short-column backward GEMV variants against the CPU oracle (-m gpu), and the
+split / colscale forms of the long-column k_bwd_s.
 
 m < 2048 rows selects the short-column kernels (bwd.cu launch_bwd):
   * k_bwd_wo when a CTA owns >= 64 columns (C4's 1000 x 100000 operator):
@@ -193,3 +194,36 @@ def test_sharded_loopback_short_columns(lb, orc, P):
     # 80000 columns under the 0.05 bound still fit b almost exactly (f* ~ 1e-11): compare f on the scale of
     # its rounding floor, that of the carried residual, eps * f(x0) = eps * ||b||^2 / 2
     assert abs(r1.f - ro.f) <= 1e-12 * 0.5 * float(prob.b @ prob.b)
+
+
+# ---- the long-column k_bwd_s (m >= 2048) with the split and colscale operators (C3 / SVM forms)
+def test_gemvt_kbwd_s_split_and_colscale(lb, orc):
+    rng = np.random.default_rng(91)
+    m, n = 3000, 5001
+    A = rng.standard_normal((m, n))
+    r = rng.standard_normal(m)
+    bound = np.abs(A).T @ np.abs(r)
+    gt = orc.matvec_t(A, r)
+    g = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    lb.op_gemvt(lb.LSQObjective(lb.colmajor(A), split=True), _cuda(r), g)
+    gg = g.cpu().numpy()
+    assert np.array_equal(gg[:n], -gg[n:])
+    assert np.all(np.abs(gg[:n] - gt) <= 1e-12 * bound)
+    w = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    g2 = torch.empty(n, dtype=torch.float64, device="cuda")
+    lb.op_gemvt(lb.LSQObjective(lb.colmajor(A), colscale=_cuda(w)), _cuda(r), g2)
+    assert np.all(np.abs(g2.cpu().numpy() - w * gt) <= 1e-12 * bound)
+
+
+def test_lasso_split_kbwd_s_first_iterations(lb, orc):
+    """The C3 form on k_bwd_s: a split operator whose CTAs own 2 x 135 variables (two epilogue tiles);
+    10 iterations against the oracle's."""
+    import synth
+    prob = synth.lasso_split(3000, 20000, 92)
+    r, x = _solve(lb, prob, opts=lb.Options(max_iters=10, tol=1e-12))
+    ro = _oracle(orc, prob, opts=orc.Options(max_iters=10, tol=1e-12))
+    assert r.iters == ro.iters == 10
+    assert abs(r.f - ro.f) <= 1e-10 * abs(ro.f)
+    assert np.max(np.abs(x - ro.x)) <= 1e-8 * max(np.max(np.abs(ro.x)), 1e-300)
+    n = prob.ncols
+    assert np.max(x[:n] * x[n:]) <= 1e-12
