@@ -227,3 +227,22 @@ def test_lasso_split_kbwd_s_first_iterations(lb, orc):
     assert np.max(np.abs(x - ro.x)) <= 1e-8 * max(np.max(np.abs(ro.x)), 1e-300)
     n = prob.ncols
     assert np.max(x[:n] * x[n:]) <= 1e-12
+
+
+def test_svm_dual_al_short_columns(lb, orc):
+    """The C4 form (linear-SVM dual: colscale = y, 0 <= a <= C, y^T a = 0 through Alg. 4) on k_bwd_wo:
+    20000 samples, so the fused AL path's epilogue (ccoef E_k terms) runs in the mini-tiles."""
+    import synth
+    prob = synth.svm_dual_linear(20000, 20, 93)
+    M = lb.colmajor(prob.M)
+    obj = lb.LSQObjective(M, c=_cuda(prob.c), colscale=_cuda(prob.colscale))
+    s = lb.Solver(prob.nvars, 5, lower=_cuda(prob.lower), upper=_cuda(prob.upper), opts=lb.Options(tol=1e-6))
+    x = torch.zeros(prob.nvars, dtype=torch.float64, device="cuda")
+    r = s.al_solve(obj, x, E=_cuda(prob.E), e=prob.e)
+    P = orc.LSQ(prob.M, c=prob.c, colscale=prob.colscale, E=prob.E, e=prob.e)
+    ro = orc.al_solve(P, l=prob.lower, u=prob.upper, opts=orc.Options(tol=1e-6))
+    assert r.status == lb.CONVERGED and ro.status == orc.CONVERGED
+    assert r.violation_inf <= 1e-6
+    assert abs(r.f - ro.f) <= 1e-6 * abs(ro.f)
+    a = x.cpu().numpy()
+    assert np.all(a >= 0) and np.all(a <= 1.0)
